@@ -1,0 +1,244 @@
+/*
+ * vmsplat_b200 — C ABI of the B200-native per-frame VM/LOD splat path.
+ *
+ * Drop-in boundary for the reference package `vmsplat` (arXiv 2506.19415
+ * restatement).  The reference binds its native code through Python: the
+ * `vmsplat.kernels` wrappers (pkg/src/vmsplat/kernels/__init__.py:24-51)
+ * call the Cython core (pkg/src/vmsplat/kernels/_core.pyx), and
+ * `VmSession.render_frame` (pkg/src/vmsplat/runtime.py:436-489) strings the
+ * per-frame stages together in NumPy.  Every entry point below replaces one
+ * of those, as cited per function; the ctypes binding that plays the role of
+ * the reference's Cython module lives in paper_2506_19415_b200/_lib.py and
+ * is reproduced in INTEGRATION.md.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only.  Pointers marked [dev] are device (or
+ *    device-mapped pinned host) memory; [host] are host memory.
+ *  - `stream` is a cudaStream_t passed as void*; NULL = legacy stream.
+ *  - Every int32_t-returning call returns a VMS_* status; vms_last_error()
+ *    gives the thread-local message of the last failure.  Status codes map
+ *    onto the reference's exceptions (pkg/src/vmsplat/errors.py:1-26):
+ *    VMS_ERR_INVARIANT / VMS_ERR_RANGE -> InvariantViolation,
+ *    VMS_ERR_INVALID -> ValueError/DataError, VMS_ERR_CUDA -> RuntimeError.
+ *  - No hot-path allocation: callers size workspaces with the *_bytes
+ *    queries and own every buffer (kernels hold no state).
+ *  - Results are bit-exact with the reference for every integer/index output
+ *    (page-ID images, required lists, plans, sort orders); images are within
+ *    1e-3 max-abs in fast mode and FP64-faithful in exact mode.
+ */
+#ifndef VMSPLAT_B200_H
+#define VMSPLAT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VMS_OK 0
+#define VMS_ERR_INVALID 1
+#define VMS_ERR_RANGE 2
+#define VMS_ERR_CUDA 3
+#define VMS_ERR_NOMEM 4
+#define VMS_ERR_INVARIANT 5
+
+#define VMS_ABI_VERSION 1
+
+/* Camera for a kernel launch: render.Camera (pkg/src/vmsplat/render.py:47-101)
+ * reduced to the numbers the kernels use.  rot = quat_to_matrix(orientation),
+ * row-major, view = (p - pos) @ rot.  dot_mode selects the FP64 dot order
+ * matching the host BLAS (0 = fused fma chain, 1 = unfused), probed once per
+ * session. */
+typedef struct vms_camera {
+  double pos[3];
+  double rot[9];
+  double focal;
+  double half_w;
+  double half_h;
+  double near;
+  int32_t width;
+  int32_t height;
+  int32_t dot_mode;
+  int32_t pad_;
+} vms_camera;
+
+/* LOD thresholds (runtime.LodController.thresholds, runtime.py:99-121). */
+typedef struct vms_lod {
+  double thresholds[8];
+  int32_t count;
+  int32_t pad_;
+} vms_lod;
+
+/* Required-page list (runtime.RequiredList, runtime.py:46-60) in compacted
+ * form, ascending page id, written by the GPU into [dev]-mapped pinned host
+ * memory.  meta[0] = clipped triangles, meta[1] = required pages,
+ * meta[2] = largest out-of-range page id seen (0 = none). */
+typedef struct vms_required_out {
+  uint32_t* pid;
+  uint32_t* enc;
+  uint8_t* direct;
+  uint8_t* level;
+  uint32_t* meta;
+} vms_required_out;
+
+typedef struct vms_vis_args {
+  vms_camera cam;               /* the visibility camera (camera.scaled(vis_scale)) */
+  const double* verts;          /* [dev] (nv, 3) f64 proxy-mesh vertices */
+  const int32_t* faces;         /* [dev] (nf, 3) */
+  const uint32_t* face_page;    /* [dev] (nf,) page id per face, 0 = occluder */
+  uint32_t n_faces;
+  uint32_t page_count;
+  const uint32_t* link_off;     /* [dev] (P + 1,) CSR offsets (scene_io.py:163-165) */
+  const uint32_t* link_tgt;     /* [dev] link targets */
+  vms_lod lod;
+  uint32_t* id_image;           /* [dev] optional (h, w) page-ID image */
+  double* invz_image;           /* [dev] optional (h, w) 1/z image */
+  uint32_t* depth_out;          /* [dev] optional (P + 1,) encoded depths after links */
+  uint8_t* direct_out;          /* [dev] optional (P + 1,) direct flags */
+  vms_required_out out;
+  void* workspace;              /* [dev] vms_visibility_workspace_bytes() */
+} vms_vis_args;
+
+/* A run of <= 128 resident records: device-pool rows [row, row + count)
+ * carry gather indices [gather, gather + count) (runtime.gather_resident,
+ * runtime.py:377-390, without the gather copy). */
+typedef struct vms_chunk {
+  uint32_t row;
+  uint32_t gather;
+  uint32_t count;
+  uint32_t pad_;
+} vms_chunk;
+
+typedef struct vms_render_args {
+  vms_camera cam;
+  const float* pool;            /* [dev] (rows, 59) f32 record pool */
+  const vms_chunk* chunks;      /* [dev] chunk table */
+  uint32_t n_chunks;
+  uint32_t n_splats;            /* gather indices in use (resident records) */
+  uint32_t n_cap;               /* workspace splat capacity */
+  uint32_t m_cap;               /* workspace tile-instance capacity */
+  float* image;                 /* [dev] (h, w, 3) f32 output */
+  int32_t accumulate;           /* 1: blend over image's current content */
+  int32_t exact;                /* 1: FP64 blend (reference arithmetic) */
+  uint32_t* counters_out;       /* [host pinned] optional: n_kept, n_inst, overflow */
+  void* workspace;              /* [dev] vms_render_workspace_bytes() */
+  void* ev_sorted;              /* optional cudaEvent_t recorded after the depth sort */
+} vms_render_args;
+
+/* One planned page copy in bytes (runtime.execute_copies, runtime.py:362-374). */
+typedef struct vms_copy {
+  uint64_t src_offset;
+  uint64_t dst_offset;
+  uint64_t nbytes;
+} vms_copy;
+
+typedef struct vms_pagetable vms_pagetable;
+
+/* ---- library --------------------------------------------------------- */
+const char* vms_last_error(void);
+int32_t vms_abi_version(void);
+
+/* ---- kernel-level drop-ins (pkg/src/vmsplat/kernels/__init__.py) ------ */
+
+/* composite_splats (kernels/__init__.py:24-33, _core.pyx:24-78): blend n
+ * caller-ordered splats into image (h, w, 3) f32 in place.  n_instances is
+ * an upper bound on the 16x16-tile instances (sum over splats of the tiles
+ * their clamped box touches); a smaller true count is fine, a larger one
+ * fails with VMS_ERR_NOMEM and leaves image unchanged. */
+size_t vms_composite_workspace_bytes(int64_t n, int64_t n_instances, int32_t h, int32_t w);
+int32_t vms_composite_splats(const float* centers, const float* conics, const float* colors,
+                             const float* alphas, const int32_t* bounds, int64_t n,
+                             int64_t n_instances, float* image, int32_t h, int32_t w,
+                             int32_t exact, void* workspace, size_t workspace_bytes,
+                             void* stream);
+
+/* rasterize_triangles (kernels/__init__.py:36-43, _core.pyx:81-159): tris
+ * (n, 3, 3) f64 of (x, y, 1/z); depth-tested in place into id_image / invz. */
+size_t vms_rasterize_workspace_bytes(int64_t n);
+int32_t vms_rasterize_triangles(const double* tris, const uint32_t* ids, int64_t n,
+                                uint32_t* id_image, double* invz_image, int32_t h, int32_t w,
+                                void* workspace, size_t workspace_bytes, void* stream);
+
+/* radix_sort_pairs (kernels/__init__.py:46-51, _core.pyx:162-202): stable
+ * ascending sort of u32 keys carrying an i64 payload, in place. */
+size_t vms_radix_workspace_bytes(int64_t n);
+int32_t vms_radix_sort_pairs(uint32_t* keys, int64_t* values, int64_t n, void* workspace,
+                             size_t workspace_bytes, void* stream);
+
+/* Camera.world_to_view (render.py:79-81) on the device; also the probe that
+ * picks dot_mode against the host BLAS. out (n, 3) f64. */
+int32_t vms_world_to_view(const double* points, int64_t n, const vms_camera* cam, double* out,
+                          void* stream);
+
+/* project_records + compute_keys (render.py:138-220) over a contiguous [dev]
+ * (n, 59) f32 record array, one row per output index.  keys[i] = IEEE bits of
+ * f32 view z for live rows (opacity > 0, z > near), 0xFFFFFFFF otherwise.
+ * centers f64 (n,2), conics f64 (n,3), colors f32 (n,3), bounds i32 (n,4)
+ * half-open, kept u8 (n,): written together (all null to skip); rows with
+ * kept == 0 leave the geometry outputs untouched. */
+int32_t vms_project_records(const float* records, int64_t n, const vms_camera* cam,
+                            double* centers, double* conics, float* colors, int32_t* bounds,
+                            uint8_t* kept, uint32_t* keys, void* stream);
+
+/* evaluate_sh (render.py:104-135): coeffs (n, 16, 3) f64, dirs (n, 3) f64 unit
+ * vectors -> out (n, 3) f64 = max(0, 0.5 + sum). */
+int32_t vms_evaluate_sh(const double* coeffs, const double* dirs, int64_t n, double* out,
+                        void* stream);
+
+/* ---- per-frame stages (runtime.VmSession.render_frame) ----------------- */
+
+/* render_visibility + reduce_visibility + select_lod (render.py:279-307,
+ * runtime.py:70-96,129-132): subsystems [1] and [2]. */
+size_t vms_visibility_workspace_bytes(uint32_t n_faces, uint32_t page_count);
+int32_t vms_visibility(const vms_vis_args* args, void* stream);
+
+/* reduce_visibility (runtime.py:70-96) over a given page-ID image and f64
+ * depth image: depths_out (P + 1,) encoded nearest depth after the one-hop
+ * link pass, direct_out (P + 1,) u8, *bad_id_out = largest id > P (0 = ok;
+ * the caller raises InvariantViolation).  workspace >= 4 * (P + 1) bytes. */
+int32_t vms_reduce_visibility(const uint32_t* page_image, const double* depth_image,
+                              int64_t n_pixels, uint32_t page_count, const uint32_t* link_off,
+                              const uint32_t* link_tgt, uint32_t* depths_out, uint8_t* direct_out,
+                              uint32_t* bad_id_out, void* workspace, size_t workspace_bytes,
+                              void* stream);
+
+/* execute_copies (runtime.py:362-374): subsystem [3] data movement.
+ * mode 0: one cudaMemcpyAsync per copy (copies in host memory);
+ * mode 1: one gather kernel reading mapped pinned host memory (copies in
+ * [dev]-accessible memory). */
+int32_t vms_upload_pages(const vms_copy* copies, int64_t n, const void* host_base,
+                         void* dev_base, int32_t mode, void* stream);
+
+/* gather_resident + depth_order + composite_ordered (runtime.py:377-390,
+ * render.py:235-248): subsystems [4], [5], [6]. */
+size_t vms_render_workspace_bytes(uint32_t n_cap, uint32_t m_cap, int32_t width,
+                                  int32_t height);
+int32_t vms_render(const vms_render_args* args, void* stream);
+
+/* ---- page table (runtime.PageTable / update_page_table, runtime.py:161-346)
+ * Host C++ with O(log n) allocation; exact reference semantics. */
+vms_pagetable* vms_pt_create(int64_t capacity);
+void vms_pt_destroy(vms_pagetable* pt);
+int32_t vms_pt_update(vms_pagetable* pt, const uint32_t* pid, const uint32_t* enc,
+                      const uint8_t* direct, const uint8_t* level, int64_t n, int64_t frame,
+                      double budget, uint32_t* plan_pid, uint8_t* plan_level,
+                      int32_t* plan_entry, int32_t* plan_slot, int64_t plan_cap,
+                      int64_t* n_plan, int64_t* missing);
+int64_t vms_pt_capacity(const vms_pagetable* pt);
+int64_t vms_pt_occupied(const vms_pagetable* pt);
+int64_t vms_pt_resident_count(const vms_pagetable* pt);
+int32_t vms_pt_resident(const vms_pagetable* pt, uint32_t* pid, int32_t* entry, int32_t* slot,
+                        int64_t cap);
+int32_t vms_pt_entries(const vms_pagetable* pt, int32_t* level, int64_t* last_used,
+                       uint32_t* slots, int32_t max_slots);
+int32_t vms_pt_resident_counts(const vms_pagetable* pt, int64_t* counts, int32_t levels);
+int32_t vms_pt_check(const vms_pagetable* pt);
+int64_t vms_pt_chunks(const vms_pagetable* pt, int64_t page_size, vms_chunk* out, int64_t cap,
+                      int64_t* n_records);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* VMSPLAT_B200_H */

@@ -1,0 +1,151 @@
+"""ctypes binding of libvmsplat_b200.so — the role the reference's Cython
+module plays for `vmsplat.kernels` (pkg/src/vmsplat/kernels/__init__.py:13-21),
+without a fallback: if the CUDA library is missing the import fails loudly.
+
+Structs mirror include/vmsplat_b200.h field for field.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+from paper_2506_19415_b200.errors import CudaError, InvariantViolation
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libvmsplat_b200.so")
+
+VMS_OK = 0
+VMS_ERR_INVALID = 1
+VMS_ERR_RANGE = 2
+VMS_ERR_CUDA = 3
+VMS_ERR_NOMEM = 4
+VMS_ERR_INVARIANT = 5
+
+P = ctypes.c_void_p
+I32 = ctypes.c_int32
+I64 = ctypes.c_int64
+U32 = ctypes.c_uint32
+SZ = ctypes.c_size_t
+D = ctypes.c_double
+
+
+class Camera(ctypes.Structure):
+    _fields_ = [("pos", D * 3), ("rot", D * 9), ("focal", D), ("half_w", D), ("half_h", D),
+                ("near", D), ("width", I32), ("height", I32), ("dot_mode", I32),
+                ("pad_", I32)]
+
+
+class Lod(ctypes.Structure):
+    _fields_ = [("thresholds", D * 8), ("count", I32), ("pad_", I32)]
+
+
+class RequiredOut(ctypes.Structure):
+    _fields_ = [("pid", P), ("enc", P), ("direct", P), ("level", P), ("meta", P)]
+
+
+class VisArgs(ctypes.Structure):
+    _fields_ = [("cam", Camera), ("verts", P), ("faces", P), ("face_page", P),
+                ("n_faces", U32), ("page_count", U32), ("link_off", P), ("link_tgt", P),
+                ("lod", Lod), ("id_image", P), ("invz_image", P), ("depth_out", P),
+                ("direct_out", P), ("out", RequiredOut), ("workspace", P)]
+
+
+class Chunk(ctypes.Structure):
+    _fields_ = [("row", U32), ("gather", U32), ("count", U32), ("pad_", U32)]
+
+
+class RenderArgs(ctypes.Structure):
+    _fields_ = [("cam", Camera), ("pool", P), ("chunks", P), ("n_chunks", U32),
+                ("n_splats", U32), ("n_cap", U32), ("m_cap", U32), ("image", P),
+                ("accumulate", I32), ("exact", I32), ("counters_out", P), ("workspace", P),
+                ("ev_sorted", P)]
+
+
+class Copy(ctypes.Structure):
+    _fields_ = [("src_offset", ctypes.c_uint64), ("dst_offset", ctypes.c_uint64),
+                ("nbytes", ctypes.c_uint64)]
+
+
+# name -> (restype, argtypes); every symbol include/vmsplat_b200.h declares
+SIGNATURES = {
+    "vms_last_error": (ctypes.c_char_p, []),
+    "vms_abi_version": (I32, []),
+    "vms_composite_workspace_bytes": (SZ, [I64, I64, I32, I32]),
+    "vms_composite_splats": (I32, [P, P, P, P, P, I64, I64, P, I32, I32, I32, P, SZ, P]),
+    "vms_rasterize_workspace_bytes": (SZ, [I64]),
+    "vms_rasterize_triangles": (I32, [P, P, I64, P, P, I32, I32, P, SZ, P]),
+    "vms_radix_workspace_bytes": (SZ, [I64]),
+    "vms_radix_sort_pairs": (I32, [P, P, I64, P, SZ, P]),
+    "vms_world_to_view": (I32, [P, I64, ctypes.POINTER(Camera), P, P]),
+    "vms_project_records": (I32, [P, I64, ctypes.POINTER(Camera), P, P, P, P, P, P, P]),
+    "vms_evaluate_sh": (I32, [P, P, I64, P, P]),
+    "vms_visibility_workspace_bytes": (SZ, [U32, U32]),
+    "vms_visibility": (I32, [ctypes.POINTER(VisArgs), P]),
+    "vms_reduce_visibility": (I32, [P, P, I64, U32, P, P, P, P, P, P, SZ, P]),
+    "vms_upload_pages": (I32, [P, I64, P, P, I32, P]),
+    "vms_render_workspace_bytes": (SZ, [U32, U32, I32, I32]),
+    "vms_render": (I32, [ctypes.POINTER(RenderArgs), P]),
+    "vms_pt_create": (P, [I64]),
+    "vms_pt_destroy": (None, [P]),
+    "vms_pt_update": (I32, [P, P, P, P, P, I64, I64, D, P, P, P, P, I64,
+                            ctypes.POINTER(I64), ctypes.POINTER(I64)]),
+    "vms_pt_capacity": (I64, [P]),
+    "vms_pt_occupied": (I64, [P]),
+    "vms_pt_resident_count": (I64, [P]),
+    "vms_pt_resident": (I32, [P, P, P, P, I64]),
+    "vms_pt_entries": (I32, [P, P, P, P, I32]),
+    "vms_pt_resident_counts": (I32, [P, P, I32]),
+    "vms_pt_check": (I32, [P]),
+    "vms_pt_chunks": (I64, [P, I64, P, I64, ctypes.POINTER(I64)]),
+}
+
+_lib = None
+
+
+def load():
+    """Load (and if needed build) the CUDA library; raise if impossible."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            from paper_2506_19415_b200 import build as _build
+
+            _build.build()
+        lib = ctypes.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        if lib.vms_abi_version() != 1:
+            raise RuntimeError("libvmsplat_b200.so ABI version mismatch")
+        _lib = lib
+    return _lib
+
+
+def check(status: int, what: str = "") -> None:
+    if status == VMS_OK:
+        return
+    msg = load().vms_last_error().decode(errors="replace")
+    text = f"{what}: {msg}" if what else msg
+    if status in (VMS_ERR_RANGE, VMS_ERR_INVARIANT):
+        raise InvariantViolation(text)
+    if status == VMS_ERR_INVALID:
+        raise ValueError(text)
+    if status == VMS_ERR_NOMEM:
+        raise MemoryError(text)
+    raise CudaError(text)
+
+
+def ptr(t) -> int | None:
+    """Raw address of a torch tensor / numpy array (None for None)."""
+    if t is None:
+        return None
+    if hasattr(t, "data_ptr"):
+        return t.data_ptr()
+    return t.ctypes.data
+
+
+def stream_ptr(stream) -> int | None:
+    if stream is None:
+        return None
+    return stream.cuda_stream

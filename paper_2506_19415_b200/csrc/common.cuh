@@ -1,0 +1,61 @@
+// Shared device helpers for the vmsplat B200 kernels (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/vmsplat_b200.h"
+
+#define VMS_DEV __device__ __forceinline__
+
+namespace vms {
+
+constexpr int kWarp = 32;
+constexpr int kSMs = 148;
+
+// Thread-local last error string (filled by the ABI layer).
+void set_error(const char* fmt, ...);
+int32_t cuda_status(cudaError_t e, const char* where);
+
+#define VMS_CUDA(call)                                         \
+  do {                                                         \
+    cudaError_t _e = (call);                                   \
+    if (_e != cudaSuccess) return ::vms::cuda_status(_e, #call); \
+  } while (0)
+
+#define VMS_LAUNCH_CHECK(where)                                 \
+  do {                                                          \
+    cudaError_t _e = cudaGetLastError();                        \
+    if (_e != cudaSuccess) return ::vms::cuda_status(_e, where); \
+  } while (0)
+
+VMS_DEV uint32_t lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+VMS_DEV int lane_id() { return threadIdx.x & 31; }
+
+// Non-contracted FP64 helpers: the exactness-critical stages follow NumPy's
+// elementwise semantics (no FMA) and OpenBLAS's fused dot order explicitly.
+VMS_DEV double dmul(double a, double b) { return __dmul_rn(a, b); }
+VMS_DEV double dadd(double a, double b) { return __dadd_rn(a, b); }
+VMS_DEV double dsub(double a, double b) { return __dsub_rn(a, b); }
+VMS_DEV double ddiv(double a, double b) { return __ddiv_rn(a, b); }
+
+// 3-term dot product in the order the host BLAS uses (probed at session
+// start): mode 0 = fma(a2,b2, fma(a1,b1, a0*b0)),
+// mode 1 = (a0*b0 + a1*b1) + a2*b2 without contraction.
+VMS_DEV double dot3(int mode, double a0, double a1, double a2, double b0, double b1,
+                    double b2) {
+  if (mode == 0) return __fma_rn(a2, b2, __fma_rn(a1, b1, __dmul_rn(a0, b0)));
+  return __dadd_rn(__dadd_rn(__dmul_rn(a0, b0), __dmul_rn(a1, b1)), __dmul_rn(a2, b2));
+}
+
+template <typename T>
+__host__ __device__ __forceinline__ T ceil_div(T a, T b) {
+  return (a + b - 1) / b;
+}
+
+}  // namespace vms

@@ -1,0 +1,81 @@
+// Splat-render stage interfaces (internal to the .so): preprocess over the
+// resident page chunks, depth sort, tile duplication, tile sort, blend.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/vmsplat_b200.h"
+
+namespace vms {
+
+constexpr int kRecordFloats = 59;   // gaussians.py:1-33
+constexpr int kChunkRecords = 128;  // records per preprocess CTA
+constexpr int kTile = 16;           // blend tile edge (pixels)
+
+using RenderCamera = vms_camera;
+using Chunk = vms_chunk;
+
+// Per-splat blend payload, 48 B (3 x 16 B): f32 center/conic exactly as the
+// reference wrapper casts them (kernels/__init__.py:27-28), f32 colour
+// (render.py:215), f32 alpha, half-open int16 pixel bounds.
+struct __align__(16) BlendRec {
+  float cx, cy;
+  float ca, cb, cc;
+  float r, g, b;
+  float alpha;
+  uint32_t bx;  // x0 | x1 << 16
+  uint32_t by;  // y0 | y1 << 16
+  uint32_t pad_;
+};
+
+// Frame counters living in device memory.
+struct RenderCounters {
+  uint32_t n_kept;
+  uint32_t n_inst;
+  uint32_t overflow;
+  uint32_t pad_;
+};
+
+struct RenderWs {
+  uint32_t n_cap;  // splat capacity (gather indices)
+  uint32_t m_cap;  // tile-instance capacity
+  uint32_t *key_g, *flag, *pos;
+  BlendRec* rec;
+  uint32_t *k0, *v0, *k1, *v1;
+  uint32_t *cnt, *off;
+  uint32_t *tk0, *tv0, *tk1, *tv1;
+  uint32_t* ranges;  // 2 per tile
+  RenderCounters* ctr;
+  void* scan_ws;
+  void* radix_ws;
+};
+
+size_t render_ws_bytes(uint32_t n_cap, uint32_t m_cap, uint32_t n_tiles);
+RenderWs render_carve(void* ws, uint32_t n_cap, uint32_t m_cap, uint32_t n_tiles);
+
+// Preprocess (EWA + SH, FP64) of every record named by the chunk table;
+// writes key_g / flag / rec at gather indices.
+int32_t render_preprocess(const float* pool, const Chunk* chunks, uint32_t n_chunks,
+                          const RenderCamera& cam, const RenderWs& w, cudaStream_t s);
+
+// From preprocessed splats to an image: compaction, depth sort, tile
+// duplication, tile sort, ranges, blend.  n_splats = gather indices in use.
+int32_t render_finish(const RenderCamera& cam, uint32_t n_splats, const RenderWs& w,
+                      float* image, int accumulate, int exact, cudaEvent_t ev_sorted,
+                      cudaStream_t s);
+
+// project_records / compute_keys over a contiguous record array; any output
+// pointer may be null except that centers..kept come together.
+int32_t project_records(const float* recs, uint32_t n, const RenderCamera& cam, double* centers,
+                        double* conics, float* colors, int32_t* bounds, uint8_t* kept,
+                        uint32_t* keys, cudaStream_t s);
+int32_t evaluate_sh(const double* coeffs, const double* dirs, uint32_t n, double* out,
+                    cudaStream_t s);
+
+// Kernel-level composite of caller-ordered splats (composite_splats).
+int32_t composite_ordered(const float* centers, const float* conics, const float* colors,
+                          const float* alphas, const int32_t* bounds, uint32_t n, float* image,
+                          int h, int w, int exact, const RenderWs& ws, cudaStream_t s);
+
+}  // namespace vms

@@ -1,0 +1,457 @@
+// Subsystems [1] + [2]: proxy-mesh page-ID visibility and required-page
+// extraction.  Compiled with -fmad=false: every FP64 operation below follows
+// the reference's NumPy/Cython arithmetic one rounding at a time, so page-ID
+// images, depths and required lists are bit-exact with the CPU reference.
+//
+//  K1 vis_count_k / vis_emit_k  per-face near clip + projection
+//        (pkg/src/vmsplat/render.py:256-304), scan-ordered emission so the
+//        triangle order is (face, clip-fan) exactly as the reference builds it.
+//  K2 vis_raster_k  16x16-pixel tile per CTA; each CTA compacts the
+//        triangles overlapping its tile in index order and every pixel walks
+//        that list sequentially - exact first-triangle-wins ties without
+//        atomics (pkg/src/vmsplat/kernels/_core.pyx:81-159).
+//        Fused epilogue K3: depth encode + per-page atomicMax + direct flag
+//        (pkg/src/vmsplat/runtime.py:70-89), warp-aggregated with match_any.
+//  K4 vis_links_k / vis_required_k  one-hop link expansion from the
+//        pre-propagation snapshot, LOD level per page, ordered compaction of
+//        the required list into host-mapped memory (runtime.py:89-96,129-132).
+#include <cfloat>
+
+#include "common.cuh"
+#include "prims.h"
+#include "vis.h"
+
+namespace vms {
+
+namespace {
+
+constexpr int kVisTile = 16;
+constexpr int kVisThreads = kVisTile * kVisTile;
+
+struct View3 {
+  double x, y, z;
+};
+
+__device__ __forceinline__ View3 to_view(const VisCamera& c, const double* p) {
+  const double d0 = dsub(p[0], c.pos[0]);
+  const double d1 = dsub(p[1], c.pos[1]);
+  const double d2 = dsub(p[2], c.pos[2]);
+  View3 v;
+  v.x = dot3(c.dot_mode, d0, d1, d2, c.rot[0], c.rot[3], c.rot[6]);
+  v.y = dot3(c.dot_mode, d0, d1, d2, c.rot[1], c.rot[4], c.rot[7]);
+  v.z = dot3(c.dot_mode, d0, d1, d2, c.rot[2], c.rot[5], c.rot[8]);
+  return v;
+}
+
+__device__ __forceinline__ View3 lerp_near(const View3& a, const View3& b, double near) {
+  const double t = ddiv(dsub(near, a.z), dsub(b.z, a.z));
+  View3 r;
+  r.x = dadd(a.x, dmul(t, dsub(b.x, a.x)));
+  r.y = dadd(a.y, dmul(t, dsub(b.y, a.y)));
+  r.z = dadd(a.z, dmul(t, dsub(b.z, a.z)));
+  return r;
+}
+
+// Clip one view-space triangle at z = near into a polygon of 0, 3 or 4
+// corners (render.py:256-276); the fan from poly[0] gives 0..2 triangles.
+__device__ __forceinline__ int clip_poly(const View3* v, double near, View3* poly) {
+  const bool in0 = v[0].z > near, in1 = v[1].z > near, in2 = v[2].z > near;
+  const int n_in = (int)in0 + (int)in1 + (int)in2;
+  if (n_in == 0) return 0;
+  if (n_in == 3) {
+    poly[0] = v[0];
+    poly[1] = v[1];
+    poly[2] = v[2];
+    return 3;
+  }
+  const bool ins[3] = {in0, in1, in2};
+  int k = 0;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    const View3& a = v[i];
+    const View3& b = v[(i + 1) % 3];
+    if (ins[i]) poly[k++] = a;
+    if (ins[i] != ins[(i + 1) % 3]) poly[k++] = lerp_near(a, b, near);
+  }
+  return k;
+}
+
+__device__ __forceinline__ void face_view(const VisCamera& c, const double* verts,
+                                          const int32_t* faces, uint32_t f, View3* v) {
+#pragma unroll
+  for (int j = 0; j < 3; ++j) v[j] = to_view(c, verts + 3 * (int64_t)faces[3 * f + j]);
+}
+
+__global__ void vis_count_k(VisCamera cam, const double* __restrict__ verts,
+                            const int32_t* __restrict__ faces, uint32_t nf,
+                            uint32_t* __restrict__ counts) {
+  uint32_t f = blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= nf) return;
+  View3 v[3], poly[4];
+  face_view(cam, verts, faces, f, v);
+  int k = clip_poly(v, cam.near, poly);
+  counts[f] = k >= 3 ? (uint32_t)(k - 2) : 0u;
+}
+
+// Setup of one screen-space triangle exactly as _core.pyx:105-143 does it.
+__device__ __forceinline__ void setup_tri(double ax, double ay, double iza, double bx,
+                                          double by, double izb, double cx, double cy,
+                                          double izc, uint32_t id, int w, int h,
+                                          VisTri* out) {
+  double area = dsub(dmul(dsub(bx, ax), dsub(cy, ay)), dmul(dsub(by, ay), dsub(cx, ax)));
+  VisTri t;
+  t.id = id;
+  t.x0 = 1;
+  t.x1 = 0;  // empty unless proven otherwise
+  t.y0 = 1;
+  t.y1 = 0;
+  if (area != 0.0) {
+    if (area < 0.0) {
+      double s;
+      s = bx; bx = cx; cx = s;
+      s = by; by = cy; cy = s;
+      s = izb; izb = izc; izc = s;
+      area = -area;
+    }
+    const double mnx = fmin(ax, fmin(bx, cx)), mxx = fmax(ax, fmax(bx, cx));
+    const double mny = fmin(ay, fmin(by, cy)), mxy = fmax(ay, fmax(by, cy));
+    double fx0 = floor(dsub(mnx, 0.5)), fx1 = ceil(dsub(mxx, 0.5));
+    double fy0 = floor(dsub(mny, 0.5)), fy1 = ceil(dsub(mxy, 0.5));
+    if (fx0 < 0.0) fx0 = 0.0;
+    if (fy0 < 0.0) fy0 = 0.0;
+    if (fx1 > (double)(w - 1)) fx1 = (double)(w - 1);
+    if (fy1 > (double)(h - 1)) fy1 = (double)(h - 1);
+    if (!(fx1 < fx0 || fy1 < fy0)) {
+      t.x0 = (int)fx0;
+      t.x1 = (int)fx1;
+      t.y0 = (int)fy0;
+      t.y1 = (int)fy1;
+    }
+  }
+  t.ax = ax; t.ay = ay; t.bx = bx; t.by = by; t.cx = cx; t.cy = cy;
+  t.iza = iza; t.izb = izb; t.izc = izc; t.area = area;
+  *out = t;
+}
+
+__device__ __forceinline__ void to_pixels(const VisCamera& c, const View3& v, double* x,
+                                          double* y, double* iz) {
+  *x = dadd(ddiv(dmul(c.focal, v.x), v.z), c.half_w);
+  *y = dadd(ddiv(dmul(c.focal, v.y), v.z), c.half_h);
+  *iz = ddiv(1.0, v.z);
+}
+
+__global__ void vis_emit_k(VisCamera cam, const double* __restrict__ verts,
+                           const int32_t* __restrict__ faces,
+                           const uint32_t* __restrict__ face_page, uint32_t nf,
+                           const uint32_t* __restrict__ offsets, VisTri* __restrict__ tris) {
+  uint32_t f = blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= nf) return;
+  View3 v[3], poly[4];
+  face_view(cam, verts, faces, f, v);
+  int k = clip_poly(v, cam.near, poly);
+  uint32_t o = offsets[f];
+  for (int i = 1; i + 1 < k; ++i) {
+    double x[3], y[3], z[3];
+    to_pixels(cam, poly[0], &x[0], &y[0], &z[0]);
+    to_pixels(cam, poly[i], &x[1], &y[1], &z[1]);
+    to_pixels(cam, poly[i + 1], &x[2], &y[2], &z[2]);
+    setup_tri(x[0], y[0], z[0], x[1], y[1], z[1], x[2], y[2], z[2], face_page[f],
+              cam.width, cam.height, &tris[o + i - 1]);
+  }
+}
+
+__global__ void vis_setup_raw_k(const double* __restrict__ raw, const uint32_t* __restrict__ ids,
+                                uint32_t n, int w, int h, VisTri* __restrict__ tris) {
+  uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double* r = raw + 9 * (int64_t)i;
+  setup_tri(r[0], r[1], r[2], r[3], r[4], r[5], r[6], r[7], r[8], ids[i], w, h, &tris[i]);
+}
+
+__global__ void __launch_bounds__(kVisThreads) vis_raster_k(
+    const VisTri* __restrict__ tris, const uint32_t* __restrict__ n_tris_dev, uint32_t n_host,
+    int w, int h, uint32_t* __restrict__ id_image, double* __restrict__ invz_image,
+    int init_from_images, uint32_t page_count, uint32_t* __restrict__ page_depth,
+    uint8_t* __restrict__ page_direct, uint32_t* __restrict__ err) {
+  __shared__ VisTri stri[kVisThreads];
+  __shared__ uint32_t wsum[kVisThreads / 32];
+  __shared__ uint32_t nlist;
+
+  const int tx0 = blockIdx.x * kVisTile, ty0 = blockIdx.y * kVisTile;
+  const int tx1 = min(tx0 + kVisTile, w) - 1, ty1 = min(ty0 + kVisTile, h) - 1;
+  const int px = tx0 + (threadIdx.x & (kVisTile - 1));
+  const int py = ty0 + (threadIdx.x / kVisTile);
+  const bool inside_img = px < w && py < h;
+  const double fx = (double)px + 0.5, fy = (double)py + 0.5;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+
+  uint32_t best_id = 0;
+  double best_z = 0.0;
+  if (init_from_images && inside_img) {
+    best_id = id_image[(int64_t)py * w + px];
+    best_z = invz_image[(int64_t)py * w + px];
+  }
+  const uint32_t n = n_tris_dev ? *n_tris_dev : n_host;
+  for (uint32_t base = 0; base < n; base += kVisThreads) {
+    const uint32_t ti = base + threadIdx.x;
+    bool hit = false;
+    VisTri t;
+    if (ti < n) {
+      t = tris[ti];
+      hit = t.x0 <= t.x1 && t.x0 <= tx1 && t.x1 >= tx0 && t.y0 <= ty1 && t.y1 >= ty0;
+    }
+    const uint32_t bal = __ballot_sync(0xffffffffu, hit);
+    if (lane == 0) wsum[warp] = __popc(bal);
+    __syncthreads();
+    uint32_t pre = 0, tot = 0;
+#pragma unroll
+    for (int k = 0; k < kVisThreads / 32; ++k) {
+      uint32_t c = wsum[k];
+      pre += k < warp ? c : 0u;
+      tot += c;
+    }
+    if (hit) stri[pre + __popc(bal & lanemask_lt())] = t;
+    if (threadIdx.x == 0) nlist = tot;
+    __syncthreads();
+    if (inside_img) {
+      const uint32_t m = nlist;
+      for (uint32_t j = 0; j < m; ++j) {
+        const VisTri& q = stri[j];
+        if (px < q.x0 || px > q.x1 || py < q.y0 || py > q.y1) continue;
+        const double e0 = dsub(dmul(dsub(q.cx, q.bx), dsub(fy, q.by)),
+                               dmul(dsub(q.cy, q.by), dsub(fx, q.bx)));
+        if (e0 < 0.0) continue;
+        const double e1 = dsub(dmul(dsub(q.ax, q.cx), dsub(fy, q.cy)),
+                               dmul(dsub(q.ay, q.cy), dsub(fx, q.cx)));
+        if (e1 < 0.0) continue;
+        const double e2 = dsub(dmul(dsub(q.bx, q.ax), dsub(fy, q.ay)),
+                               dmul(dsub(q.by, q.ay), dsub(fx, q.ax)));
+        if (e2 < 0.0) continue;
+        const double iz =
+            ddiv(dadd(dadd(dmul(e0, q.iza), dmul(e1, q.izb)), dmul(e2, q.izc)), q.area);
+        if (iz > best_z) {
+          best_z = iz;
+          best_id = q.id;
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (inside_img) {
+    if (id_image) id_image[(int64_t)py * w + px] = best_id;
+    if (invz_image) invz_image[(int64_t)py * w + px] = best_z;
+  }
+  if (!page_depth) return;
+  // K3: depth = 1/invz -> float32 -> encoded (runtime.py:26-43, render.py:305-307)
+  uint32_t pid = inside_img ? best_id : 0u;
+  if (pid > page_count) {
+    atomicMax(err, pid);
+    pid = 0;
+  }
+  uint32_t enc = 0;
+  if (pid) {
+    const float d32 = __double2float_rn(ddiv(1.0, best_z));
+    enc = 0xFFFFFFFFu - __float_as_uint(d32);
+  }
+  const uint32_t peers = __match_any_sync(0xffffffffu, pid);
+  if (pid) {
+    const uint32_t mx = __reduce_max_sync(peers, enc);
+    if (lane == __ffs(peers) - 1) {
+      atomicMax(&page_depth[pid], mx);
+      page_direct[pid] = 1;
+    }
+  }
+}
+
+// Standalone reduce_visibility over given images (runtime.py:70-89).
+__global__ void vis_reduce_images_k(const uint32_t* __restrict__ ids,
+                                    const double* __restrict__ depth, uint64_t n_px,
+                                    uint32_t page_count, uint32_t* __restrict__ page_depth,
+                                    uint8_t* __restrict__ page_direct, uint32_t* __restrict__ err) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n_px;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t pid = ids[i];
+    if (!pid) continue;
+    if (pid > page_count) {
+      atomicMax(err, pid);
+      continue;
+    }
+    const uint32_t enc = 0xFFFFFFFFu - __float_as_uint(__double2float_rn(depth[i]));
+    atomicMax(&page_depth[pid], enc);
+    page_direct[pid] = 1;
+  }
+}
+
+__global__ void vis_links_k(const uint32_t* __restrict__ base, uint32_t* __restrict__ depth,
+                            const uint8_t* __restrict__ direct,
+                            const uint32_t* __restrict__ link_off,
+                            const uint32_t* __restrict__ link_tgt, uint32_t page_count) {
+  // one warp per page; lanes stride the page's link list
+  const uint32_t p = 1 + (blockIdx.x * blockDim.x + threadIdx.x) / 32;
+  if (p > page_count || !direct[p]) return;
+  const uint32_t src = base[p];
+  const uint32_t a = link_off[p - 1], b = link_off[p];
+  for (uint32_t i = a + (threadIdx.x & 31); i < b; i += 32) {
+    const uint32_t q = link_tgt[i];
+    if (q != p && q >= 1 && q <= page_count) atomicMax(&depth[q], src);
+  }
+}
+
+__global__ void vis_flags_k(const uint32_t* __restrict__ depth, uint32_t page_count,
+                            uint32_t* __restrict__ flags) {
+  uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p > page_count) return;
+  flags[p] = (p > 0 && depth[p] != 0u) ? 1u : 0u;
+}
+
+__global__ void vis_required_k(const uint32_t* __restrict__ depth,
+                               const uint8_t* __restrict__ direct,
+                               const uint32_t* __restrict__ pos, uint32_t page_count,
+                               VisLod lod, RequiredOut out) {
+  uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p == 0 || p > page_count) return;
+  const uint32_t e = depth[p];
+  if (!e) return;
+  const uint32_t o = pos[p];
+  // select_lod: level = #thresholds strictly below the decoded depth
+  const double d = (double)__uint_as_float(0xFFFFFFFFu - e);
+  uint8_t level = 0;
+  for (int k = 0; k < lod.count; ++k) level += lod.thresholds[k] < d ? 1 : 0;
+  out.pid[o] = p;
+  out.enc[o] = e;
+  out.direct[o] = direct[p];
+  out.level[o] = level;
+}
+
+}  // namespace
+
+size_t vis_ws_bytes(uint32_t n_faces, uint32_t page_count) {
+  size_t b = 0;
+  b += sizeof(uint32_t) * (n_faces + 1) * 2;        // counts + offsets
+  b += sizeof(uint32_t) * 4;                         // n_tris, n_req
+  b += sizeof(VisTri) * ((size_t)n_faces * 2 + 1);   // clipped triangles
+  b += sizeof(uint32_t) * (page_count + 1) * 3;      // base, depth, flags/pos
+  b += sizeof(uint8_t) * (page_count + 1);           // direct
+  b += scan_ws_bytes() + 1024;
+  return b + 8 * 256;
+}
+
+namespace {
+struct VisWs {
+  uint32_t *counts, *offsets, *n_tris, *n_req, *base, *depth, *pos, *err;
+  VisTri* tris;
+  uint8_t* direct;
+  void* scan;
+};
+
+template <typename T>
+T* carve(char*& p, size_t n) {
+  uintptr_t a = (reinterpret_cast<uintptr_t>(p) + 255) & ~uintptr_t(255);
+  T* r = reinterpret_cast<T*>(a);
+  p = reinterpret_cast<char*>(a + sizeof(T) * n);
+  return r;
+}
+
+VisWs carve_ws(void* ws, uint32_t nf, uint32_t P) {
+  char* p = static_cast<char*>(ws);
+  VisWs w;
+  w.counts = carve<uint32_t>(p, nf + 1);
+  w.offsets = carve<uint32_t>(p, nf + 1);
+  w.n_tris = carve<uint32_t>(p, 4);
+  w.n_req = w.n_tris + 1;
+  w.err = w.n_tris + 2;
+  w.tris = carve<VisTri>(p, (size_t)nf * 2 + 1);
+  w.base = carve<uint32_t>(p, P + 1);
+  w.depth = carve<uint32_t>(p, P + 1);
+  w.pos = carve<uint32_t>(p, P + 1);
+  w.direct = carve<uint8_t>(p, P + 1);
+  w.scan = carve<char>(p, scan_ws_bytes());
+  return w;
+}
+}  // namespace
+
+int32_t vis_frame(const VisArgs& a, cudaStream_t s) {
+  if (a.n_faces && (!a.verts || !a.faces || !a.face_page)) {
+    set_error("vis_frame: null mesh pointer");
+    return VMS_ERR_INVALID;
+  }
+  VisWs w = carve_ws(a.workspace, a.n_faces, a.page_count);
+  const int T = 256;
+  VMS_CUDA(cudaMemsetAsync(w.n_tris, 0, sizeof(uint32_t) * 4, s));
+  VMS_CUDA(cudaMemsetAsync(w.base, 0, sizeof(uint32_t) * (a.page_count + 1), s));
+  VMS_CUDA(cudaMemsetAsync(w.direct, 0, a.page_count + 1, s));
+  if (a.n_faces) {
+    vis_count_k<<<ceil_div<uint32_t>(a.n_faces, T), T, 0, s>>>(a.cam, a.verts, a.faces,
+                                                                a.n_faces, w.counts);
+    int32_t st = scan_exclusive_u32(w.counts, w.offsets, nullptr, a.n_faces, w.n_tris, w.scan, s);
+    if (st) return st;
+    vis_emit_k<<<ceil_div<uint32_t>(a.n_faces, T), T, 0, s>>>(
+        a.cam, a.verts, a.faces, a.face_page, a.n_faces, w.offsets, w.tris);
+  }
+  dim3 grid(ceil_div(a.cam.width, kVisTile), ceil_div(a.cam.height, kVisTile));
+  vis_raster_k<<<grid, kVisThreads, 0, s>>>(w.tris, w.n_tris, 0, a.cam.width, a.cam.height,
+                                            a.id_image, a.invz_image, 0, a.page_count,
+                                            w.base, w.direct, w.err);
+  VMS_CUDA(cudaMemcpyAsync(w.depth, w.base, sizeof(uint32_t) * (a.page_count + 1),
+                           cudaMemcpyDeviceToDevice, s));
+  if (a.page_count) {
+    vis_links_k<<<ceil_div<uint32_t>(a.page_count * 32, T), T, 0, s>>>(
+        w.base, w.depth, w.direct, a.link_off, a.link_tgt, a.page_count);
+  }
+  vis_flags_k<<<ceil_div<uint32_t>(a.page_count + 1, T), T, 0, s>>>(w.depth, a.page_count,
+                                                                     w.pos);
+  int32_t st = scan_exclusive_u32(w.pos, w.pos, nullptr, a.page_count + 1, w.n_req, w.scan, s);
+  if (st) return st;
+  vis_required_k<<<ceil_div<uint32_t>(a.page_count + 1, T), T, 0, s>>>(
+      w.depth, w.direct, w.pos, a.page_count, a.lod, a.out);
+  if (a.out.meta) {
+    VMS_CUDA(cudaMemcpyAsync(a.out.meta, w.n_tris, sizeof(uint32_t) * 4,
+                             cudaMemcpyDeviceToHost, s));
+  }
+  if (a.depth_out) {
+    VMS_CUDA(cudaMemcpyAsync(a.depth_out, w.depth, sizeof(uint32_t) * (a.page_count + 1),
+                             cudaMemcpyDeviceToDevice, s));
+  }
+  if (a.direct_out) {
+    VMS_CUDA(cudaMemcpyAsync(a.direct_out, w.direct, a.page_count + 1,
+                             cudaMemcpyDeviceToDevice, s));
+  }
+  VMS_LAUNCH_CHECK("vis_frame");
+  return VMS_OK;
+}
+
+int32_t reduce_images(const uint32_t* ids, const double* depth, uint64_t n_px,
+                      uint32_t page_count, const uint32_t* link_off, const uint32_t* link_tgt,
+                      uint32_t* depth_out, uint8_t* direct_out, uint32_t* err, void* ws,
+                      cudaStream_t s) {
+  uint32_t* base = static_cast<uint32_t*>(ws);
+  const int T = 256;
+  VMS_CUDA(cudaMemsetAsync(base, 0, sizeof(uint32_t) * (page_count + 1), s));
+  VMS_CUDA(cudaMemsetAsync(direct_out, 0, page_count + 1, s));
+  VMS_CUDA(cudaMemsetAsync(err, 0, sizeof(uint32_t), s));
+  if (n_px)
+    vis_reduce_images_k<<<4 * kSMs, T, 0, s>>>(ids, depth, n_px, page_count, base, direct_out,
+                                               err);
+  VMS_CUDA(cudaMemcpyAsync(depth_out, base, sizeof(uint32_t) * (page_count + 1),
+                           cudaMemcpyDeviceToDevice, s));
+  if (page_count)
+    vis_links_k<<<ceil_div<uint32_t>(page_count * 32, T), T, 0, s>>>(base, depth_out, direct_out,
+                                                                     link_off, link_tgt,
+                                                                     page_count);
+  VMS_LAUNCH_CHECK("reduce_images");
+  return VMS_OK;
+}
+
+int32_t raster_triangles(const double* raw, const uint32_t* ids, uint32_t n, uint32_t* id_image,
+                         double* invz_image, int w, int h, void* ws, cudaStream_t s) {
+  VisTri* tris = static_cast<VisTri*>(ws);
+  const int T = 256;
+  if (n) vis_setup_raw_k<<<ceil_div<uint32_t>(n, T), T, 0, s>>>(raw, ids, n, w, h, tris);
+  dim3 grid(ceil_div(w, kVisTile), ceil_div(h, kVisTile));
+  vis_raster_k<<<grid, kVisThreads, 0, s>>>(tris, nullptr, n, w, h, id_image, invz_image, 1, 0,
+                                            nullptr, nullptr, nullptr);
+  VMS_LAUNCH_CHECK("raster_triangles");
+  return VMS_OK;
+}
+
+}  // namespace vms

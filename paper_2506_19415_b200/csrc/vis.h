@@ -1,0 +1,33 @@
+// Visibility / required-page stage interfaces (internal to the .so).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/vmsplat_b200.h"
+
+namespace vms {
+
+using VisCamera = vms_camera;
+
+struct VisTri {
+  double ax, ay, bx, by, cx, cy, iza, izb, izc, area;
+  int x0, x1, y0, y1;  // inclusive clamped pixel box; x0 > x1 means empty
+  uint32_t id;
+  uint32_t pad_;
+};
+
+using VisLod = vms_lod;
+using RequiredOut = vms_required_out;
+using VisArgs = vms_vis_args;
+
+size_t vis_ws_bytes(uint32_t n_faces, uint32_t page_count);
+int32_t vis_frame(const VisArgs& a, cudaStream_t s);
+int32_t reduce_images(const uint32_t* ids, const double* depth, uint64_t n_px,
+                      uint32_t page_count, const uint32_t* link_off, const uint32_t* link_tgt,
+                      uint32_t* depth_out, uint8_t* direct_out, uint32_t* err, void* ws,
+                      cudaStream_t s);
+int32_t raster_triangles(const double* raw, const uint32_t* ids, uint32_t n, uint32_t* id_image,
+                         double* invz_image, int w, int h, void* ws, cudaStream_t s);
+
+}  // namespace vms

@@ -1,0 +1,332 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the pinned oracle /
+the reference's golden vectors.
+
+Tolerances (north star): integer/index outputs — page-ID images, depths,
+required lists, plans, residency, sort orders, stats.csv — bit-exact;
+images max-abs <= 1e-3 per channel in fast (FP32 blend) mode and <= 1e-5 in
+exact (FP64 blend) mode.
+"""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+from oracle import core
+from tests.golden import inputs
+
+pytestmark = pytest.mark.gpu
+
+FAST_TOL = 1e-3
+EXACT_TOL = 1e-5
+
+
+def _maxabs(a, b):
+    return float(np.max(np.abs(np.asarray(a, np.float64) - np.asarray(b, np.float64)))) if \
+        np.size(a) else 0.0
+
+
+# -- kernel-level drop-ins (pkg/tests/test_kernels.py) -----------------------
+def test_composite_matches_reference(cuda, golden):
+    from paper_2506_19415_b200 import kernels
+
+    g = golden["kernels"]
+    for seed in (0, 1, 2):
+        args = inputs.random_splats(seed, 400, 64, 48)
+        for exact, tol in ((True, EXACT_TOL), (False, FAST_TOL)):
+            img = np.zeros((48, 64, 3), np.float32)
+            kernels.composite_splats(*args, img, exact=exact)
+            assert _maxabs(img, g[f"composite_{seed}"]) <= tol, (seed, exact)
+
+
+def test_composite_saturates_behind_opaque(cuda):
+    """pkg/tests/test_kernels.py:49-75."""
+    from paper_2506_19415_b200 import kernels
+
+    h = w = 16
+    centers = np.array([[8.0, 8.0], [8.0, 8.0]], dtype=np.float32)
+    conics = np.array([[1e-8, 0.0, 1e-8]] * 2, dtype=np.float32)
+    colors = np.array([[1.0, 0.0, 0.0], [0.0, 1.0, 0.0]], dtype=np.float32)
+    alphas = np.array([1.0, 1.0], dtype=np.float32)
+    bounds = np.array([[0, w, 0, h]] * 2, dtype=np.int32)
+    for exact in (True, False):
+        both = np.zeros((h, w, 3), dtype=np.float32)
+        kernels.composite_splats(centers, conics, colors, alphas, bounds, both, exact=exact)
+        rep = lambda a, k: np.repeat(a[:1], k, axis=0)  # noqa: E731
+        s4 = np.zeros((h, w, 3), dtype=np.float32)
+        s5 = np.zeros((h, w, 3), dtype=np.float32)
+        kernels.composite_splats(rep(centers, 4), rep(conics, 4), rep(colors, 4),
+                                 rep(alphas, 4), rep(bounds, 4), s4, exact=exact)
+        kernels.composite_splats(rep(centers, 5), rep(conics, 5), rep(colors, 5),
+                                 rep(alphas, 5), rep(bounds, 5), s5, exact=exact)
+        assert np.array_equal(s4, s5)
+        assert both[8, 8, 1] > 0.0
+
+
+def test_composite_accumulates_in_place(cuda):
+    from paper_2506_19415_b200 import kernels
+
+    args = inputs.random_splats(9, 300, 40, 30)
+    base = np.random.default_rng(0).uniform(0, 0.2, (30, 40, 3)).astype(np.float32)
+    a = base.copy()
+    b = base.copy()
+    kernels.composite_splats(*args, a, exact=True)
+    from oracle import ckernels
+
+    ckernels.composite_splats(*args, b)
+    assert _maxabs(a, b) <= EXACT_TOL
+
+
+def test_rasterize_matches_reference_bit_exact(cuda, golden):
+    from paper_2506_19415_b200 import kernels
+
+    g = golden["kernels"]
+    for seed in (3, 4):
+        tris, ids = inputs.random_tris(seed)
+        idi = np.zeros((48, 64), np.uint32)
+        zi = np.zeros((48, 64), np.float64)
+        kernels.rasterize_triangles(tris, ids, idi, zi)
+        assert np.array_equal(idi, g[f"raster_ids_{seed}"])
+        assert np.array_equal(zi.view(np.uint64), g[f"raster_invz_{seed}"].view(np.uint64))
+
+
+def test_rasterize_first_triangle_wins_ties(cuda):
+    from paper_2506_19415_b200 import kernels
+
+    tri = np.array([[[2.0, 2.0, 1.0], [30.0, 2.0, 1.0], [2.0, 30.0, 1.0]]])
+    idi = np.zeros((32, 32), np.uint32)
+    zi = np.zeros((32, 32), np.float64)
+    kernels.rasterize_triangles(np.concatenate([tri, tri]), np.array([7, 9], np.uint32), idi, zi)
+    assert set(np.unique(idi)) <= {0, 7} and (idi == 7).any()
+
+
+def test_rasterize_large_random_matches_oracle(cuda):
+    from oracle import ckernels
+    from paper_2506_19415_b200 import kernels
+
+    rng = np.random.default_rng(77)
+    t = 3000
+    tris = np.empty((t, 3, 3))
+    tris[:, :, 0] = rng.uniform(-40, 300, size=(t, 3))
+    tris[:, :, 1] = rng.uniform(-40, 200, size=(t, 3))
+    tris[:, :, 2] = rng.choice([0.5, 1.0, 2.0], size=(t, 3))  # many exact depth ties
+    ids = rng.integers(1, 1 << 20, size=t).astype(np.uint32)
+    a_i = np.zeros((170, 260), np.uint32)
+    a_z = np.zeros((170, 260))
+    b_i, b_z = a_i.copy(), a_z.copy()
+    kernels.rasterize_triangles(tris, ids, a_i, a_z)
+    ckernels.rasterize_triangles(tris, ids, b_i, b_z)
+    assert np.array_equal(a_i, b_i)
+    assert np.array_equal(a_z.view(np.uint64), b_z.view(np.uint64))
+
+
+def test_radix_matches_reference(cuda, golden):
+    from paper_2506_19415_b200 import kernels
+
+    g = golden["kernels"]
+    for seed in range(4):
+        keys = inputs.random_keys(seed, 5000)
+        sk, sv = kernels.radix_sort_pairs(keys, np.arange(len(keys), dtype=np.int64))
+        assert np.array_equal(sv, g[f"radix_vals_{seed}"])
+        assert np.array_equal(sk, keys[sv])
+
+
+@pytest.mark.parametrize("n", [0, 1, 2, 2047, 2048, 2049, 100_000, 1_000_003])
+def test_radix_equals_stable_argsort(cuda, n):
+    """pkg/tests/test_kernels.py:109-136 + acceptance criterion 9 sizes."""
+    from paper_2506_19415_b200 import kernels
+
+    rng = np.random.default_rng(n)
+    keys = rng.integers(0, 2 ** 32, size=n, dtype=np.uint64).astype(np.uint32)
+    if n > 10:
+        keys[: n // 3] = rng.integers(0, 7, size=n // 3).astype(np.uint32)  # heavy duplicates
+    vals = rng.integers(-2 ** 62, 2 ** 62, size=n, dtype=np.int64)
+    sk, sv = kernels.radix_sort_pairs(keys, vals)
+    order = np.argsort(keys, kind="stable")
+    assert np.array_equal(sk, keys[order])
+    assert np.array_equal(sv, vals[order])
+
+
+# -- renderer API (pkg/tests/test_render.py) -----------------------------------
+def test_project_and_keys_match_reference(cuda, golden):
+    from paper_2506_19415_b200 import render
+
+    g = golden["render"]
+    recs = inputs.small_records(7, 3000)
+    for i, cam in enumerate(inputs.small_cameras()):
+        c = render.Camera(**cam)
+        k, idx = render.compute_keys(recs, c)
+        assert np.array_equal(k, g[f"keys_{i}"]) and np.array_equal(idx, g[f"keyidx_{i}"])
+        centers, conics, colors, alphas, bounds, kept = render.project_records(recs, c)
+        assert np.array_equal(kept, g[f"kept_{i}"])
+        assert np.array_equal(bounds, g[f"bounds_{i}"])
+        assert np.allclose(centers, g[f"centers_{i}"], rtol=1e-12, atol=1e-9)
+        assert np.allclose(conics, g[f"conics_{i}"], rtol=1e-9, atol=1e-12)
+        assert _maxabs(colors, g[f"colors_{i}"]) <= 1e-6
+    c, d = inputs.sh_inputs(11, 500)
+    assert np.allclose(render.evaluate_sh(c, d), g["sh"], rtol=0, atol=1e-12)
+
+
+def test_depth_order_sorts_front_to_back(cuda):
+    from paper_2506_19415_b200 import render
+
+    cam = render.Camera((0.0, 0.0, 0.0), (1.0, 0.0, 0.0, 0.0), np.pi / 2, 64, 64)
+    zs = [9.0, 1.0, 4.0, 2.5, 30.0]
+    recs = np.zeros((5, 59), np.float32)
+    recs[:, 2] = zs
+    recs[:, 3] = 1.0
+    recs[:, 7:10] = 0.3
+    recs[:, 10] = 0.9
+    order = render.depth_order(recs, cam)
+    assert np.array_equal(np.asarray(zs)[order], np.sort(zs))
+
+
+@pytest.mark.parametrize("exact", [True, False])
+def test_render_records_matches_reference(cuda, golden, exact):
+    from paper_2506_19415_b200 import render
+
+    g = golden["render"]
+    recs = inputs.small_records(7, 3000)
+    for i, cam in enumerate(inputs.small_cameras()):
+        img = render.render_records(recs, render.Camera(**cam), exact=exact)
+        assert _maxabs(img, g[f"image_{i}"]) <= (EXACT_TOL if exact else FAST_TOL), i
+
+
+def test_render_empty_is_black(cuda):
+    from paper_2506_19415_b200 import render
+
+    cam = render.Camera((0.0, 0.0, 0.0), (1.0, 0.0, 0.0, 0.0), np.pi / 2, 32, 24)
+    img = render.render_records(np.zeros((0, 59), np.float32), cam)
+    assert img.shape == (24, 32, 3) and not img.any()
+    img = render.render_records(np.zeros((10, 59), np.float32), cam)
+    assert not img.any()
+
+
+# -- visibility and reduction (subsystems [1], [2]) ----------------------------
+def _city():
+    from paper_2506_19415_b200 import scenegen
+
+    return scenegen.city_scene(inputs.CITY_SMALL)
+
+
+def test_visibility_and_reduce_bit_exact(cuda, golden):
+    from paper_2506_19415_b200 import render, runtime
+
+    g = golden["city"]
+    sc = _city()
+    mesh = runtime.ProxyMesh(sc.vertices.astype(np.float64), sc.faces.astype(np.int32),
+                             sc.face_page)
+    links = runtime.links_table(sc)
+    for i, cam in enumerate(inputs.city_cameras(inputs.CITY_SMALL)):
+        ids, depth = render.render_visibility(mesh, render.Camera(**cam))
+        assert np.array_equal(ids, g[f"vis_ids_{i}"]), i
+        assert np.array_equal(depth.view(np.uint64), g[f"vis_depth_{i}"].view(np.uint64)), i
+        req = runtime.reduce_visibility(ids, depth, links)
+        assert np.array_equal(req.depths, g[f"req_depths_{i}"])
+        assert np.array_equal(req.direct, g[f"req_direct_{i}"])
+
+
+def test_reduce_visibility_reference_cases(cuda):
+    """pkg/tests/test_runtime.py:45-85."""
+    from paper_2506_19415_b200.errors import InvariantViolation
+    from paper_2506_19415_b200.runtime import decode_depth, reduce_visibility
+
+    def links(n, table=None):
+        out = [np.zeros(0, np.uint32) for _ in range(n + 1)]
+        for s, t in (table or {}).items():
+            out[s] = np.asarray(t, np.uint32)
+        return out
+
+    req = reduce_visibility(np.array([[1, 1, 2], [0, 2, 2]], np.uint32),
+                            np.array([[4.0, 2.0, 9.0], [np.inf, 3.0, 5.0]]), links(2))
+    assert set(req.required_ids()) == {1, 2}
+    assert decode_depth(int(req.depths[1])) == pytest.approx(2.0)
+    req = reduce_visibility(np.array([[1]], np.uint32), np.array([[4.0]]),
+                            links(3, {1: [2], 2: [3]}))
+    assert set(req.required_ids()) == {1, 2} and not req.direct[2]
+    assert req.depths[2] == req.depths[1]
+    req = reduce_visibility(np.array([[1, 2]], np.uint32), np.array([[9.0, 2.0]]),
+                            links(2, {1: [2]}))
+    assert decode_depth(int(req.depths[2])) == pytest.approx(2.0)
+    with pytest.raises(InvariantViolation):
+        reduce_visibility(np.array([[5]], np.uint32), np.array([[1.0]]), links(2))
+    req = reduce_visibility(np.zeros((4, 4), np.uint32), np.full((4, 4), np.inf), links(3))
+    assert len(req.required_ids()) == 0
+
+
+# -- whole sessions ------------------------------------------------------------
+@pytest.mark.parametrize("variant", sorted(inputs.SESSION_VARIANTS))
+@pytest.mark.parametrize("exact", [False, True])
+def test_session_matches_reference(cuda, golden, variant, exact):
+    from paper_2506_19415_b200.runtime import VmSession
+
+    g = golden["city"]
+    sc = _city()
+    path = inputs.city_path(inputs.CITY_SMALL)
+    s = VmSession(sc, exact=exact, **inputs.SESSION_VARIANTS[variant])
+    assert s.dot_mode_exact, "host BLAS dot order not reproduced"
+    stats = []
+    for f in range(path.frame_count):
+        img, st = s.render_frame(path.frame_camera(f), f)
+        stats.append(st)
+        assert np.array_equal(np.array(sorted(s.table.resident), np.int64),
+                              g[f"{variant}_resident_{f}"]), f
+        assert _maxabs(img, g[f"{variant}_image_{f}"]) <= (EXACT_TOL if exact else FAST_TOL), f
+        s.table.check()
+    assert core.stats_csv(stats).encode() == g[f"{variant}_stats"].tobytes()
+
+
+@pytest.mark.parametrize("upload_mode", [0, 1])
+def test_c1_session_matches_reference(cuda, golden, upload_mode):
+    """BASELINE config 1 (reference-preprocessed box scene, 8 frames, 256^2,
+    default knobs): stats.csv identical, images within tolerance of the
+    reference frames (the oracle reproduces them bit for bit)."""
+    from paper_2506_19415_b200.runtime import VmSession
+
+    g = golden["c1"]
+    sc, _ = inputs.c1_scene()
+    path = inputs.c1_path()
+    s = VmSession(sc, upload_mode=upload_mode)
+    o = core.OSession(sc)
+    stats = []
+    for f in range(path.frame_count):
+        cam = path.frame_camera(f)
+        img, st = s.render_frame(cam, f)
+        ref, _ = o.render_frame(cam, f)
+        assert hashlib.sha256(ref.tobytes()).digest() == g[f"image_sha_{f}"].tobytes()
+        stats.append(st)
+        assert _maxabs(img, ref) <= FAST_TOL, f
+        assert core.psnr(img, ref) >= 50.0
+    assert core.stats_csv(stats).encode() == g["stats"].tobytes()
+
+
+def test_full_buffer_renders_like_flat_scene(cuda):
+    """Criterion 2 analogue: every page resident at level 0 -> the streamed
+    frame equals the flat render of the level-0 records."""
+    from paper_2506_19415_b200 import render
+    from paper_2506_19415_b200.runtime import VmSession
+
+    sc = _city()
+    s = VmSession(sc, buffer_pages=sc.page_count, staging_pages=float(sc.page_count),
+                  vis_scale=1.0, lod_enabled=False, exact=True)
+    cam = render.Camera((12.0, -8.0, -30.0), (1.0, 0.0, 0.0, 0.0), np.pi / 2, 96, 80)
+    for f in range(3):
+        img, st = s.render_frame(cam, f)
+    level0 = np.asarray(sc.gaussians[: sc.page_count * sc.page_size])
+    assert st["resident_pages"] == len(s.table.resident)
+    flat = render.render_records(level0, cam, exact=True)
+    if st["resident_pages"] == sc.page_count:
+        assert np.array_equal(img, flat)
+
+
+def test_session_is_deterministic(cuda):
+    from paper_2506_19415_b200.runtime import VmSession
+
+    sc = _city()
+    path = inputs.city_path(inputs.CITY_SMALL)
+    outs = []
+    for _ in range(2):
+        s = VmSession(sc, buffer_pages=16, staging_pages=6.0, vis_scale=0.5)
+        outs.append([s.render_frame(path.frame_camera(f), f)[0] for f in range(path.frame_count)])
+    for a, b in zip(*outs):
+        assert np.array_equal(a, b)
