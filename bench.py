@@ -1,0 +1,373 @@
+"""Benchmark: frames/sec of the per-frame VM/LOD splat path at 1080p.
+
+Workload (BASELINE.json configs[1], "C2"): synthetic 2M-Gaussian paged city
+(1000 pages x 2048 records, 3 LOD levels, written by scenegen.write_city),
+1080p 120-frame street fly-through, reference session defaults (buffer 500
+pages, staging 40 pages/frame, vis scale 0.25, LOD + links on).  One step =
+one ``VmSession.render_frame``: visibility -> required pages -> page table ->
+page uploads (pinned host -> HBM) -> preprocess -> sorts -> blend.
+
+  value  frames/s with the image left in HBM (out="device"); page uploads are
+         part of every step (the scene lives in host memory by design).
+  e2e    frames/s through the public API with the frame copied to a pinned
+         host buffer every step (render_frame(out=<pinned numpy>)).
+
+Multi-GPU (torchrun): views are sharded - rank r renders its contiguous
+block of the trajectory with its own page cache over its own pinned host copy
+of the scene ("scaling": "weak": K frames per rank); the only collective is
+the final NCCL gather of per-frame stats and each rank's last image.
+
+--impl reference: the reference's CPU path (its Cython kernels compiled into
+oracle/_ref, driven by the NumPy restatement in oracle/core.py) on the same
+scene/path, rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "frames/sec at 1080p (device-timed)"
+UNIT = "frames/s"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=30)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    p.add_argument("--exact", action="store_true", help="FP64 blend")
+    p.add_argument("--upload-mode", type=int, default=1)
+    p.add_argument("--frames", type=int, default=120, help="trajectory length")
+    p.add_argument("--width", type=int, default=1920)
+    p.add_argument("--height", type=int, default=1080)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-frames", type=int, default=1)
+    p.add_argument("--scene-dir", default=os.environ.get("VMSPLAT_SCENE_DIR", "/tmp/vmsplat_bench"))
+    return p.parse_args()
+
+
+def scene_path(args):
+    from paper_2506_19415_b200 import scenegen
+
+    lay = scenegen.C2
+    os.makedirs(args.scene_dir, exist_ok=True)
+    path = os.path.join(args.scene_dir, f"c2_p{lay.n_pages}_s{lay.page_size}_l{lay.levels}"
+                                        f"_seed{lay.seed}.vms")
+    return lay, path
+
+
+def ensure_scene(args, rank):
+    from paper_2506_19415_b200 import scenegen
+
+    lay, path = scene_path(args)
+    if rank == 0 and not os.path.exists(path):
+        tmp = path + f".tmp{os.getpid()}"
+        scenegen.write_city(tmp, lay)
+        os.replace(tmp, path)
+    return lay, path
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback"
+
+
+def launches_per_frame(stats, n_faces, upload_mode):
+    """Kernel launches of libvmsplat_b200.so per frame (static count of the
+    launch sequence in vis.cu / abi.cu / prims.cu / blend.cu)."""
+    vis = (5 if n_faces else 0) + 1 + 1 + 1 + 3 + 1
+    up = 1 if (stats["planned_copies"] and upload_mode == 1) else 0
+    render = 0
+    if stats["n_resident_records"]:
+        render = 1 + 4 + 12 + 14
+    else:
+        render = 12 + 14
+    return vis + up + render
+
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+
+    from paper_2506_19415_b200.runtime import VmSession
+    from paper_2506_19415_b200.scene_io import read_scene
+    from paper_2506_19415_b200 import scenegen
+
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    lay, path = ensure_scene(args, rank)
+    if dist:
+        dist.barrier()
+    scene = read_scene(path, mmap_gaussians=True)
+    traj = scenegen.street_path(lay, frames=args.frames, width=args.width, height=args.height)
+    F = traj.frame_count
+    start = rank * F // world
+    block = max(1, (rank + 1) * F // world - start)
+    sess = VmSession(scene, buffer_pages=500, staging_pages=40, vis_scale=0.25,
+                     exact=args.exact, upload_mode=args.upload_mode)
+    step = [0]
+
+    def frame(out):
+        i = step[0]
+        step[0] += 1
+        cam = traj.frame_camera(start + (i % block))
+        return sess.render_frame(cam, start + i, out=out)
+
+    for _ in range(args.warmup):
+        frame("device")
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    sampler = ClockSampler(local_rank)
+
+    def timed(out):
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        sts = [frame(out)[1] for _ in range(args.steps)]
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        if dist:
+            t = torch.tensor([ms], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+            dist.barrier()
+        return ms, sts
+
+    sampler.start()
+    ms_dev, stats = timed("device")
+    clocks = sampler.stop()
+    pinned = torch.empty((args.height, args.width, 3), dtype=torch.float32).pin_memory()
+    ms_e2e, stats_e2e = timed(pinned.numpy())
+
+    # final NCCL gather of per-frame stats rows and each rank's last image
+    rows = torch.tensor([[s["frame"], s["required_pages"], s["missing_pages"], s["bytes_copied"],
+                          s["resident_pages"]] for s in stats + stats_e2e],
+                        dtype=torch.int64, device="cuda")
+    last = sess.render_frame(traj.frame_camera(start), start + step[0], out="device")[0]
+    if dist:
+        allrows = [torch.empty_like(rows) for _ in range(world)] if rank == 0 else None
+        dist.gather(rows, allrows, dst=0)
+        imgs = [torch.empty_like(last) for _ in range(world)] if rank == 0 else None
+        dist.gather(last.contiguous(), imgs, dst=0)
+        dist.barrier()
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return None
+
+    hbm, peak_kind = peaks()
+    W, H = args.width, args.height
+    blend_s = sum(s["time_blend"] for s in stats)
+    pre_s = sum(s["time_preprocess"] for s in stats)
+    blend_bytes = sum(s["n_instances"] * (4 + 48) + W * H * 12 for s in stats)
+    pre_bytes = sum(s["n_resident_records"] * (236 + 4 + 4) + s["n_kept"] * 48 for s in stats)
+    stages = {k: 1e3 * statistics.mean(s[f"time_{k}"] for s in stats)
+              for k in ("visibility", "update", "copy", "sort", "render", "preprocess", "tiles",
+                        "blend", "device_frame")}
+    dominant = "blend" if blend_s >= pre_s else "preprocess"
+    if dominant == "blend":
+        ach = blend_bytes / blend_s / 1e9
+    else:
+        ach = pre_bytes / pre_s / 1e9
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tf):
+        try:
+            traffic = json.load(open(tf)).get(dominant)
+        except ValueError:
+            traffic = None
+    up_bytes = sum(s["bytes_copied"] for s in stats)
+    up_s = sum(s["time_copy"] for s in stats if s["bytes_copied"])
+    value = world * args.steps / (ms_dev / 1e3)
+    e2e = world * args.steps / (ms_e2e / 1e3)
+    launches = sum(launches_per_frame(s, len(scene.faces), args.upload_mode) for s in stats)
+    out = {
+        "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_dev / args.steps, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64+f32",
+        "data": "synthetic (scenegen city, seed 0)",
+        "config": {"workload": "C2: 2M-Gaussian paged city (1000 pages x 2048, 3 LOD), "
+                               "1080p 120-frame street fly-through, buffer 500, staging 40, "
+                               "vis 0.25, LOD+links on",
+                   "width": W, "height": H, "frames": F, "parallelism": f"view-shard x{world}",
+                   "blend": "fp64-exact" if args.exact else "fp32",
+                   "l2": "inputs larger than L2 (resident pool up to 241 MB > 126 MB L2)",
+                   "upload_mode": args.upload_mode},
+        "e2e": {"value": round(e2e, 3), "unit": UNIT,
+                "h2d_bytes_per_step": int(statistics.mean(s["bytes_copied"] for s in stats_e2e))
+                + 16 * int(statistics.mean(s.get("n_chunks", 0) for s in stats_e2e)),
+                "d2h_bytes_per_step": W * H * 12 + 10 * int(statistics.mean(
+                    s["required_pages"] for s in stats_e2e))},
+        "roofline": {"bound": "hbm", "kernel": dominant, "achieved": round(ach, 2),
+                     "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s",
+                     "frac": round(ach / hbm, 4), "traffic": traffic},
+        "stages_ms": {k: round(v, 4) for k, v in stages.items()},
+        "upload": {"gbs": round(up_bytes / up_s / 1e9, 2) if up_s else None,
+                   "bytes": up_bytes, "frames_with_copies": sum(1 for s in stats if s["bytes_copied"])},
+        "mean_instances": int(statistics.mean(s["n_instances"] for s in stats)),
+        "mean_resident_records": int(statistics.mean(s["n_resident_records"] for s in stats)),
+        "gpu_launches": int(launches),
+        "clocks": clocks,
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(scene, traj, args, start_frame=args.warmup,
+                                           frames=args.cpu_frames)
+    if dist:
+        dist.destroy_process_group()
+    return out
+
+
+def reference_session(scene, traj, args, warm_to):
+    """Oracle session (reference kernels when built) warmed to frame
+    ``warm_to`` without compositing (visibility + paging + copies only)."""
+    from oracle import core, refkernels
+
+    kern = refkernels if refkernels.available() else None
+    s = core.OSession(scene, buffer_pages=500, staging_pages=40, vis_scale=0.25, kern=kern)
+    for f in range(warm_to):
+        s.render_frame(traj.frame_camera(f), f, want_image=False)
+    return s, ("reference" if kern is not None else "port")
+
+
+def cpu_baseline(scene, traj, args, start_frame, frames):
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    s, kind = reference_session(scene, traj, args, start_frame)
+    t0 = time.perf_counter()
+    for f in range(start_frame, start_frame + frames):
+        s.render_frame(traj.frame_camera(f), f)
+    dt = time.perf_counter() - t0
+    return {"value": round(frames / dt, 5), "unit": UNIT, "cores": 1, "kind": kind,
+            "sample": f"{frames} full 1080p frame(s) of the C2 trajectory at frames "
+                      f"{start_frame}..{start_frame + frames - 1} after warming the page table "
+                      f"(visibility+paging only) through frame {start_frame - 1}; reference "
+                      f"Cython kernels (oracle/_ref) driven by oracle/core.py, 1 thread"}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return None
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    from paper_2506_19415_b200 import scenegen
+    from paper_2506_19415_b200.scene_io import read_scene
+
+    lay, path = ensure_scene(args, 0)
+    scene = read_scene(path, mmap_gaussians=True)
+    traj = scenegen.street_path(lay, frames=args.frames, width=args.width, height=args.height)
+    s, kind = reference_session(scene, traj, args, 0)
+    f = 0
+    for _ in range(args.warmup):
+        s.render_frame(traj.frame_camera(f), f, want_image=False)
+        f += 1
+    n = min(args.steps, 12)  # bounded sample: ~3 s per 1080p frame on one core
+    t0 = time.perf_counter()
+    for _ in range(n):
+        s.render_frame(traj.frame_camera(f % traj.frame_count), f)
+        f += 1
+    dt = time.perf_counter() - t0
+    v = n / dt
+    return {"metric": METRIC, "value": round(v, 5), "unit": UNIT, "n_gpus": 0,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * dt / args.steps, 2),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (scenegen city, seed 0)", "impl": "reference",
+            "config": {"workload": "C2: 2M-Gaussian paged city, 1080p 120-frame street "
+                                   "fly-through, buffer 500, staging 40", "width": args.width,
+                       "height": args.height},
+            "cpu_baseline": {"value": round(v, 5), "unit": UNIT, "cores": 1, "kind": kind,
+                             "sample": f"{n} full 1080p frames (step count capped at 12) after {args.warmup} "
+                                       "warm-up frames without compositing; single-threaded "
+                                       "reference hot loops"},
+            "e2e": {"value": round(v, 5), "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        out = run_reference(args, rank, world)
+    else:
+        out = run_ours(args, rank, world, local_rank)
+    if rank == 0 and out is not None:
+        print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()

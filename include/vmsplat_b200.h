@@ -123,7 +123,8 @@ typedef struct vms_render_args {
   int32_t exact;                /* 1: FP64 blend (reference arithmetic) */
   uint32_t* counters_out;       /* [host pinned] optional: n_kept, n_inst, overflow */
   void* workspace;              /* [dev] vms_render_workspace_bytes() */
-  void* ev_sorted;              /* optional cudaEvent_t recorded after the depth sort */
+  void* events[4];              /* optional cudaEvent_t, recorded after: preprocess,
+                                   depth sort, tile sort (blend start), blend */
 } vms_render_args;
 
 /* One planned page copy in bytes (runtime.execute_copies, runtime.py:362-374). */

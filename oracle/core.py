@@ -563,7 +563,7 @@ class OSession:
         records = self.resident_records()
         t5 = time.perf_counter()
         image = None
-        order = order_of(records, cam, self.kern)
+        order = order_of(records, cam, self.kern) if want_image else None
         t6 = time.perf_counter()
         if want_image:
             image = composite_in_order(records, order, cam, self.kern)

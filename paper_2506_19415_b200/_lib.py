@@ -59,7 +59,7 @@ class RenderArgs(ctypes.Structure):
     _fields_ = [("cam", Camera), ("pool", P), ("chunks", P), ("n_chunks", U32),
                 ("n_splats", U32), ("n_cap", U32), ("m_cap", U32), ("image", P),
                 ("accumulate", I32), ("exact", I32), ("counters_out", P), ("workspace", P),
-                ("ev_sorted", P)]
+                ("events", P * 4)]
 
 
 class Copy(ctypes.Structure):

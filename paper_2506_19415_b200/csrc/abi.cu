@@ -284,8 +284,8 @@ int32_t vms_render(const vms_render_args* a, void* stream) {
   RenderWs w = render_carve(a->workspace, a->n_cap, a->m_cap, tiles);
   int32_t st = render_preprocess(a->pool, a->chunks, a->n_chunks, a->cam, w, s);
   if (st) return st;
-  st = render_finish(a->cam, a->n_splats, w, a->image, a->accumulate, a->exact,
-                     static_cast<cudaEvent_t>(a->ev_sorted), s);
+  if (a->events[0]) VMS_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(a->events[0]), s));
+  st = render_finish(a->cam, a->n_splats, w, a->image, a->accumulate, a->exact, a->events, s);
   if (st) return st;
   if (a->counters_out)
     VMS_CUDA(cudaMemcpyAsync(a->counters_out, w.ctr, sizeof(uint32_t) * 3,

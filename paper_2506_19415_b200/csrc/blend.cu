@@ -220,7 +220,8 @@ int tile_bits(uint32_t n_tiles) {
 }
 
 int32_t tiles_and_blend(const RenderCamera& cam, const uint32_t* vals, const RenderWs& w,
-                        float* image, int accumulate, int exact, cudaStream_t s) {
+                        float* image, int accumulate, int exact, void* const* events,
+                        cudaStream_t s) {
   const int tiles_x = ceil_div(cam.width, kTile), tiles_y = ceil_div(cam.height, kTile);
   const uint32_t n_tiles = (uint32_t)tiles_x * tiles_y;
   const int T = 256;
@@ -237,12 +238,14 @@ int32_t tiles_and_blend(const RenderCamera& cam, const uint32_t* vals, const Ren
   const uint32_t* tv = alt ? w.tv1 : w.tv0;
   VMS_CUDA(cudaMemsetAsync(w.ranges, 0, sizeof(uint32_t) * 2 * n_tiles, s));
   ranges_k<<<8 * kSMs, T, 0, s>>>(tk, w.ctr, w.ranges);
+  if (events && events[2]) VMS_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(events[2]), s));
   if (exact)
     blend_k<true><<<n_tiles, kBlendThreads, 0, s>>>(w.ranges, tv, w.rec, cam.width, cam.height,
                                                     tiles_x, image, accumulate);
   else
     blend_k<false><<<n_tiles, kBlendThreads, 0, s>>>(w.ranges, tv, w.rec, cam.width, cam.height,
                                                      tiles_x, image, accumulate);
+  if (events && events[3]) VMS_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(events[3]), s));
   VMS_LAUNCH_CHECK("tiles_and_blend");
   return VMS_OK;
 }
@@ -288,7 +291,7 @@ RenderWs render_carve(void* ws, uint32_t n_cap, uint32_t m_cap, uint32_t n_tiles
 }
 
 int32_t render_finish(const RenderCamera& cam, uint32_t n_splats, const RenderWs& w,
-                      float* image, int accumulate, int exact, cudaEvent_t ev_sorted,
+                      float* image, int accumulate, int exact, void* const* events,
                       cudaStream_t s) {
   const int T = 256;
   VMS_CUDA(cudaMemsetAsync(w.ctr, 0, sizeof(RenderCounters), s));
@@ -304,8 +307,8 @@ int32_t render_finish(const RenderCamera& cam, uint32_t n_splats, const RenderWs
   int32_t st = radix_sort_u32(w.k0, w.v0, w.k1, w.v1, &w.ctr->n_kept, 0, 0, 31, &alt,
                               w.radix_ws, s);
   if (st) return st;
-  if (ev_sorted) VMS_CUDA(cudaEventRecord(ev_sorted, s));
-  return tiles_and_blend(cam, alt ? w.v1 : w.v0, w, image, accumulate, exact, s);
+  if (events && events[1]) VMS_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(events[1]), s));
+  return tiles_and_blend(cam, alt ? w.v1 : w.v0, w, image, accumulate, exact, events, s);
 }
 
 int32_t composite_ordered(const float* centers, const float* conics, const float* colors,
@@ -324,7 +327,7 @@ int32_t composite_ordered(const float* centers, const float* conics, const float
     if (st) return st;
     compact_k<<<ceil_div<uint32_t>(n, T), T, 0, s>>>(ws.flag, ws.pos, ws.v1, n, ws.k0, ws.v0);
   }
-  return tiles_and_blend(cam, ws.v0, ws, image, 1, exact, s);
+  return tiles_and_blend(cam, ws.v0, ws, image, 1, exact, nullptr, s);
 }
 
 }  // namespace vms

@@ -86,7 +86,8 @@ struct Proj {
 };
 
 // compute_keys cull + project_records for one record r[59] (render.py:138-220).
-__device__ __forceinline__ void project_one(const float* r, const RenderCamera& cam, Proj& o) {
+__device__ __forceinline__ void project_one(const float* r, const RenderCamera& cam, Proj& o,
+                                            bool cull_live) {
   const double d0 = (double)r[0] - cam.pos[0], d1 = (double)r[1] - cam.pos[1],
                d2 = (double)r[2] - cam.pos[2];
   const int dm = cam.dot_mode;
@@ -96,7 +97,7 @@ __device__ __forceinline__ void project_one(const float* r, const RenderCamera& 
   o.tz = tz;
   o.live = r[10] > 0.0f && tz > cam.near;
   o.kept = false;
-  if (!o.live) return;
+  if (cull_live && !o.live) return;
   double R[9];
   quat_rot((double)r[3], (double)r[4], (double)r[5], (double)r[6], R);
   const double sx = r[7], sy = r[8], sz = r[9];
@@ -185,7 +186,7 @@ __global__ void __launch_bounds__(kChunkRecords) preprocess_k(
   const uint32_t g = ch.gather + t;
   const float* r = srec + t * kRecordFloats;
   Proj p;
-  project_one(r, cam, p);
+  project_one(r, cam, p, true);
   if (!p.kept) {
     flag[g] = 0u;
     key_g[g] = 0xFFFFFFFFu;
@@ -218,7 +219,7 @@ __global__ void project_k(const float* __restrict__ recs, uint32_t n, RenderCame
   if (i >= n) return;
   const float* r = recs + (size_t)i * kRecordFloats;
   Proj p;
-  project_one(r, cam, p);
+  project_one(r, cam, p, false);
   if (keys) keys[i] = p.live ? __float_as_uint(__double2float_rn(p.tz)) : 0xFFFFFFFFu;
   if (!centers) return;
   kept[i] = p.kept ? 1 : 0;

@@ -62,7 +62,7 @@ int32_t render_preprocess(const float* pool, const Chunk* chunks, uint32_t n_chu
 // From preprocessed splats to an image: compaction, depth sort, tile
 // duplication, tile sort, ranges, blend.  n_splats = gather indices in use.
 int32_t render_finish(const RenderCamera& cam, uint32_t n_splats, const RenderWs& w,
-                      float* image, int accumulate, int exact, cudaEvent_t ev_sorted,
+                      float* image, int accumulate, int exact, void* const* events,
                       cudaStream_t s);
 
 // project_records / compute_keys over a contiguous record array; any output

@@ -392,8 +392,10 @@ class VmSession:
             self.copy_stream = t.cuda.Stream(device=self.device)
             ev = lambda: t.cuda.Event(enable_timing=True)  # noqa: E731
             self.ev = {k: ev() for k in ("start", "vis", "req", "copy0", "copy1", "render0",
-                                         "sorted", "end")}
+                                         "pre", "sorted", "blend0", "blend1", "end")}
             self.ev_copy_done = t.cuda.Event()
+            for e in self.ev.values():  # torch creates CUDA events lazily
+                e.record(t.cuda.current_stream())
         self._last_render = None  # args of the last render, for overflow recovery
         self.frame_log = []
 
@@ -446,7 +448,9 @@ class VmSession:
         a.exact = int(self.exact)
         a.counters_out = self.counters.data_ptr()
         a.workspace = self.render_ws.data_ptr()
-        a.ev_sorted = self.ev["sorted"].cuda_event if record_events else None
+        if record_events:
+            for i, k in enumerate(("pre", "sorted", "blend0", "blend1")):
+                a.events[i] = self.ev[k].cuda_event
         _lib.check(_lib.load().vms_render(ctypes.byref(a), _device.sptr()), "render")
 
     def _check_overflow(self, camera, image, n_chunks, n_res):
@@ -563,9 +567,14 @@ class VmSession:
             "time_sort": d("render0", "sorted"),
             "time_render": d("sorted", "end"),
             "time_frame_wall": h5 - h0,
+            "time_preprocess": d("render0", "pre"),
+            "time_tiles": d("sorted", "blend0"),
+            "time_blend": d("blend0", "blend1"),
+            "time_device_frame": d("start", "end"),
             "n_kept": int(self.counters[0]),
             "n_instances": int(self.counters[1]),
             "n_resident_records": n_res,
+            "n_chunks": n_chunks,
         }
         return host_img, stats
 
