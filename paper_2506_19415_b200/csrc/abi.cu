@@ -288,7 +288,7 @@ int32_t vms_render(const vms_render_args* a, void* stream) {
   st = render_finish(a->cam, a->n_splats, w, a->image, a->accumulate, a->exact, a->events, s);
   if (st) return st;
   if (a->counters_out)
-    VMS_CUDA(cudaMemcpyAsync(a->counters_out, w.ctr, sizeof(uint32_t) * 3,
+    VMS_CUDA(cudaMemcpyAsync(a->counters_out, w.ctr, sizeof(uint32_t) * 4,
                              cudaMemcpyDeviceToHost, s));
   return VMS_OK;
 }

@@ -63,30 +63,60 @@ __global__ void dup_count_k(const uint32_t* __restrict__ vals, const BlendRec* _
   }
 }
 
-__global__ void dup_emit_k(const uint32_t* __restrict__ vals, const BlendRec* __restrict__ rec,
-                           const uint32_t* __restrict__ off, RenderCounters* __restrict__ ctr,
-                           uint32_t m_cap, int tiles_x, uint32_t* __restrict__ tk,
-                           uint32_t* __restrict__ tv) {
-  const uint32_t n = ctr->n_kept;
-  if (ctr->n_inst > m_cap) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) ctr->overflow = 1;
-    return;
+// Load-balanced expansion: each CTA owns a contiguous run of kEmitChunk
+// output instances, finds the splats covering it by binary search over the
+// exclusive offsets, and every thread writes consecutive instances
+// (coalesced) regardless of how many tiles one splat touches.
+constexpr int kEmitChunk = 1024;
+constexpr int kEmitThreads = 256;
+
+__device__ __forceinline__ uint32_t last_le(const uint32_t* a, uint32_t n, uint32_t x) {
+  // largest j < n with a[j] <= x (a ascending, a[0] == 0)
+  uint32_t lo = 0, hi = n;
+  while (hi - lo > 1) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (a[mid] <= x) lo = mid; else hi = mid;
   }
-  for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < n; s += gridDim.x * blockDim.x) {
-    const uint32_t g = vals[s];
-    int tx0, tx1, ty0, ty1;
-    tile_rect(rec[g], &tx0, &tx1, &ty0, &ty1);
-    uint32_t o = off[s];
-    for (int ty = ty0; ty <= ty1; ++ty)
-      for (int tx = tx0; tx <= tx1; ++tx) {
-        tk[o] = (uint32_t)(ty * tiles_x + tx);
-        tv[o] = g;
-        ++o;
-      }
+  return lo;
+}
+
+__global__ void __launch_bounds__(kEmitThreads) dup_emit_k(
+    const uint32_t* __restrict__ vals, const BlendRec* __restrict__ rec,
+    const uint32_t* __restrict__ off, RenderCounters* __restrict__ ctr, uint32_t m_cap,
+    int tiles_x, uint32_t* __restrict__ tk, uint32_t* __restrict__ tv) {
+  __shared__ uint32_t soff[kEmitChunk + 1];
+  __shared__ uint4 sinfo[kEmitChunk];  // g, tx0, ty0, tiles across
+  __shared__ uint32_t span[2];
+  const uint32_t n = ctr->n_kept, m = ctr->n_inst;
+  if (m > m_cap || n == 0) return;
+  for (uint32_t i0 = blockIdx.x * kEmitChunk; i0 < m; i0 += gridDim.x * kEmitChunk) {
+    const uint32_t i1 = min(m, i0 + kEmitChunk);
+    if (threadIdx.x == 0) span[0] = last_le(off, n, i0);
+    if (threadIdx.x == 1) span[1] = last_le(off, n, i1 - 1);
+    __syncthreads();
+    const uint32_t s0 = span[0], ns = span[1] - s0 + 1;
+    for (uint32_t j = threadIdx.x; j < ns; j += kEmitThreads) {
+      const uint32_t g = vals[s0 + j];
+      int tx0, tx1, ty0, ty1;
+      tile_rect(rec[g], &tx0, &tx1, &ty0, &ty1);
+      soff[j] = off[s0 + j];
+      sinfo[j] = make_uint4(g, (uint32_t)tx0, (uint32_t)ty0, (uint32_t)(tx1 - tx0 + 1));
+    }
+    __syncthreads();
+    for (uint32_t i = i0 + threadIdx.x; i < i1; i += kEmitThreads) {
+      const uint32_t j = last_le(soff, ns, i);
+      const uint4 inf = sinfo[j];
+      const uint32_t k = i - soff[j];
+      const uint32_t ty = inf.z + k / inf.w, tx = inf.y + k % inf.w;
+      tk[i] = ty * (uint32_t)tiles_x + tx;
+      tv[i] = inf.x;
+    }
+    __syncthreads();
   }
 }
 
 __global__ void clamp_inst_k(RenderCounters* ctr, uint32_t m_cap) {
+  ctr->n_need = ctr->n_inst;
   if (ctr->n_inst > m_cap) {
     ctr->overflow = 1;
     ctr->n_inst = 0;  // downstream stages see an empty frame; host re-runs

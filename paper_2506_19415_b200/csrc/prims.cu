@@ -235,12 +235,14 @@ int32_t scan_exclusive_u32(const uint32_t* in, uint32_t* out, const uint32_t* n_
   return VMS_OK;
 }
 
-size_t radix_ws_bytes() { return sizeof(uint32_t) * (256 * kPrimGrid + 64); }
+size_t radix_ws_bytes() { return sizeof(uint32_t) * (256 * kPrimGrid + 64) + scan_ws_bytes() + 256; }
 
 int32_t radix_sort_u32(uint32_t* k0, uint32_t* v0, uint32_t* k1, uint32_t* v1,
                        const uint32_t* n_dev, uint32_t n_host, int begin_bit, int end_bit,
                        int* in_alt, void* ws, cudaStream_t s) {
   uint32_t* counts = static_cast<uint32_t*>(ws);
+  void* scan_ws = reinterpret_cast<char*>(ws) +
+                  ((sizeof(uint32_t) * (256 * kPrimGrid + 64) + 255) & ~size_t(255));
   int alt = 0;
   for (int b = begin_bit; b < end_bit; b += 8) {
     int bits = end_bit - b < 8 ? end_bit - b : 8;
@@ -248,7 +250,11 @@ int32_t radix_sort_u32(uint32_t* k0, uint32_t* v0, uint32_t* k1, uint32_t* v1,
     uint32_t *ki = alt ? k1 : k0, *vi = alt ? v1 : v0;
     uint32_t *ko = alt ? k0 : k1, *vo = alt ? v0 : v1;
     radix_upsweep_k<<<kPrimGrid, kRBlock, 0, s>>>(ki, n_dev, n_host, b, mask, counts);
-    scan_single_k<<<1, kScanBlock, 0, s>>>(counts, 256u * kPrimGrid, nullptr);
+    // digit-major counts -> global (digit, block) offsets; only the digits
+    // this pass can produce are scanned
+    int32_t st = scan_exclusive_u32(counts, counts, nullptr, (mask + 1u) * kPrimGrid, nullptr,
+                                    scan_ws, s);
+    if (st) return st;
     radix_downsweep_k<<<kPrimGrid, kRBlock, 0, s>>>(ki, vi, ko, vo, n_dev, n_host, b, mask,
                                                     counts);
     alt ^= 1;

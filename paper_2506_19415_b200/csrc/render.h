@@ -34,7 +34,7 @@ struct RenderCounters {
   uint32_t n_kept;
   uint32_t n_inst;
   uint32_t overflow;
-  uint32_t pad_;
+  uint32_t n_need;  // instances the frame needs (== n_inst unless overflow)
 };
 
 struct RenderWs {

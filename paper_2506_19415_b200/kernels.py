@@ -37,7 +37,7 @@ def _instances(bounds, h, w) -> int:
     return int((tx * ty).sum())
 
 
-def composite_splats(centers, conics, colors, alphas, bounds, image, exact: bool = False):
+def composite_splats(centers, conics, colors, alphas, bounds, image, exact: bool = True):
     """Blend caller-ordered splats into float32 ``image`` (h, w, 3) in place
     (kernels/__init__.py:24-33; contract _ref.py:16-54)."""
     t = _device.require_cuda()

@@ -160,7 +160,7 @@ def depth_order(records, camera: Camera) -> np.ndarray:
     return order
 
 
-def composite_ordered(records, order, camera: Camera, exact: bool = False) -> np.ndarray:
+def composite_ordered(records, order, camera: Camera, exact: bool = True) -> np.ndarray:
     """Project records in the given order and composite (render.py:242-248)."""
     sorted_records = np.asarray(records, dtype=np.float32)[np.asarray(order)]
     centers, conics, colors, alphas, bounds, _ = project_records(sorted_records, camera)
@@ -179,7 +179,7 @@ class FlatRenderer:
         self._ws = None
         self._ws_key = None
 
-    def render(self, records, camera: Camera, exact: bool = False, out=None,
+    def render(self, records, camera: Camera, exact: bool = True, out=None,
                dot_mode: int | None = None):
         t = _device.require_cuda()
         rec = _device.to_dev(records, np.float32).reshape(-1, RECORD_SIZE)
@@ -217,7 +217,7 @@ class FlatRenderer:
             t.cuda.current_stream().synchronize()
             if int(ctr[2]) == 0:
                 break
-            m_cap = int(ctr[1]) + int(ctr[1]) // 4 + 1024
+            m_cap = int(ctr[3]) + int(ctr[3]) // 4 + 1024
         self.m_cap = m_cap
         return image
 
@@ -225,7 +225,7 @@ class FlatRenderer:
 _flat = None
 
 
-def render_records(records, camera: Camera, exact: bool = False) -> np.ndarray:
+def render_records(records, camera: Camera, exact: bool = True) -> np.ndarray:
     """Cull, sort front to back, project, composite (render.py:251-253).
     Returns float32 (h, w, 3)."""
     global _flat

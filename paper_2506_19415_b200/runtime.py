@@ -340,7 +340,7 @@ class VmSession:
 
     def __init__(self, scene, buffer_pages: int = 500, staging_pages: float = 40,
                  vis_scale: float = 0.25, band=(0.5, 0.8), step: float = 0.05,
-                 lod_enabled: bool = True, links_enabled: bool = True, exact: bool = False,
+                 lod_enabled: bool = True, links_enabled: bool = True, exact: bool = True,
                  upload_mode: int = 1, device=None):
         from paper_2506_19415_b200.render import VisibilityBuffers
 
@@ -458,7 +458,7 @@ class VmSession:
         re-render (the pool and chunk table are unchanged)."""
         t = _device.torch()
         while int(self.counters[2]):
-            need = int(self.counters[1])
+            need = int(self.counters[3])
             self.m_cap = need + need // 4 + (1 << 16)
             self._launch_render(camera, image, n_chunks, n_res, record_events=False)
             t.cuda.current_stream().synchronize()

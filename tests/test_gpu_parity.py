@@ -271,7 +271,12 @@ def test_session_matches_reference(cuda, golden, variant, exact):
         stats.append(st)
         assert np.array_equal(np.array(sorted(s.table.resident), np.int64),
                               g[f"{variant}_resident_{f}"]), f
-        assert _maxabs(img, g[f"{variant}_image_{f}"]) <= (EXACT_TOL if exact else FAST_TOL), f
+        ref = g[f"{variant}_image_{f}"]
+        if exact:  # the default, reference-faithful blend
+            assert _maxabs(img, ref) <= EXACT_TOL, f
+        else:  # opt-in FP32 blend: an early-termination flip may exceed 1e-3 in
+            # isolated pixels
+            assert core.psnr(img, ref) >= 50.0 and _maxabs(img, ref) <= 1e-2, f
         s.table.check()
     assert core.stats_csv(stats).encode() == g[f"{variant}_stats"].tobytes()
 
@@ -295,7 +300,7 @@ def test_c1_session_matches_reference(cuda, golden, upload_mode):
         ref, _ = o.render_frame(cam, f)
         assert hashlib.sha256(ref.tobytes()).digest() == g[f"image_sha_{f}"].tobytes()
         stats.append(st)
-        assert _maxabs(img, ref) <= FAST_TOL, f
+        assert _maxabs(img, ref) <= EXACT_TOL, f
         assert core.psnr(img, ref) >= 50.0
     assert core.stats_csv(stats).encode() == g["stats"].tobytes()
 
@@ -330,3 +335,70 @@ def test_session_is_deterministic(cuda):
         outs.append([s.render_frame(path.frame_camera(f), f)[0] for f in range(path.frame_count)])
     for a, b in zip(*outs):
         assert np.array_equal(a, b)
+
+
+# -- BASELINE config 2 at full size ----------------------------------------------
+@pytest.fixture(scope="module")
+def c2_scene(tmp_path_factory):
+    from paper_2506_19415_b200 import scenegen
+    from paper_2506_19415_b200.scene_io import read_scene
+
+    p = tmp_path_factory.mktemp("c2") / "c2.vms"
+    scenegen.write_city(p, scenegen.C2)
+    return read_scene(p, mmap_gaussians=True)
+
+
+def test_c2_frames_match_oracle(cuda, c2_scene):
+    """C2 (2M records, 1000 pages, 3 LOD levels) at 1080p through the first
+    frames of the benchmark trajectory: required lists, plans, residency and
+    stats bit-identical to the oracle, images within 1e-5."""
+    from paper_2506_19415_b200 import scenegen
+    from paper_2506_19415_b200.runtime import VmSession
+
+    traj = scenegen.street_path(scenegen.C2, frames=120)
+    s = VmSession(c2_scene)
+    o = core.OSession(c2_scene)
+    for f in range(3):
+        cam = traj.frame_camera(f)
+        img, st = s.render_frame(cam, f)
+        ref, rst = o.render_frame(cam, f)
+        for k in ("required_pages", "resident_pages", "resident_per_level", "planned_copies",
+                  "missing_pages", "bytes_copied", "usage", "lod_step", "thresholds"):
+            assert st[k] == rst[k], (f, k)
+        assert sorted(s.table.resident.items()) == sorted(o.table.resident.items())
+        assert _maxabs(img, ref) <= EXACT_TOL, f
+
+
+def test_c2_paging_matches_oracle_whole_trajectory(cuda, c2_scene):
+    """All 120 frames of the benchmark path: the device visibility + LOD +
+    C++ page table reproduce the oracle's page decisions frame by frame
+    (images skipped on the CPU side: the oracle runs visibility + paging)."""
+    from paper_2506_19415_b200 import scenegen
+    from paper_2506_19415_b200.runtime import VmSession
+
+    traj = scenegen.street_path(scenegen.C2, frames=120)
+    s = VmSession(c2_scene)
+    o = core.OSession(c2_scene)
+    for f in range(traj.frame_count):
+        cam = traj.frame_camera(f)
+        _, st = s.render_frame(cam, f, out="device")
+        _, rst = o.render_frame(cam, f, want_image=False)
+        for k in ("required_pages", "resident_pages", "resident_per_level", "planned_copies",
+                  "missing_pages", "bytes_copied", "usage", "lod_step", "thresholds"):
+            assert st[k] == rst[k], (f, k)
+
+
+def test_c2_render_is_deterministic(cuda, c2_scene):
+    from paper_2506_19415_b200 import scenegen
+    from paper_2506_19415_b200.runtime import VmSession
+
+    traj = scenegen.street_path(scenegen.C2, frames=120)
+    digests = []
+    for _ in range(2):
+        s = VmSession(c2_scene)
+        h = hashlib.sha256()
+        for f in range(0, 40, 4):
+            img, _ = s.render_frame(traj.frame_camera(f), f)
+            h.update(img.tobytes())
+        digests.append(h.hexdigest())
+    assert digests[0] == digests[1]
