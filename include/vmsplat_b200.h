@@ -140,6 +140,13 @@ typedef struct vms_pagetable vms_pagetable;
 const char* vms_last_error(void);
 int32_t vms_abi_version(void);
 
+/* Per-launch device timing for profiling runs: when enabled every kernel
+ * launch records a CUDA event; the report (CSV "kernel,count,total_us")
+ * attributes consecutive event deltas on a stream to kernels.  Returns the
+ * report length; buf may be NULL to query it. */
+int32_t vms_profile_enable(int32_t on);
+int64_t vms_profile_report(char* buf, int64_t len);
+
 /* ---- kernel-level drop-ins (pkg/src/vmsplat/kernels/__init__.py) ------ */
 
 /* composite_splats (kernels/__init__.py:24-33, _core.pyx:24-78): blend n

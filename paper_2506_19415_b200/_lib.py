@@ -71,6 +71,8 @@ class Copy(ctypes.Structure):
 SIGNATURES = {
     "vms_last_error": (ctypes.c_char_p, []),
     "vms_abi_version": (I32, []),
+    "vms_profile_enable": (I32, [I32]),
+    "vms_profile_report": (I64, [P, I64]),
     "vms_composite_workspace_bytes": (SZ, [I64, I64, I32, I32]),
     "vms_composite_splats": (I32, [P, P, P, P, P, I64, I64, P, I32, I32, I32, P, SZ, P]),
     "vms_rasterize_workspace_bytes": (SZ, [I64]),
@@ -134,6 +136,14 @@ def check(status: int, what: str = "") -> None:
     if status == VMS_ERR_NOMEM:
         raise MemoryError(text)
     raise CudaError(text)
+
+
+def profile_report() -> str:
+    lib = load()
+    n = lib.vms_profile_report(None, 0)
+    buf = ctypes.create_string_buffer(int(n) + 1)
+    lib.vms_profile_report(buf, n + 1)
+    return buf.value.decode()
 
 
 def ptr(t) -> int | None:

@@ -2,6 +2,10 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+#include <algorithm>
 
 #include "common.cuh"
 #include "prims.h"
@@ -22,6 +26,29 @@ void set_error(const char* fmt, ...) {
 int32_t cuda_status(cudaError_t e, const char* where) {
   set_error("%s: %s", where, cudaGetErrorString(e));
   return e == cudaErrorMemoryAllocation ? VMS_ERR_NOMEM : VMS_ERR_CUDA;
+}
+
+bool g_profile = false;
+namespace {
+struct Mark {
+  const char* name;
+  cudaStream_t stream;
+  cudaEvent_t ev;
+};
+std::vector<Mark> g_marks;
+std::vector<cudaEvent_t> g_event_pool;
+size_t g_pool_used = 0;
+}  // namespace
+
+void mark_impl(const char* name, cudaStream_t s) {
+  if (g_pool_used == g_event_pool.size()) {
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) return;
+    g_event_pool.push_back(e);
+  }
+  cudaEvent_t e = g_event_pool[g_pool_used++];
+  cudaEventRecord(e, s);
+  g_marks.push_back({name, s, e});
 }
 
 namespace {
@@ -90,6 +117,47 @@ using namespace vms;
 extern "C" {
 
 const char* vms_last_error(void) { return g_err; }
+
+int32_t vms_profile_enable(int32_t on) {
+  g_profile = on != 0;
+  g_marks.clear();
+  g_pool_used = 0;
+  return VMS_OK;
+}
+
+int64_t vms_profile_report(char* buf, int64_t len) {
+  // per kernel name: count and summed device time (us) between a mark and the
+  // previous mark on the same stream ("begin" marks open a sequence)
+  std::vector<std::pair<std::string, std::pair<int64_t, double>>> agg;
+  std::map<cudaStream_t, cudaEvent_t> last;
+  for (const Mark& m : g_marks) {
+    cudaEventSynchronize(m.ev);
+    auto it = last.find(m.stream);
+    if (it != last.end() && std::strcmp(m.name, "begin") != 0) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, it->second, m.ev);
+      size_t k = 0;
+      while (k < agg.size() && agg[k].first != m.name) ++k;
+      if (k == agg.size()) agg.push_back({m.name, {0, 0.0}});
+      agg[k].second.first += 1;
+      agg[k].second.second += 1e3 * ms;
+    }
+    last[m.stream] = m.ev;
+  }
+  std::string out;
+  char line[256];
+  for (auto& a : agg) {
+    snprintf(line, sizeof(line), "%s,%lld,%.3f\n", a.first.c_str(), (long long)a.second.first,
+             a.second.second);
+    out += line;
+  }
+  if (buf && len > 0) {
+    const size_t n = std::min<size_t>(out.size(), (size_t)len - 1);
+    std::memcpy(buf, out.data(), n);
+    buf[n] = 0;
+  }
+  return (int64_t)out.size();
+}
 
 int32_t vms_abi_version(void) { return VMS_ABI_VERSION; }
 
@@ -256,12 +324,14 @@ int32_t vms_upload_pages(const vms_copy* copies, int64_t n, const void* host_bas
                                copies[i].nbytes, cudaMemcpyHostToDevice, s));
     return VMS_OK;
   }
+  mark("begin", s);
   int vec16 = 1;
   for (int64_t i = 0; i < n; ++i)
     vec16 &= ((copies[i].src_offset | copies[i].dst_offset | copies[i].nbytes) & 15u) == 0;
   dim3 grid(64, (unsigned)(n < 65535 ? n : 65535));
   upload_k<<<grid, 256, 0, s>>>(copies, n, static_cast<const char*>(host_base),
                                 static_cast<char*>(dev_base), vec16);
+  mark("upload", s);
   VMS_LAUNCH_CHECK("upload_pages");
   return VMS_OK;
 }
@@ -282,6 +352,7 @@ int32_t vms_render(const vms_render_args* a, void* stream) {
   const uint32_t tiles =
       (uint32_t)(ceil_div(a->cam.width, kTile) * ceil_div(a->cam.height, kTile));
   RenderWs w = render_carve(a->workspace, a->n_cap, a->m_cap, tiles);
+  mark("begin", s);
   int32_t st = render_preprocess(a->pool, a->chunks, a->n_chunks, a->cam, w, s);
   if (st) return st;
   if (a->events[0]) VMS_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(a->events[0]), s));

@@ -256,10 +256,13 @@ int32_t tiles_and_blend(const RenderCamera& cam, const uint32_t* vals, const Ren
   const uint32_t n_tiles = (uint32_t)tiles_x * tiles_y;
   const int T = 256;
   dup_count_k<<<4 * kSMs, T, 0, s>>>(vals, w.rec, w.ctr, w.cnt);
+  mark("dup_count", s);
   int32_t st = scan_exclusive_u32(w.cnt, w.off, &w.ctr->n_kept, 0, &w.ctr->n_inst, w.scan_ws, s);
   if (st) return st;
   dup_emit_k<<<4 * kSMs, T, 0, s>>>(vals, w.rec, w.off, w.ctr, w.m_cap, tiles_x, w.tk0, w.tv0);
+  mark("dup_emit", s);
   clamp_inst_k<<<1, 1, 0, s>>>(w.ctr, w.m_cap);
+  mark("clamp", s);
   int alt = 0;
   st = radix_sort_u32(w.tk0, w.tv0, w.tk1, w.tv1, &w.ctr->n_inst, 0, 0, tile_bits(n_tiles), &alt,
                       w.radix_ws, s);
@@ -268,6 +271,7 @@ int32_t tiles_and_blend(const RenderCamera& cam, const uint32_t* vals, const Ren
   const uint32_t* tv = alt ? w.tv1 : w.tv0;
   VMS_CUDA(cudaMemsetAsync(w.ranges, 0, sizeof(uint32_t) * 2 * n_tiles, s));
   ranges_k<<<8 * kSMs, T, 0, s>>>(tk, w.ctr, w.ranges);
+  mark("ranges", s);
   if (events && events[2]) VMS_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(events[2]), s));
   if (exact)
     blend_k<true><<<n_tiles, kBlendThreads, 0, s>>>(w.ranges, tv, w.rec, cam.width, cam.height,
@@ -275,6 +279,7 @@ int32_t tiles_and_blend(const RenderCamera& cam, const uint32_t* vals, const Ren
   else
     blend_k<false><<<n_tiles, kBlendThreads, 0, s>>>(w.ranges, tv, w.rec, cam.width, cam.height,
                                                      tiles_x, image, accumulate);
+  mark("blend", s);
   if (events && events[3]) VMS_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(events[3]), s));
   VMS_LAUNCH_CHECK("tiles_and_blend");
   return VMS_OK;
@@ -331,6 +336,7 @@ int32_t render_finish(const RenderCamera& cam, uint32_t n_splats, const RenderWs
     if (st) return st;
     compact_k<<<ceil_div<uint32_t>(n_splats, T), T, 0, s>>>(w.flag, w.pos, w.key_g, n_splats,
                                                              w.k0, w.v0);
+    mark("compact", s);
   }
   int alt = 0;
   // keys are IEEE bits of positive f32 depths: bit 31 is always clear

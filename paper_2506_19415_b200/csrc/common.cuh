@@ -17,6 +17,15 @@ constexpr int kSMs = 148;
 void set_error(const char* fmt, ...);
 int32_t cuda_status(cudaError_t e, const char* where);
 
+// Optional per-launch device timing (vms_profile_enable): records a CUDA
+// event after each kernel; vms_profile_report turns consecutive events on a
+// stream into per-kernel device times.  A no-op unless enabled.
+extern bool g_profile;
+void mark_impl(const char* name, cudaStream_t s);
+inline void mark(const char* name, cudaStream_t s) {
+  if (g_profile) mark_impl(name, s);
+}
+
 #define VMS_CUDA(call)                                         \
   do {                                                         \
     cudaError_t _e = (call);                                   \

@@ -251,6 +251,7 @@ int32_t render_preprocess(const float* pool, const Chunk* chunks, uint32_t n_chu
                           const RenderCamera& cam, const RenderWs& w, cudaStream_t s) {
   if (n_chunks == 0) return VMS_OK;
   preprocess_k<<<n_chunks, kChunkRecords, 0, s>>>(pool, chunks, cam, w.key_g, w.flag, w.rec);
+  mark("preprocess", s);
   VMS_LAUNCH_CHECK("render_preprocess");
   return VMS_OK;
 }

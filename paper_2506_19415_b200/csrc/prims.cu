@@ -229,8 +229,11 @@ int32_t scan_exclusive_u32(const uint32_t* in, uint32_t* out, const uint32_t* n_
                            uint32_t n_host, uint32_t* total, void* ws, cudaStream_t s) {
   uint32_t* partial = static_cast<uint32_t*>(ws);
   scan_reduce_k<<<kPrimGrid, kScanBlock, 0, s>>>(in, n_dev, n_host, partial);
+  mark("scan_reduce", s);
   scan_single_k<<<1, kScanBlock, 0, s>>>(partial, kPrimGrid, total);
+  mark("scan_single", s);
   scan_down_k<<<kPrimGrid, kScanBlock, 0, s>>>(in, out, n_dev, n_host, partial);
+  mark("scan_down", s);
   VMS_LAUNCH_CHECK("scan_exclusive_u32");
   return VMS_OK;
 }
@@ -250,6 +253,7 @@ int32_t radix_sort_u32(uint32_t* k0, uint32_t* v0, uint32_t* k1, uint32_t* v1,
     uint32_t *ki = alt ? k1 : k0, *vi = alt ? v1 : v0;
     uint32_t *ko = alt ? k0 : k1, *vo = alt ? v0 : v1;
     radix_upsweep_k<<<kPrimGrid, kRBlock, 0, s>>>(ki, n_dev, n_host, b, mask, counts);
+    mark("radix_up", s);
     // digit-major counts -> global (digit, block) offsets; only the digits
     // this pass can produce are scanned
     int32_t st = scan_exclusive_u32(counts, counts, nullptr, (mask + 1u) * kPrimGrid, nullptr,
@@ -257,6 +261,7 @@ int32_t radix_sort_u32(uint32_t* k0, uint32_t* v0, uint32_t* k1, uint32_t* v1,
     if (st) return st;
     radix_downsweep_k<<<kPrimGrid, kRBlock, 0, s>>>(ki, vi, ko, vo, n_dev, n_host, b, mask,
                                                     counts);
+    mark("radix_down", s);
     alt ^= 1;
   }
   VMS_LAUNCH_CHECK("radix_sort_u32");

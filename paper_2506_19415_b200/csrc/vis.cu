@@ -377,33 +377,40 @@ int32_t vis_frame(const VisArgs& a, cudaStream_t s) {
   }
   VisWs w = carve_ws(a.workspace, a.n_faces, a.page_count);
   const int T = 256;
+  mark("begin", s);
   VMS_CUDA(cudaMemsetAsync(w.n_tris, 0, sizeof(uint32_t) * 4, s));
   VMS_CUDA(cudaMemsetAsync(w.base, 0, sizeof(uint32_t) * (a.page_count + 1), s));
   VMS_CUDA(cudaMemsetAsync(w.direct, 0, a.page_count + 1, s));
   if (a.n_faces) {
     vis_count_k<<<ceil_div<uint32_t>(a.n_faces, T), T, 0, s>>>(a.cam, a.verts, a.faces,
                                                                 a.n_faces, w.counts);
+    mark("vis_count", s);
     int32_t st = scan_exclusive_u32(w.counts, w.offsets, nullptr, a.n_faces, w.n_tris, w.scan, s);
     if (st) return st;
     vis_emit_k<<<ceil_div<uint32_t>(a.n_faces, T), T, 0, s>>>(
         a.cam, a.verts, a.faces, a.face_page, a.n_faces, w.offsets, w.tris);
+    mark("vis_emit", s);
   }
   dim3 grid(ceil_div(a.cam.width, kVisTile), ceil_div(a.cam.height, kVisTile));
   vis_raster_k<<<grid, kVisThreads, 0, s>>>(w.tris, w.n_tris, 0, a.cam.width, a.cam.height,
                                             a.id_image, a.invz_image, 0, a.page_count,
                                             w.base, w.direct, w.err);
+  mark("vis_raster", s);
   VMS_CUDA(cudaMemcpyAsync(w.depth, w.base, sizeof(uint32_t) * (a.page_count + 1),
                            cudaMemcpyDeviceToDevice, s));
   if (a.page_count) {
     vis_links_k<<<ceil_div<uint32_t>(a.page_count * 32, T), T, 0, s>>>(
         w.base, w.depth, w.direct, a.link_off, a.link_tgt, a.page_count);
+    mark("vis_links", s);
   }
   vis_flags_k<<<ceil_div<uint32_t>(a.page_count + 1, T), T, 0, s>>>(w.depth, a.page_count,
                                                                      w.pos);
+  mark("vis_flags", s);
   int32_t st = scan_exclusive_u32(w.pos, w.pos, nullptr, a.page_count + 1, w.n_req, w.scan, s);
   if (st) return st;
   vis_required_k<<<ceil_div<uint32_t>(a.page_count + 1, T), T, 0, s>>>(
       w.depth, w.direct, w.pos, a.page_count, a.lod, a.out);
+  mark("vis_required", s);
   if (a.out.meta) {
     VMS_CUDA(cudaMemcpyAsync(a.out.meta, w.n_tris, sizeof(uint32_t) * 4,
                              cudaMemcpyDeviceToHost, s));
