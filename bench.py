@@ -175,8 +175,10 @@ def run_ours(args, rank, world, local_rank):
     scene = read_scene(path, mmap_gaussians=True)
     traj = scenegen.street_path(lay, frames=args.frames, width=args.width, height=args.height)
     F = traj.frame_count
-    start = rank * F // world
-    block = max(1, (rank + 1) * F // world - start)
+    from paper_2506_19415_b200.sharding import frame_block
+
+    start, stop = frame_block(rank, world, F)
+    block = max(1, stop - start)
     holder = {}
     step = [0]
 
@@ -227,13 +229,11 @@ def run_ours(args, rank, world, local_rank):
     sess = holder["s"]
 
     # final NCCL gather of per-frame stats rows and each rank's last image
-    rows = torch.tensor([[s["frame"], s["required_pages"], s["missing_pages"], s["bytes_copied"],
-                          s["resident_pages"]] for s in stats + stats_e2e],
-                        dtype=torch.int64, device="cuda")
+    from paper_2506_19415_b200 import sharding
+
     last = sess.render_frame(traj.frame_camera(start), start + step[0], out="device")[0]
     if dist:
-        allrows = [torch.empty_like(rows) for _ in range(world)] if rank == 0 else None
-        dist.gather(rows, allrows, dst=0)
+        sharding.gather_rows(sharding.stats_rows(stats + stats_e2e), dist, device="cuda")
         imgs = [torch.empty_like(last) for _ in range(world)] if rank == 0 else None
         dist.gather(last.contiguous(), imgs, dst=0)
         dist.barrier()
