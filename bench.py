@@ -182,13 +182,14 @@ def run_ours(args, rank, world, local_rank):
     holder = {}
     step = [0]
 
-    def fresh_session():
-        # same knobs, same warm-up frames: the device-resident and the e2e
-        # timings cover the identical frames with the identical page state
+    def fresh_session(timing=False):
+        # same knobs, same warm-up frames: the device-resident, the e2e and
+        # the stage-timing passes cover identical frames with identical state
         holder.pop("s", None)
         torch.cuda.empty_cache()
         holder["s"] = VmSession(scene, buffer_pages=500, staging_pages=40, vis_scale=0.25,
-                                exact=not args.fast, upload_mode=args.upload_mode)
+                                exact=not args.fast, upload_mode=args.upload_mode,
+                                timing=timing)
         step[0] = 0
         for _ in range(args.warmup):
             frame("device")
@@ -212,6 +213,7 @@ def run_ours(args, rank, world, local_rank):
         sts = [frame(out)[1] for _ in range(args.steps)]
         e1.record(stream)
         torch.cuda.synchronize()
+        holder["s"].flush()
         ms = e0.elapsed_time(e1)
         if dist:
             t = torch.tensor([ms], device="cuda")
@@ -226,6 +228,10 @@ def run_ours(args, rank, world, local_rank):
     pinned = torch.empty((args.height, args.width, 3), dtype=torch.float32).pin_memory()
     fresh_session()
     ms_e2e, stats_e2e = timed(pinned.numpy())
+    # third pass over the same frames with per-stage CUDA events (one sync per
+    # frame): the stage breakdown and the roofline come from here
+    fresh_session(timing=True)
+    _, stats_t = timed("device")
     sess = holder["s"]
 
     # final NCCL gather of per-frame stats rows and each rank's last image
@@ -244,11 +250,11 @@ def run_ours(args, rank, world, local_rank):
 
     hbm, peak_kind = peaks()
     W, H = args.width, args.height
-    blend_s = sum(s["time_blend"] for s in stats)
-    pre_s = sum(s["time_preprocess"] for s in stats)
-    blend_bytes = sum(s["n_instances"] * (4 + 48) + W * H * 12 for s in stats)
-    pre_bytes = sum(s["n_resident_records"] * (236 + 4 + 4) + s["n_kept"] * 48 for s in stats)
-    stages = {k: 1e3 * statistics.mean(s[f"time_{k}"] for s in stats)
+    blend_s = sum(s["time_blend"] for s in stats_t)
+    pre_s = sum(s["time_preprocess"] for s in stats_t)
+    blend_bytes = sum(s["n_instances"] * (4 + 48) + W * H * 12 for s in stats_t)
+    pre_bytes = sum(s["n_resident_records"] * (236 + 4 + 4) + s["n_kept"] * 48 for s in stats_t)
+    stages = {k: 1e3 * statistics.mean(s[f"time_{k}"] for s in stats_t)
               for k in ("visibility", "update", "copy", "sort", "render", "preprocess", "tiles",
                         "blend", "device_frame")}
     dominant = "blend" if blend_s >= pre_s else "preprocess"
@@ -263,8 +269,8 @@ def run_ours(args, rank, world, local_rank):
             traffic = json.load(open(tf)).get(dominant)
         except ValueError:
             traffic = None
-    up_bytes = sum(s["bytes_copied"] for s in stats)
-    up_s = sum(s["time_copy"] for s in stats if s["bytes_copied"])
+    up_bytes = sum(s["bytes_copied"] for s in stats_t)
+    up_s = sum(s["time_copy"] for s in stats_t if s["bytes_copied"])
     value = world * args.steps / (ms_dev / 1e3)
     e2e = world * args.steps / (ms_e2e / 1e3)
     launches = sum(launches_per_frame(s, len(scene.faces), args.upload_mode) for s in stats)
@@ -290,9 +296,9 @@ def run_ours(args, rank, world, local_rank):
                      "frac": round(ach / hbm, 4), "traffic": traffic},
         "stages_ms": {k: round(v, 4) for k, v in stages.items()},
         "upload": {"gbs": round(up_bytes / up_s / 1e9, 2) if up_s else None,
-                   "bytes": up_bytes, "frames_with_copies": sum(1 for s in stats if s["bytes_copied"])},
-        "mean_instances": int(statistics.mean(s["n_instances"] for s in stats)),
-        "mean_resident_records": int(statistics.mean(s["n_resident_records"] for s in stats)),
+                   "bytes": up_bytes, "frames_with_copies": sum(1 for s in stats_t if s["bytes_copied"])},
+        "mean_instances": int(statistics.mean(s["n_instances"] for s in stats_t)),
+        "mean_resident_records": int(statistics.mean(s["n_resident_records"] for s in stats_t)),
         "gpu_launches": int(launches),
         "clocks": clocks,
     }

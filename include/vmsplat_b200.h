@@ -139,6 +139,8 @@ typedef struct vms_pagetable vms_pagetable;
 /* ---- library --------------------------------------------------------- */
 const char* vms_last_error(void);
 int32_t vms_abi_version(void);
+/* Edge (pixels) of the square blend tiles: 32, or 16 with VMSPLAT_TILE=16. */
+int32_t vms_tile_size(void);
 
 /* Per-launch device timing for profiling runs: when enabled every kernel
  * launch records a CUDA event; the report (CSV "kernel,count,total_us")
@@ -244,6 +246,82 @@ int32_t vms_pt_resident_counts(const vms_pagetable* pt, int64_t* counts, int32_t
 int32_t vms_pt_check(const vms_pagetable* pt);
 int64_t vms_pt_chunks(const vms_pagetable* pt, int64_t page_size, vms_chunk* out, int64_t cap,
                       int64_t* n_records);
+
+/* ---- whole frames: VmSession (runtime.py:393-489) -------------------------
+ * One host call per frame: visibility -> (event sync) -> page table ->
+ * uploads on a side stream -> chunk table -> render.  The session owns the
+ * page table, two CUDA events/streams and small pinned buffers; the caller
+ * owns the big buffers (pool, workspaces, the pinned host scene). */
+typedef struct vms_session vms_session;
+
+typedef struct vms_session_desc {
+  const float* host_records;    /* [dev-mapped pinned] the GAUS section, all levels */
+  uint64_t host_rows;
+  uint32_t page_size;
+  uint32_t lod_levels;          /* levels stored in the scene */
+  uint32_t page_counts[16];     /* pages per level (scene_io.py:144-157) */
+  uint32_t page_count;          /* level-0 pages P */
+  uint32_t n_faces;
+  const double* verts;          /* [dev] */
+  const int32_t* faces;         /* [dev] */
+  const uint32_t* face_page;    /* [dev] */
+  const uint32_t* link_off;     /* [dev] (P + 1,) - all zero when links are disabled */
+  const uint32_t* link_tgt;     /* [dev] */
+  float* pool;                  /* [dev] capacity * page_size rows of 59 f32 */
+  uint32_t capacity;            /* buffer_pages */
+  uint32_t m_cap;               /* tile-instance capacity of render_ws */
+  void* vis_ws;                 /* [dev] vms_visibility_workspace_bytes(n_faces, P) */
+  void* render_ws;              /* [dev] vms_session_render_ws_bytes(...) */
+  uint64_t render_ws_bytes;
+  int32_t width;                /* render resolution render_ws is sized for */
+  int32_t height;
+  int32_t exact;                /* 1: FP64 blend */
+  int32_t upload_mode;          /* see vms_upload_pages */
+} vms_session_desc;
+
+typedef struct vms_frame_args {
+  vms_camera cam;               /* render camera */
+  vms_camera vis_cam;           /* camera.scaled(vis_scale) */
+  vms_lod lod;                  /* controller thresholds before this frame's adaptation */
+  int64_t frame;
+  double budget;                /* staging_pages */
+  float* image;                 /* [dev] (h, w, 3) */
+  float* host_image;            /* [host pinned] optional: D2H + sync at the end */
+  int32_t timing;               /* 1: stage CUDA events + sync at the end */
+  int32_t pad_;
+} vms_frame_args;
+
+typedef struct vms_frame_stats {
+  uint32_t required;            /* len(required_ids) */
+  uint32_t resident;            /* len(table.resident) */
+  uint32_t planned;             /* len(plan) */
+  uint32_t missing;
+  uint64_t bytes_copied;
+  uint32_t occupied_entries;    /* usage = occupied_entries / capacity */
+  uint32_t capacity;
+  uint32_t n_tris, n_chunks, n_res;
+  uint32_t n_kept, n_inst, overflow, n_need;  /* valid when the call synchronised */
+  uint32_t pad_;
+  int64_t resident_per_level[16];
+  float ms_vis, ms_copy, ms_preprocess, ms_sort, ms_tiles, ms_blend, ms_frame, ms_pad;
+  double host_update_s;
+} vms_frame_stats;
+
+size_t vms_session_render_ws_bytes(uint32_t capacity, uint32_t page_size, uint32_t m_cap,
+                                   int32_t width, int32_t height);
+vms_session* vms_session_create(const vms_session_desc* desc);
+void vms_session_destroy(vms_session* s);
+vms_pagetable* vms_session_table(vms_session* s);
+int32_t vms_session_set_render_ws(vms_session* s, void* ws, uint64_t bytes, uint32_t m_cap,
+                                  int32_t width, int32_t height);
+/* VMS_ERR_NOMEM: the tile-instance buffer overflowed (stats->n_need says how
+ * many are needed) - either in this frame (when the call synchronised) or in
+ * the previous one; grow the workspace, vms_session_rerender(), and for a
+ * previous-frame overflow repeat this call (nothing was mutated). */
+int32_t vms_session_frame(vms_session* s, const vms_frame_args* args, vms_frame_stats* stats,
+                          void* stream);
+int32_t vms_session_rerender(vms_session* s, float* host_image, void* stream);
+int32_t vms_session_counters(vms_session* s, uint32_t* out4, void* stream);
 
 #ifdef __cplusplus
 }

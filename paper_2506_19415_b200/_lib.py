@@ -67,10 +67,39 @@ class Copy(ctypes.Structure):
                 ("nbytes", ctypes.c_uint64)]
 
 
+class SessionDesc(ctypes.Structure):
+    _fields_ = [("host_records", P), ("host_rows", ctypes.c_uint64), ("page_size", U32),
+                ("lod_levels", U32), ("page_counts", U32 * 16), ("page_count", U32),
+                ("n_faces", U32), ("verts", P), ("faces", P), ("face_page", P),
+                ("link_off", P), ("link_tgt", P), ("pool", P), ("capacity", U32),
+                ("m_cap", U32), ("vis_ws", P), ("render_ws", P),
+                ("render_ws_bytes", ctypes.c_uint64), ("width", I32), ("height", I32),
+                ("exact", I32), ("upload_mode", I32)]
+
+
+class FrameArgs(ctypes.Structure):
+    _fields_ = [("cam", Camera), ("vis_cam", Camera), ("lod", Lod), ("frame", I64),
+                ("budget", D), ("image", P), ("host_image", P), ("timing", I32),
+                ("pad_", I32)]
+
+
+class FrameStats(ctypes.Structure):
+    _fields_ = [("required", U32), ("resident", U32), ("planned", U32), ("missing", U32),
+                ("bytes_copied", ctypes.c_uint64), ("occupied_entries", U32),
+                ("capacity", U32), ("n_tris", U32), ("n_chunks", U32), ("n_res", U32),
+                ("n_kept", U32), ("n_inst", U32), ("overflow", U32), ("n_need", U32),
+                ("pad_", U32), ("resident_per_level", I64 * 16), ("ms_vis", ctypes.c_float),
+                ("ms_copy", ctypes.c_float), ("ms_preprocess", ctypes.c_float),
+                ("ms_sort", ctypes.c_float), ("ms_tiles", ctypes.c_float),
+                ("ms_blend", ctypes.c_float), ("ms_frame", ctypes.c_float),
+                ("ms_pad", ctypes.c_float), ("host_update_s", D)]
+
+
 # name -> (restype, argtypes); every symbol include/vmsplat_b200.h declares
 SIGNATURES = {
     "vms_last_error": (ctypes.c_char_p, []),
     "vms_abi_version": (I32, []),
+    "vms_tile_size": (I32, []),
     "vms_profile_enable": (I32, [I32]),
     "vms_profile_report": (I64, [P, I64]),
     "vms_composite_workspace_bytes": (SZ, [I64, I64, I32, I32]),
@@ -100,6 +129,14 @@ SIGNATURES = {
     "vms_pt_resident_counts": (I32, [P, P, I32]),
     "vms_pt_check": (I32, [P]),
     "vms_pt_chunks": (I64, [P, I64, P, I64, ctypes.POINTER(I64)]),
+    "vms_session_render_ws_bytes": (SZ, [U32, U32, U32, I32, I32]),
+    "vms_session_create": (P, [ctypes.POINTER(SessionDesc)]),
+    "vms_session_destroy": (None, [P]),
+    "vms_session_table": (P, [P]),
+    "vms_session_set_render_ws": (I32, [P, P, ctypes.c_uint64, U32, I32, I32]),
+    "vms_session_frame": (I32, [P, ctypes.POINTER(FrameArgs), ctypes.POINTER(FrameStats), P]),
+    "vms_session_rerender": (I32, [P, P, P]),
+    "vms_session_counters": (I32, [P, P, P]),
 }
 
 _lib = None

@@ -27,6 +27,7 @@ UNITS = {
     "prims.cu": [],
     "blend.cu": [],
     "abi.cu": [],
+    "session.cu": [],
 }
 HOST_UNITS = {"pagetable.cpp": ["-O2", "-std=c++17", "-fPIC"]}
 HEADERS = ["common.cuh", "prims.h", "render.h", "vis.h"]

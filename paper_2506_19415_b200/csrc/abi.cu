@@ -161,8 +161,10 @@ int64_t vms_profile_report(char* buf, int64_t len) {
 
 int32_t vms_abi_version(void) { return VMS_ABI_VERSION; }
 
+int32_t vms_tile_size(void) { return tile_size(); }
+
 size_t vms_composite_workspace_bytes(int64_t n, int64_t n_instances, int32_t h, int32_t w) {
-  const uint32_t tiles = (uint32_t)(ceil_div(w, kTile) * ceil_div(h, kTile));
+  const uint32_t tiles = tile_count(w, h);
   return render_ws_bytes((uint32_t)(n > 0 ? n : 1),
                          (uint32_t)(n_instances > 0 ? n_instances : 1), tiles);
 }
@@ -181,7 +183,7 @@ int32_t vms_composite_splats(const float* centers, const float* conics, const fl
     set_error("composite_splats: workspace too small");
     return VMS_ERR_INVALID;
   }
-  const uint32_t tiles = (uint32_t)(ceil_div(w, kTile) * ceil_div(h, kTile));
+  const uint32_t tiles = tile_count(w, h);
   RenderWs ws = render_carve(workspace, (uint32_t)(n > 0 ? n : 1),
                              (uint32_t)(n_instances > 0 ? n_instances : 1), tiles);
   return composite_ordered(centers, conics, colors, alphas, bounds, (uint32_t)n, image, h, w,
@@ -338,7 +340,7 @@ int32_t vms_upload_pages(const vms_copy* copies, int64_t n, const void* host_bas
 
 size_t vms_render_workspace_bytes(uint32_t n_cap, uint32_t m_cap, int32_t width,
                                   int32_t height) {
-  const uint32_t tiles = (uint32_t)(ceil_div(width, kTile) * ceil_div(height, kTile));
+  const uint32_t tiles = tile_count(width, height);
   return render_ws_bytes(n_cap, m_cap, tiles);
 }
 
@@ -350,7 +352,7 @@ int32_t vms_render(const vms_render_args* a, void* stream) {
   }
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const uint32_t tiles =
-      (uint32_t)(ceil_div(a->cam.width, kTile) * ceil_div(a->cam.height, kTile));
+      tile_count(a->cam.width, a->cam.height);
   RenderWs w = render_carve(a->workspace, a->n_cap, a->m_cap, tiles);
   mark("begin", s);
   int32_t st = render_preprocess(a->pool, a->chunks, a->n_chunks, a->cam, w, s);

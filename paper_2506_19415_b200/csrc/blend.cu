@@ -16,15 +16,30 @@
 // Fast mode blends in FP32 (measured <= 2.6e-5 from the FP64 reference,
 // SURVEY A16); exact mode reproduces the reference's FP64 arithmetic with
 // f32 storage of T and colour.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "prims.h"
 #include "render.h"
 
 namespace vms {
 
+int tile_size() {
+  static const int ts = [] {
+    const char* e = std::getenv("VMSPLAT_TILE");
+    return (e && std::atoi(e) == 16) ? 16 : 32;
+  }();
+  return ts;
+}
+
+uint32_t tile_count(int width, int height) {
+  const int t = tile_size();
+  return (uint32_t)(ceil_div(width, t) * ceil_div(height, t));
+}
+
 namespace {
 
-constexpr int kBlendThreads = kTile * kTile;
+constexpr int kBlendThreads = 256;
 
 template <typename T>
 T* carve(char*& p, size_t n) {
@@ -44,21 +59,22 @@ __global__ void compact_k(const uint32_t* __restrict__ flag, const uint32_t* __r
   v0[o] = g;
 }
 
-__device__ __forceinline__ void tile_rect(const BlendRec& r, int* tx0, int* tx1, int* ty0,
-                                          int* ty1) {
+__device__ __forceinline__ void tile_rect(const BlendRec& r, int shift, int* tx0, int* tx1,
+                                          int* ty0, int* ty1) {
   const int x0 = r.bx & 0xFFFF, x1 = r.bx >> 16, y0 = r.by & 0xFFFF, y1 = r.by >> 16;
-  *tx0 = x0 / kTile;
-  *tx1 = (x1 - 1) / kTile;
-  *ty0 = y0 / kTile;
-  *ty1 = (y1 - 1) / kTile;
+  *tx0 = x0 >> shift;
+  *tx1 = (x1 - 1) >> shift;
+  *ty0 = y0 >> shift;
+  *ty1 = (y1 - 1) >> shift;
 }
 
 __global__ void dup_count_k(const uint32_t* __restrict__ vals, const BlendRec* __restrict__ rec,
-                            const RenderCounters* __restrict__ ctr, uint32_t* __restrict__ cnt) {
+                            const RenderCounters* __restrict__ ctr, int shift,
+                            uint32_t* __restrict__ cnt) {
   const uint32_t n = ctr->n_kept;
   for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < n; s += gridDim.x * blockDim.x) {
     int tx0, tx1, ty0, ty1;
-    tile_rect(rec[vals[s]], &tx0, &tx1, &ty0, &ty1);
+    tile_rect(rec[vals[s]], shift, &tx0, &tx1, &ty0, &ty1);
     cnt[s] = (uint32_t)((tx1 - tx0 + 1) * (ty1 - ty0 + 1));
   }
 }
@@ -83,7 +99,7 @@ __device__ __forceinline__ uint32_t last_le(const uint32_t* a, uint32_t n, uint3
 __global__ void __launch_bounds__(kEmitThreads) dup_emit_k(
     const uint32_t* __restrict__ vals, const BlendRec* __restrict__ rec,
     const uint32_t* __restrict__ off, RenderCounters* __restrict__ ctr, uint32_t m_cap,
-    int tiles_x, uint32_t* __restrict__ tk, uint32_t* __restrict__ tv) {
+    int tiles_x, int shift, uint32_t* __restrict__ tk, uint32_t* __restrict__ tv) {
   __shared__ uint32_t soff[kEmitChunk + 1];
   __shared__ uint4 sinfo[kEmitChunk];  // g, tx0, ty0, tiles across
   __shared__ uint32_t span[2];
@@ -98,7 +114,7 @@ __global__ void __launch_bounds__(kEmitThreads) dup_emit_k(
     for (uint32_t j = threadIdx.x; j < ns; j += kEmitThreads) {
       const uint32_t g = vals[s0 + j];
       int tx0, tx1, ty0, ty1;
-      tile_rect(rec[g], &tx0, &tx1, &ty0, &ty1);
+      tile_rect(rec[g], shift, &tx0, &tx1, &ty0, &ty1);
       soff[j] = off[s0 + j];
       sinfo[j] = make_uint4(g, (uint32_t)tx0, (uint32_t)ty0, (uint32_t)(tx1 - tx0 + 1));
     }
@@ -133,82 +149,120 @@ __global__ void ranges_k(const uint32_t* __restrict__ tk, const RenderCounters* 
   }
 }
 
-template <bool kExact>
+// One CTA per TS x TS tile, 256 threads; thread (lx, ly) owns the pixels of
+// column lx at rows ly, ly + 256/TS, ... (PPT = TS*TS/256 pixels).  Splats
+// of the tile's list are staged 256 at a time in shared memory; the per-splat
+// column work (dx, a*dx*dx, FP64 conversions) is shared by a thread's pixels.
+template <bool kExact, int TS>
 __global__ void __launch_bounds__(kBlendThreads) blend_k(const uint32_t* __restrict__ ranges,
                                                          const uint32_t* __restrict__ tv,
                                                          const BlendRec* __restrict__ rec,
                                                          int w, int h, int tiles_x,
                                                          float* __restrict__ image,
                                                          int accumulate) {
+  constexpr int PPT = TS * TS / kBlendThreads;
+  constexpr int ROWS = kBlendThreads / TS;
   __shared__ BlendRec srec[kBlendThreads];
   const int tile = blockIdx.x;
-  const int px = (tile % tiles_x) * kTile + (threadIdx.x % kTile);
-  const int py = (tile / tiles_x) * kTile + (threadIdx.x / kTile);
-  const bool inside = px < w && py < h;
+  const int px = (tile % tiles_x) * TS + (threadIdx.x % TS);
+  const int py0 = (tile / tiles_x) * TS + (threadIdx.x / TS);
   const uint32_t start = ranges[2 * tile], end = ranges[2 * tile + 1];
-  float cr = 0.f, cg = 0.f, cb = 0.f, T = 1.f;
-  if (accumulate && inside) {
-    const float* p = image + ((size_t)py * w + px) * 3;
-    cr = p[0];
-    cg = p[1];
-    cb = p[2];
+  float cr[PPT], cg[PPT], cb[PPT], T[PPT];
+  bool done[PPT];
+  bool all_done = true;
+#pragma unroll
+  for (int k = 0; k < PPT; ++k) {
+    const int py = py0 + k * ROWS;
+    const bool inside = px < w && py < h;
+    cr[k] = cg[k] = cb[k] = 0.f;
+    T[k] = 1.f;
+    if (accumulate && inside) {
+      const float* p = image + ((size_t)py * w + px) * 3;
+      cr[k] = p[0];
+      cg[k] = p[1];
+      cb[k] = p[2];
+    }
+    done[k] = !inside;
+    all_done = all_done && done[k];
   }
-  bool done = !inside;
-  const float fpx = (float)px + 0.5f, fpy = (float)py + 0.5f;
   for (uint32_t base = start; base < end; base += kBlendThreads) {
-    if (__syncthreads_and(done)) break;
+    if (__syncthreads_and(all_done)) break;
     const uint32_t i = base + threadIdx.x;
     if (i < end) srec[threadIdx.x] = rec[tv[i]];
     __syncthreads();
     const int cnt = min((uint32_t)kBlendThreads, end - base);
-    if (!done) {
+    if (!all_done) {
       for (int j = 0; j < cnt; ++j) {
         const BlendRec& s = srec[j];
-        const int x0 = s.bx & 0xFFFF, x1 = s.bx >> 16, y0 = s.by & 0xFFFF, y1 = s.by >> 16;
-        if (px < x0 || px >= x1 || py < y0 || py >= y1) continue;
+        const int x0 = s.bx & 0xFFFF, x1 = s.bx >> 16;
+        if (px < x0 || px >= x1) continue;
+        const int y0 = s.by & 0xFFFF, y1 = s.by >> 16;
         if constexpr (kExact) {
-          const double t = (double)T;
-          if (t < 1.0 / 255.0) {
-            done = true;
-            break;
-          }
+          // _core.pyx:49-78 in FP64 with f32 storage of T and colour
           const double dx = ((double)px + 0.5) - (double)s.cx;
-          const double dy = ((double)py + 0.5) - (double)s.cy;
-          const double sig =
-              -0.5 * (__dadd_rn(__dadd_rn(__dmul_rn(__dmul_rn((double)s.ca, dx), dx),
-                                          __dmul_rn(__dmul_rn(__dmul_rn(2.0, (double)s.cb), dy), dx)),
-                                __dmul_rn(__dmul_rn((double)s.cc, dy), dy)));
-          double wgt = __dmul_rn((double)s.alpha, exp(sig));
-          if (wgt > 0.99) wgt = 0.99;
-          const double wt = __dmul_rn(wgt, t);
-          cr = __double2float_rn(__dadd_rn((double)cr, __dmul_rn(wt, (double)s.r)));
-          cg = __double2float_rn(__dadd_rn((double)cg, __dmul_rn(wt, (double)s.g)));
-          cb = __double2float_rn(__dadd_rn((double)cb, __dmul_rn(wt, (double)s.b)));
-          T = __double2float_rn(__dmul_rn(t, __dsub_rn(1.0, wgt)));
-        } else {
-          if (T < (1.0f / 255.0f)) {
-            done = true;
-            break;
+          const double ddx = __dmul_rn(__dmul_rn((double)s.ca, dx), dx);
+          const double b2 = __dmul_rn(2.0, (double)s.cb);
+          const double cy = (double)s.cy, cc = (double)s.cc, al = (double)s.alpha;
+#pragma unroll
+          for (int k = 0; k < PPT; ++k) {
+            const int py = py0 + k * ROWS;
+            if (done[k] || py < y0 || py >= y1) continue;
+            const double t = (double)T[k];
+            if (t < 1.0 / 255.0) {
+              done[k] = true;
+              continue;
+            }
+            const double dy = ((double)py + 0.5) - cy;
+            const double sig = -0.5 * __dadd_rn(__dadd_rn(ddx, __dmul_rn(__dmul_rn(b2, dy), dx)),
+                                                __dmul_rn(__dmul_rn(cc, dy), dy));
+            double wgt = __dmul_rn(al, exp(sig));
+            if (wgt > 0.99) wgt = 0.99;
+            const double wt = __dmul_rn(wgt, t);
+            cr[k] = __double2float_rn(__dadd_rn((double)cr[k], __dmul_rn(wt, (double)s.r)));
+            cg[k] = __double2float_rn(__dadd_rn((double)cg[k], __dmul_rn(wt, (double)s.g)));
+            cb[k] = __double2float_rn(__dadd_rn((double)cb[k], __dmul_rn(wt, (double)s.b)));
+            T[k] = __double2float_rn(__dmul_rn(t, __dsub_rn(1.0, wgt)));
           }
-          const float dx = fpx - s.cx, dy = fpy - s.cy;
-          const float sig = -0.5f * (s.ca * dx * dx + 2.0f * s.cb * dy * dx + s.cc * dy * dy);
-          const float wgt = fminf(s.alpha * __expf(sig), 0.99f);
-          const float wt = wgt * T;
-          cr += wt * s.r;
-          cg += wt * s.g;
-          cb += wt * s.b;
-          T = T * (1.0f - wgt);
+        } else {
+          const float dx = ((float)px + 0.5f) - s.cx;
+          const float adx = s.ca * dx * dx, bdx = 2.0f * s.cb * dx;
+#pragma unroll
+          for (int k = 0; k < PPT; ++k) {
+            const int py = py0 + k * ROWS;
+            if (done[k] || py < y0 || py >= y1) continue;
+            if (T[k] < (1.0f / 255.0f)) {
+              done[k] = true;
+              continue;
+            }
+            const float dy = ((float)py + 0.5f) - s.cy;
+            const float sig = -0.5f * (adx + bdx * dy + s.cc * dy * dy);
+            const float wgt = fminf(s.alpha * __expf(sig), 0.99f);
+            const float wt = wgt * T[k];
+            cr[k] += wt * s.r;
+            cg[k] += wt * s.g;
+            cb[k] += wt * s.b;
+            T[k] = T[k] * (1.0f - wgt);
+          }
         }
       }
-      if (!done && T < (1.0f / 255.0f)) done = true;
+      all_done = true;
+#pragma unroll
+      for (int k = 0; k < PPT; ++k) {
+        if (!done[k] && T[k] < (1.0f / 255.0f)) done[k] = true;
+        all_done = all_done && done[k];
+      }
     }
     __syncthreads();
   }
-  if (inside) {
-    float* p = image + ((size_t)py * w + px) * 3;
-    p[0] = cr;
-    p[1] = cg;
-    p[2] = cb;
+#pragma unroll
+  for (int k = 0; k < PPT; ++k) {
+    const int py = py0 + k * ROWS;
+    if (px < w && py < h) {
+      float* p = image + ((size_t)py * w + px) * 3;
+      p[0] = cr[k];
+      p[1] = cg[k];
+      p[2] = cb[k];
+    }
   }
 }
 
@@ -252,14 +306,16 @@ int tile_bits(uint32_t n_tiles) {
 int32_t tiles_and_blend(const RenderCamera& cam, const uint32_t* vals, const RenderWs& w,
                         float* image, int accumulate, int exact, void* const* events,
                         cudaStream_t s) {
-  const int tiles_x = ceil_div(cam.width, kTile), tiles_y = ceil_div(cam.height, kTile);
+  const int ts = tile_size(), shift = ts == 16 ? 4 : 5;
+  const int tiles_x = ceil_div(cam.width, ts), tiles_y = ceil_div(cam.height, ts);
   const uint32_t n_tiles = (uint32_t)tiles_x * tiles_y;
   const int T = 256;
-  dup_count_k<<<4 * kSMs, T, 0, s>>>(vals, w.rec, w.ctr, w.cnt);
+  dup_count_k<<<4 * kSMs, T, 0, s>>>(vals, w.rec, w.ctr, shift, w.cnt);
   mark("dup_count", s);
   int32_t st = scan_exclusive_u32(w.cnt, w.off, &w.ctr->n_kept, 0, &w.ctr->n_inst, w.scan_ws, s);
   if (st) return st;
-  dup_emit_k<<<4 * kSMs, T, 0, s>>>(vals, w.rec, w.off, w.ctr, w.m_cap, tiles_x, w.tk0, w.tv0);
+  dup_emit_k<<<4 * kSMs, T, 0, s>>>(vals, w.rec, w.off, w.ctr, w.m_cap, tiles_x, shift, w.tk0,
+                                    w.tv0);
   mark("dup_emit", s);
   clamp_inst_k<<<1, 1, 0, s>>>(w.ctr, w.m_cap);
   mark("clamp", s);
@@ -273,12 +329,10 @@ int32_t tiles_and_blend(const RenderCamera& cam, const uint32_t* vals, const Ren
   ranges_k<<<8 * kSMs, T, 0, s>>>(tk, w.ctr, w.ranges);
   mark("ranges", s);
   if (events && events[2]) VMS_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(events[2]), s));
-  if (exact)
-    blend_k<true><<<n_tiles, kBlendThreads, 0, s>>>(w.ranges, tv, w.rec, cam.width, cam.height,
-                                                    tiles_x, image, accumulate);
-  else
-    blend_k<false><<<n_tiles, kBlendThreads, 0, s>>>(w.ranges, tv, w.rec, cam.width, cam.height,
-                                                     tiles_x, image, accumulate);
+  auto* kern = exact ? (ts == 16 ? blend_k<true, 16> : blend_k<true, 32>)
+                     : (ts == 16 ? blend_k<false, 16> : blend_k<false, 32>);
+  kern<<<n_tiles, kBlendThreads, 0, s>>>(w.ranges, tv, w.rec, cam.width, cam.height, tiles_x,
+                                         image, accumulate);
   mark("blend", s);
   if (events && events[3]) VMS_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(events[3]), s));
   VMS_LAUNCH_CHECK("tiles_and_blend");

@@ -11,7 +11,9 @@ namespace vms {
 
 constexpr int kRecordFloats = 59;   // gaussians.py:1-33
 constexpr int kChunkRecords = 128;  // records per preprocess CTA
-constexpr int kTile = 16;           // blend tile edge (pixels)
+// Blend tile edge in pixels (32 by default; VMSPLAT_TILE=16 selects 16x16).
+int tile_size();
+uint32_t tile_count(int width, int height);
 
 using RenderCamera = vms_camera;
 using Chunk = vms_chunk;

@@ -15,7 +15,6 @@ import numpy as np
 from paper_2506_19415_b200 import _device, _lib
 
 BACKEND = "cuda"
-TILE = 16
 
 
 def _instances(bounds, h, w) -> int:
@@ -27,6 +26,7 @@ def _instances(bounds, h, w) -> int:
     if len(b) == 0:
         return 0
     b = b.astype(np.int64)
+    TILE = int(_lib.load().vms_tile_size())
     x0 = np.maximum(b[:, 0], 0)
     x1 = np.minimum(b[:, 1], w)
     y0 = np.maximum(b[:, 2], 0)

@@ -204,10 +204,23 @@ class PageTable:
         self._cap = int(capacity)
         self._plan_cap = 0
         self._plan = None
+        self._owner = None
+
+    @classmethod
+    def borrowed(cls, handle, capacity: int, owner):
+        """A view of a page table owned by a C++ session (kept alive by owner)."""
+        self = cls.__new__(cls)
+        self._lib = _lib.load()
+        self._h = ctypes.c_void_p(handle)
+        self._cap = int(capacity)
+        self._plan_cap = 0
+        self._plan = None
+        self._owner = owner
+        return self
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h is not None and h.value:
+        if h is not None and h.value and getattr(self, "_owner", None) is None:
             self._lib.vms_pt_destroy(h)
             self._h = None
 
@@ -330,23 +343,30 @@ class ProxyMesh:
 
 class VmSession:
     """Owns the page table, the device page pool and the controller across
-    frames (runtime.py:393-434).
+    frames (runtime.py:393-434).  Each ``render_frame`` is ONE call into the
+    C++ session (csrc/session.cu): visibility -> event sync -> page table ->
+    uploads (side stream) -> chunk table -> render; the FP64 LOD controller
+    adapts on the host afterwards, exactly as the reference orders it.
 
-    Extra (non-reference) knobs: ``exact`` blends in FP64 with the
-    reference's arithmetic; ``upload_mode`` 1 uploads a frame's pages with a
-    single gather kernel over mapped pinned memory, 0 with one
-    cudaMemcpyAsync per page; ``device`` selects the GPU.
+    Extra (non-reference) knobs: ``exact`` (default) blends with the
+    reference's FP64 arithmetic, False selects the FP32 blend;
+    ``upload_mode`` 1 uploads a frame's pages with one gather kernel over
+    mapped pinned memory, 0 with one cudaMemcpyAsync per page; ``timing``
+    records per-stage CUDA events (the stats' time_* keys; costs one sync per
+    frame); ``device`` selects the GPU.
     """
 
     def __init__(self, scene, buffer_pages: int = 500, staging_pages: float = 40,
                  vis_scale: float = 0.25, band=(0.5, 0.8), step: float = 0.05,
                  lod_enabled: bool = True, links_enabled: bool = True, exact: bool = True,
-                 upload_mode: int = 1, device=None):
+                 upload_mode: int = 1, timing: bool = True, device=None):
         from paper_2506_19415_b200.render import VisibilityBuffers
 
         t = _device.require_cuda()
         if scene.page_count == 0:
             raise InvariantViolation("scene has no pages; run paging first")
+        if scene.lod_levels > 16:
+            raise InvariantViolation("at most 16 LOD levels are supported")
         self.device = t.device("cuda", t.cuda.current_device()) if device is None else \
             t.device(device)
         self.scene = scene
@@ -360,14 +380,17 @@ class VmSession:
         self.controller = LodController(initial_thresholds(radius, level_count), step=step,
                                         band_low=band[0], band_high=band[1])
         self.lod_enabled = lod_enabled and level_count > 1
-        self.table = PageTable(buffer_pages)
         self.staging_pages = staging_pages
         self.vis_scale = vis_scale
         self.exact = bool(exact)
         self.upload_mode = int(upload_mode)
+        self.timing = bool(timing)
         self.page_size = int(scene.page_size)
+        self.capacity = int(buffer_pages)
+        if buffer_pages < 1:
+            raise InvariantViolation("page table needs at least one entry")
         self.dot_mode, self.dot_mode_exact = _device.probe_dot_mode()
-
+        self._lib = _lib.load()
         with t.cuda.device(self.device):
             if links_enabled:
                 off = np.asarray(scene.link_offsets, np.uint32)
@@ -377,27 +400,49 @@ class VmSession:
                 tgt = np.zeros(0, np.uint32)
             self.vis = VisibilityBuffers(self.mesh.vertices, self.mesh.faces, self.mesh.face_page,
                                          scene.page_count, off, tgt)
-            # device page pool: capacity entries of page_size records
-            self.n_cap = buffer_pages * self.page_size
+            self.n_cap = self.capacity * self.page_size
             self.pool = t.empty((self.n_cap, RECORD_SIZE), dtype=t.float32, device=self.device)
-            # shared pinned host copy of every level's records (the streaming source)
-            self.host = _pinned_records(scene)
+            self.host = _pinned_records(scene)  # the streaming source (pinned, mapped)
             self.m_cap = max(16 * self.n_cap, 1 << 20)
-            self._alloc_render_ws()
-            max_chunks = buffer_pages * (-(-self.page_size // CHUNK) + (1 << max(0, scene.lod_levels - 1)))
-            self.chunks_host = t.zeros((max_chunks, 4), dtype=t.int32).pin_memory()
-            self.chunks_dev = t.zeros((max_chunks, 4), dtype=t.int32, device=self.device)
-            self.copies_host = t.zeros((scene.page_count + 1, 3), dtype=t.int64).pin_memory()
-            self.counters = t.zeros(4, dtype=t.int32).pin_memory()
-            self.copy_stream = t.cuda.Stream(device=self.device)
-            ev = lambda: t.cuda.Event(enable_timing=True)  # noqa: E731
-            self.ev = {k: ev() for k in ("start", "vis", "req", "copy0", "copy1", "render0",
-                                         "pre", "sorted", "blend0", "blend1", "end")}
-            self.ev_copy_done = t.cuda.Event()
-            for e in self.ev.values():  # torch creates CUDA events lazily
-                e.record(t.cuda.current_stream())
-        self._last_render = None  # args of the last render, for overflow recovery
-        self.frame_log = []
+            self._ws_res = None
+            self.render_ws = None
+            d = _lib.SessionDesc()
+            d.host_records = self.host.data_ptr()
+            d.host_rows = int(len(scene.gaussians))
+            d.page_size = self.page_size
+            d.lod_levels = int(scene.lod_levels)
+            for k, c in enumerate(scene.page_counts):
+                d.page_counts[k] = int(c)
+            d.page_count = int(scene.page_count)
+            d.n_faces = self.vis.n_faces
+            d.verts = self.vis.verts.data_ptr()
+            d.faces = self.vis.faces.data_ptr()
+            d.face_page = self.vis.face_page.data_ptr()
+            d.link_off = self.vis.link_off.data_ptr()
+            d.link_tgt = self.vis.link_tgt.data_ptr()
+            d.pool = self.pool.data_ptr()
+            d.capacity = self.capacity
+            d.vis_ws = self.vis.ws.data_ptr()
+            d.exact = int(self.exact)
+            d.upload_mode = self.upload_mode
+            self._desc = d
+            self._h = None
+            self._ensure_ws(256, 256)  # resized on the first frame
+            h = self._lib.vms_session_create(ctypes.byref(d))
+            if not h:
+                raise InvariantViolation(self._lib.vms_last_error().decode())
+            self._h = ctypes.c_void_p(h)
+            self.table = PageTable.borrowed(self._lib.vms_session_table(self._h),
+                                            self.capacity, self)
+        self._args = _lib.FrameArgs()
+        self._stats = _lib.FrameStats()
+        self._pinned_out = None
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            self._lib.vms_session_destroy(h)
+            self._h = None
 
     # reference attribute: per-page link arrays
     @property
@@ -412,171 +457,145 @@ class VmSession:
     def buffer(self):
         return self.pool
 
-    def _alloc_render_ws(self):
-        t = _device.torch()
-        sc = self.scene
-        self._ws_res = None
-        self.render_ws = None
-        self._ws_for = None
-
-    def _ensure_render_ws(self, width, height):
+    def _ensure_ws(self, width, height):
         t = _device.torch()
         key = (width, height, self.m_cap)
-        if self._ws_for != key:
-            nbytes = _lib.load().vms_render_workspace_bytes(self.n_cap, self.m_cap, width, height)
-            self.render_ws = None
-            self.render_ws = t.empty(nbytes, dtype=t.uint8, device=self.device)
-            self._ws_for = key
+        if self._ws_res == key:
+            return
+        nbytes = self._lib.vms_session_render_ws_bytes(self.capacity, self.page_size, self.m_cap,
+                                                       width, height)
+        self.render_ws = None
+        self.render_ws = t.empty(nbytes, dtype=t.uint8, device=self.device)
+        self._ws_res = key
+        self._desc.render_ws = self.render_ws.data_ptr()
+        self._desc.render_ws_bytes = nbytes
+        self._desc.m_cap = self.m_cap
+        self._desc.width, self._desc.height = width, height
+        if self._h is not None:
+            _lib.check(self._lib.vms_session_set_render_ws(self._h, self.render_ws.data_ptr(),
+                                                           nbytes, self.m_cap, width, height),
+                       "set_render_ws")
 
-    # -- stages ------------------------------------------------------------
-    def _visibility(self, camera):
-        thr = self.controller.thresholds if self.controller.thresholds.size else ()
-        self.vis.launch(camera.scaled(self.vis_scale), thr, self.dot_mode)
-
-    def _launch_render(self, camera, image, n_chunks, n_res, record_events=True):
-        self._ensure_render_ws(camera.width, camera.height)
-        a = _lib.RenderArgs()
-        a.cam = camera.struct(self.dot_mode)
-        a.pool = self.pool.data_ptr()
-        a.chunks = self.chunks_dev.data_ptr()
-        a.n_chunks = n_chunks
-        a.n_splats = n_res
-        a.n_cap = self.n_cap
-        a.m_cap = self.m_cap
-        a.image = image.data_ptr()
-        a.accumulate = 0
-        a.exact = int(self.exact)
-        a.counters_out = self.counters.data_ptr()
-        a.workspace = self.render_ws.data_ptr()
-        if record_events:
-            for i, k in enumerate(("pre", "sorted", "blend0", "blend1")):
-                a.events[i] = self.ev[k].cuda_event
-        _lib.check(_lib.load().vms_render(ctypes.byref(a), _device.sptr()), "render")
-
-    def _check_overflow(self, camera, image, n_chunks, n_res):
-        """After a sync: if the tile-instance buffer overflowed, grow it and
-        re-render (the pool and chunk table are unchanged)."""
-        t = _device.torch()
-        while int(self.counters[2]):
-            need = int(self.counters[3])
-            self.m_cap = need + need // 4 + (1 << 16)
-            self._launch_render(camera, image, n_chunks, n_res, record_events=False)
-            t.cuda.current_stream().synchronize()
+    def _grow(self, need):
+        self.m_cap = int(need + need // 4 + (1 << 16))
+        w, h = self._ws_res[0], self._ws_res[1]
+        self._ws_res = None
+        self._ensure_ws(w, h)
 
     def render_frame(self, camera, frame_index: int, out=None):
         """Run one frame.  Returns (image, stats) with the reference's stats
-        keys (runtime.py:471-488).  ``out``: None -> new numpy array;
-        a pinned/regular numpy (h, w, 3) f32 array -> filled in place;
-        "device" -> a CUDA tensor (no host copy)."""
+        keys (runtime.py:471-488) plus device counters.  ``out``: None -> a new
+        numpy array; a float32 (h, w, 3) numpy array (ideally pinned) ->
+        filled in place; "device" -> a CUDA tensor (no host copy; final once
+        the next render_frame/flush call returns)."""
         t = _device.torch()
-        ev = self.ev
-        stream = t.cuda.current_stream()
-        sc = self.scene
+        lib = self._lib
         h0 = time.perf_counter()
-        ev["start"].record(stream)
-        self._visibility(camera)
-        ev["vis"].record(stream)
-        ev["req"].record(stream)
-        ev["req"].synchronize()
-        pid, enc, direct, level = self.vis.required()
-        h1 = time.perf_counter()
-        pp, pl, pe, ps, missing = self.table.update(pid, enc, direct, level, frame_index,
-                                                    self.staging_pages)
-        h2 = time.perf_counter()
-        # uploads on the side stream
-        bytes_copied = 0
-        n_plan = len(pp)
-        if n_plan:
-            per = (self.page_size >> pl.astype(np.int64)).astype(np.int64)
-            starts = np.zeros(len(sc.page_counts) + 1, np.int64)
-            for k in range(sc.lod_levels):
-                starts[k + 1] = starts[k] + sc.page_counts[k] * (self.page_size >> k)
-            src_rows = starts[pl.astype(np.int64)] + (pp.astype(np.int64) - 1) * per
-            dst_rows = pe.astype(np.int64) * self.page_size + ps.astype(np.int64) * per
-            cp = self.copies_host.numpy()
-            cp[:n_plan, 0] = src_rows * RECORD_BYTES
-            cp[:n_plan, 1] = dst_rows * RECORD_BYTES
-            cp[:n_plan, 2] = per * RECORD_BYTES
-            bytes_copied = int((per * RECORD_BYTES).sum())
-            self.copy_stream.wait_stream(stream)
-            with t.cuda.stream(self.copy_stream):
-                ev["copy0"].record(self.copy_stream)
-                _lib.check(_lib.load().vms_upload_pages(
-                    self.copies_host.data_ptr(), n_plan, self.host.data_ptr(),
-                    self.pool.data_ptr(), self.upload_mode, self.copy_stream.cuda_stream),
-                    "upload_pages")
-                ev["copy1"].record(self.copy_stream)
-            stream.wait_stream(self.copy_stream)
-        h3 = time.perf_counter()
-        usage = self.table.usage_ratio()
+        self._ensure_ws(camera.width, camera.height)
+        a = self._args
+        a.cam = camera.struct(self.dot_mode)
+        a.vis_cam = camera.scaled(self.vis_scale).struct(self.dot_mode)
+        thr = self.controller.thresholds
+        if thr.size > 8:
+            raise InvariantViolation("at most 9 LOD levels are supported")
+        for i, v in enumerate(thr):
+            a.lod.thresholds[i] = float(v)
+        a.lod.count = int(thr.size)
+        a.frame = int(frame_index)
+        a.budget = float(self.staging_pages)
+        a.timing = int(self.timing)
+        device_out = isinstance(out, str) and out == "device"
+        image = self._frame_image(camera)
+        a.image = image.data_ptr()
+        host = None
+        if not device_out:
+            if out is None:
+                key = (camera.height, camera.width)
+                if self._pinned_out is None or self._pinned_out[0] != key:
+                    self._pinned_out = (key, t.empty((camera.height, camera.width, 3),
+                                                     dtype=t.float32).pin_memory())
+                host = self._pinned_out[1]
+                a.host_image = host.data_ptr()
+            else:
+                if out.dtype != np.float32 or out.shape != (camera.height, camera.width, 3) \
+                        or not out.flags.c_contiguous:
+                    raise ValueError("out must be a C-contiguous float32 (h, w, 3) array")
+                a.host_image = out.ctypes.data
+        else:
+            a.host_image = None
+        stream = _device.sptr()
+        st = self._stats
+        while True:
+            rc = lib.vms_session_frame(self._h, ctypes.byref(a), ctypes.byref(st), stream)
+            if rc != _lib.VMS_ERR_NOMEM:
+                _lib.check(rc, "render_frame")
+                break
+            # tile-instance buffer overflow (this frame when synchronised,
+            # else the previous one): grow, re-render, retry
+            self._grow(int(st.n_need))
+            prev = st.overflow == 2  # the previous frame overflowed (detected late)
+            rc2 = lib.vms_session_rerender(self._h, None if prev else a.host_image, stream)
+            while rc2 == _lib.VMS_ERR_NOMEM:
+                cnt = (ctypes.c_uint32 * 4)()
+                lib.vms_session_counters(self._h, cnt, stream)
+                self._grow(int(cnt[3]))
+                rc2 = lib.vms_session_rerender(self._h, None if prev else a.host_image, stream)
+            _lib.check(rc2, "rerender")
+            if not prev:
+                lib.vms_session_counters(self._h, _CNT, stream)
+                st.n_kept, st.n_inst, st.overflow = _CNT[0], _CNT[1], 0
+                break
+        usage = st.occupied_entries / self.capacity
         if self.lod_enabled:
             adapt_thresholds(self.controller, usage, frame_index)
-        # chunk table of every resident page, ascending page id
-        n_rec = ctypes.c_int64(0)
-        cap = self.chunks_host.shape[0]
-        n_chunks = int(_lib.load().vms_pt_chunks(self.table.handle, self.page_size,
-                                                 self.chunks_host.data_ptr(), cap,
-                                                 ctypes.byref(n_rec)))
-        if n_chunks > cap:
-            raise InvariantViolation("chunk table overflow")
-        n_res = int(n_rec.value)
-        if n_chunks:
-            self.chunks_dev[:n_chunks].copy_(self.chunks_host[:n_chunks], non_blocking=True)
-        h4 = time.perf_counter()
-        if out is None or isinstance(out, np.ndarray):
-            image = self._frame_image(camera)
-        elif isinstance(out, str) and out == "device":
-            image = self._frame_image(camera)
-        else:
-            image = out
-        ev["render0"].record(stream)
-        self._launch_render(camera, image, n_chunks, n_res)
-        ev["end"].record(stream)
-        if out is None or isinstance(out, np.ndarray):
-            ev["end"].synchronize()
-            self._check_overflow(camera, image, n_chunks, n_res)
-            if out is None:
-                host_img = image.cpu().numpy()
-            else:
-                hv = t.from_numpy(out)
-                hv.copy_(image, non_blocking=True)
-                stream.synchronize()
-                host_img = out
-        else:
-            ev["end"].synchronize()
-            self._check_overflow(camera, image, n_chunks, n_res)
-            host_img = image
-        h5 = time.perf_counter()
-        d = lambda a, b: ev[a].elapsed_time(ev[b]) / 1e3  # noqa: E731
-        t_copy = d("copy0", "copy1") if n_plan else 0.0
+        h1 = time.perf_counter()
+        levels = self.scene.lod_levels
         stats = {
             "frame": frame_index,
-            "required_pages": int(len(pid)),
-            "resident_pages": int(self.table.resident_count()),
-            "resident_per_level": self.table.resident_counts(sc.lod_levels),
-            "planned_copies": int(n_plan),
-            "missing_pages": int(missing),
-            "bytes_copied": int(bytes_copied),
+            "required_pages": int(st.required),
+            "resident_pages": int(st.resident),
+            "resident_per_level": tuple(int(st.resident_per_level[k]) for k in range(levels)),
+            "planned_copies": int(st.planned),
+            "missing_pages": int(st.missing),
+            "bytes_copied": int(st.bytes_copied),
             "usage": usage,
             "lod_step": self.controller.step,
             "thresholds": tuple(float(x) for x in self.controller.thresholds),
-            "time_visibility": d("start", "vis"),
+            "time_visibility": st.ms_vis / 1e3,
             "time_reduce": 0.0,
-            "time_update": h2 - h1,
-            "time_copy": t_copy + (h4 - h3),
-            "time_sort": d("render0", "sorted"),
-            "time_render": d("sorted", "end"),
-            "time_frame_wall": h5 - h0,
-            "time_preprocess": d("render0", "pre"),
-            "time_tiles": d("sorted", "blend0"),
-            "time_blend": d("blend0", "blend1"),
-            "time_device_frame": d("start", "end"),
-            "n_kept": int(self.counters[0]),
-            "n_instances": int(self.counters[1]),
-            "n_resident_records": n_res,
-            "n_chunks": n_chunks,
+            "time_update": st.host_update_s,
+            "time_copy": st.ms_copy / 1e3,
+            "time_sort": (st.ms_preprocess + st.ms_sort) / 1e3,
+            "time_render": (st.ms_tiles + st.ms_blend) / 1e3,
+            "time_preprocess": st.ms_preprocess / 1e3,
+            "time_tiles": st.ms_tiles / 1e3,
+            "time_blend": st.ms_blend / 1e3,
+            "time_device_frame": st.ms_frame / 1e3,
+            "time_frame_wall": h1 - h0,
+            "n_kept": int(st.n_kept),
+            "n_instances": int(st.n_inst),
+            "n_resident_records": int(st.n_res),
+            "n_chunks": int(st.n_chunks),
+            "n_tris": int(st.n_tris),
         }
-        return host_img, stats
+        if device_out:
+            return image, stats
+        if out is None:
+            return host.numpy().copy(), stats
+        return out, stats
+
+    def flush(self):
+        """Wait for the last frame and surface a late tile-instance overflow
+        (device-output mode) by growing and re-rendering it."""
+        cnt = (ctypes.c_uint32 * 4)()
+        rc = self._lib.vms_session_counters(self._h, cnt, _device.sptr())
+        while rc == _lib.VMS_ERR_NOMEM:
+            self._grow(int(cnt[3]))
+            rc = self._lib.vms_session_rerender(self._h, None, _device.sptr())
+            if rc == _lib.VMS_ERR_NOMEM:
+                self._lib.vms_session_counters(self._h, cnt, _device.sptr())
+        _lib.check(rc, "flush")
+        return tuple(int(x) for x in cnt)
 
     def _frame_image(self, camera):
         t = _device.torch()
@@ -588,6 +607,9 @@ class VmSession:
         key, bufs, i = imgs
         self._images = (key, bufs, i ^ 1)
         return bufs[i]
+
+
+_CNT = (ctypes.c_uint32 * 4)()
 
 
 def _pinned_records(scene):

@@ -35,13 +35,15 @@ def main():
     lay, path = bench.ensure_scene(A, 0)
     scene = read_scene(path, mmap_gaussians=True)
     traj = scenegen.street_path(lay, frames=120)
-    s = VmSession(scene, exact=not a.fast)
+    s = VmSession(scene, exact=not a.fast, timing=False)
     for f in range(a.warm):
         s.render_frame(traj.frame_camera(f), f, out="device")
+    s.flush()
     torch.cuda.synchronize()
     torch.cuda.cudart().cudaProfilerStart()
     for f in range(a.warm, a.warm + a.frames):
         _, st = s.render_frame(traj.frame_camera(f), f, out="device")
+    s.flush()
     torch.cuda.synchronize()
     torch.cuda.cudart().cudaProfilerStop()
     print({k: st[k] for k in ("n_kept", "n_instances", "n_resident_records", "required_pages",
