@@ -17,6 +17,7 @@
 // SURVEY A16); exact mode reproduces the reference's FP64 arithmetic with
 // f32 storage of T and colour.
 #include <cstdlib>
+#include <type_traits>
 
 #include "common.cuh"
 #include "prims.h"
@@ -149,10 +150,18 @@ __global__ void ranges_k(const uint32_t* __restrict__ tk, const RenderCounters* 
   }
 }
 
-// One CTA per TS x TS tile, 256 threads; thread (lx, ly) owns the pixels of
-// column lx at rows ly, ly + 256/TS, ... (PPT = TS*TS/256 pixels).  Splats
-// of the tile's list are staged 256 at a time in shared memory; the per-splat
-// column work (dx, a*dx*dx, FP64 conversions) is shared by a thread's pixels.
+// Blend: one CTA per 16x16 sub-tile of a TS x TS sort tile (TS/16)^2 CTAs
+// share one tile list), one thread per pixel.  Splats of the list are staged
+// 256 at a time; each staging thread tests its splat against the CTA's
+// sub-tile and a warp-ballot compaction keeps only the overlapping ones (in
+// list order) in shared memory - the pixel loop touches relevant splats only.
+// Exact mode stages the splat parameters already widened to FP64, so the
+// inner loop has no f32->f64 conversions of splat data.
+struct SplatF64 {
+  double cx, cy, ca, cb2, cc, al, r, g, b;
+  int x0, x1, y0, y1;
+};
+
 template <bool kExact, int TS>
 __global__ void __launch_bounds__(kBlendThreads) blend_k(const uint32_t* __restrict__ ranges,
                                                          const uint32_t* __restrict__ tv,
@@ -160,109 +169,117 @@ __global__ void __launch_bounds__(kBlendThreads) blend_k(const uint32_t* __restr
                                                          int w, int h, int tiles_x,
                                                          float* __restrict__ image,
                                                          int accumulate) {
-  constexpr int PPT = TS * TS / kBlendThreads;
-  constexpr int ROWS = kBlendThreads / TS;
-  __shared__ BlendRec srec[kBlendThreads];
-  const int tile = blockIdx.x;
-  const int px = (tile % tiles_x) * TS + (threadIdx.x % TS);
-  const int py0 = (tile / tiles_x) * TS + (threadIdx.x / TS);
+  constexpr int SUB = TS / 16;  // sub-tiles per tile edge
+  using Staged = typename std::conditional<kExact, SplatF64, BlendRec>::type;
+  __shared__ Staged sp[kBlendThreads];
+  __shared__ uint32_t wsum[kBlendThreads / 32];
+  const int tile = blockIdx.x / (SUB * SUB), sub = blockIdx.x % (SUB * SUB);
+  const int sx0 = (tile % tiles_x) * TS + (sub % SUB) * 16;
+  const int sy0 = (tile / tiles_x) * TS + (sub / SUB) * 16;
+  const int px = sx0 + (threadIdx.x & 15), py = sy0 + (threadIdx.x >> 4);
+  const bool inside = px < w && py < h;
   const uint32_t start = ranges[2 * tile], end = ranges[2 * tile + 1];
-  float cr[PPT], cg[PPT], cb[PPT], T[PPT];
-  bool done[PPT];
-  bool all_done = true;
-#pragma unroll
-  for (int k = 0; k < PPT; ++k) {
-    const int py = py0 + k * ROWS;
-    const bool inside = px < w && py < h;
-    cr[k] = cg[k] = cb[k] = 0.f;
-    T[k] = 1.f;
-    if (accumulate && inside) {
-      const float* p = image + ((size_t)py * w + px) * 3;
-      cr[k] = p[0];
-      cg[k] = p[1];
-      cb[k] = p[2];
-    }
-    done[k] = !inside;
-    all_done = all_done && done[k];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  float cr = 0.f, cg = 0.f, cb = 0.f, T = 1.f;
+  if (accumulate && inside) {
+    const float* p = image + ((size_t)py * w + px) * 3;
+    cr = p[0];
+    cg = p[1];
+    cb = p[2];
   }
+  bool done = !inside;
   for (uint32_t base = start; base < end; base += kBlendThreads) {
-    if (__syncthreads_and(all_done)) break;
+    if (__syncthreads_and(done)) break;
     const uint32_t i = base + threadIdx.x;
-    if (i < end) srec[threadIdx.x] = rec[tv[i]];
+    bool hit = false;
+    BlendRec r;
+    if (i < end) {
+      r = rec[tv[i]];
+      const int x0 = r.bx & 0xFFFF, x1 = r.bx >> 16, y0 = r.by & 0xFFFF, y1 = r.by >> 16;
+      hit = x0 < sx0 + 16 && x1 > sx0 && y0 < sy0 + 16 && y1 > sy0;
+    }
+    const uint32_t bal = __ballot_sync(0xffffffffu, hit);
+    if (lane == 0) wsum[warp] = __popc(bal);
     __syncthreads();
-    const int cnt = min((uint32_t)kBlendThreads, end - base);
-    if (!all_done) {
-      for (int j = 0; j < cnt; ++j) {
-        const BlendRec& s = srec[j];
-        const int x0 = s.bx & 0xFFFF, x1 = s.bx >> 16;
-        if (px < x0 || px >= x1) continue;
-        const int y0 = s.by & 0xFFFF, y1 = s.by >> 16;
+    uint32_t pre = 0, cnt = 0;
+#pragma unroll
+    for (int k = 0; k < kBlendThreads / 32; ++k) {
+      const uint32_t c = wsum[k];
+      pre += k < warp ? c : 0u;
+      cnt += c;
+    }
+    if (hit) {
+      const uint32_t o = pre + __popc(bal & lanemask_lt());
+      if constexpr (kExact) {
+        SplatF64 d;
+        d.cx = r.cx;
+        d.cy = r.cy;
+        d.ca = r.ca;
+        d.cb2 = 2.0 * (double)r.cb;  // exact: power-of-two scaling
+        d.cc = r.cc;
+        d.al = r.alpha;
+        d.r = r.r;
+        d.g = r.g;
+        d.b = r.b;
+        d.x0 = r.bx & 0xFFFF;
+        d.x1 = r.bx >> 16;
+        d.y0 = r.by & 0xFFFF;
+        d.y1 = r.by >> 16;
+        sp[o] = d;
+      } else {
+        sp[o] = r;
+      }
+    }
+    __syncthreads();
+    if (!done) {
+      for (uint32_t j = 0; j < cnt; ++j) {
+        const Staged& s = sp[j];
         if constexpr (kExact) {
-          // _core.pyx:49-78 in FP64 with f32 storage of T and colour
-          const double dx = ((double)px + 0.5) - (double)s.cx;
-          const double ddx = __dmul_rn(__dmul_rn((double)s.ca, dx), dx);
-          const double b2 = __dmul_rn(2.0, (double)s.cb);
-          const double cy = (double)s.cy, cc = (double)s.cc, al = (double)s.alpha;
-#pragma unroll
-          for (int k = 0; k < PPT; ++k) {
-            const int py = py0 + k * ROWS;
-            if (done[k] || py < y0 || py >= y1) continue;
-            const double t = (double)T[k];
-            if (t < 1.0 / 255.0) {
-              done[k] = true;
-              continue;
-            }
-            const double dy = ((double)py + 0.5) - cy;
-            const double sig = -0.5 * __dadd_rn(__dadd_rn(ddx, __dmul_rn(__dmul_rn(b2, dy), dx)),
-                                                __dmul_rn(__dmul_rn(cc, dy), dy));
-            double wgt = __dmul_rn(al, exp(sig));
-            if (wgt > 0.99) wgt = 0.99;
-            const double wt = __dmul_rn(wgt, t);
-            cr[k] = __double2float_rn(__dadd_rn((double)cr[k], __dmul_rn(wt, (double)s.r)));
-            cg[k] = __double2float_rn(__dadd_rn((double)cg[k], __dmul_rn(wt, (double)s.g)));
-            cb[k] = __double2float_rn(__dadd_rn((double)cb[k], __dmul_rn(wt, (double)s.b)));
-            T[k] = __double2float_rn(__dmul_rn(t, __dsub_rn(1.0, wgt)));
+          if (px < s.x0 || px >= s.x1 || py < s.y0 || py >= s.y1) continue;
+          // _core.pyx:49-78: FP64 arithmetic, f32 storage of T and colour
+          const double t = (double)T;
+          if (t < 1.0 / 255.0) {
+            done = true;
+            break;
           }
+          const double dx = ((double)px + 0.5) - s.cx;
+          const double dy = ((double)py + 0.5) - s.cy;
+          const double sig = -0.5 * __dadd_rn(__dadd_rn(__dmul_rn(__dmul_rn(s.ca, dx), dx),
+                                                        __dmul_rn(__dmul_rn(s.cb2, dy), dx)),
+                                              __dmul_rn(__dmul_rn(s.cc, dy), dy));
+          double wgt = __dmul_rn(s.al, exp(sig));
+          if (wgt > 0.99) wgt = 0.99;
+          const double wt = __dmul_rn(wgt, t);
+          cr = __double2float_rn(__dadd_rn((double)cr, __dmul_rn(wt, s.r)));
+          cg = __double2float_rn(__dadd_rn((double)cg, __dmul_rn(wt, s.g)));
+          cb = __double2float_rn(__dadd_rn((double)cb, __dmul_rn(wt, s.b)));
+          T = __double2float_rn(__dmul_rn(t, __dsub_rn(1.0, wgt)));
         } else {
-          const float dx = ((float)px + 0.5f) - s.cx;
-          const float adx = s.ca * dx * dx, bdx = 2.0f * s.cb * dx;
-#pragma unroll
-          for (int k = 0; k < PPT; ++k) {
-            const int py = py0 + k * ROWS;
-            if (done[k] || py < y0 || py >= y1) continue;
-            if (T[k] < (1.0f / 255.0f)) {
-              done[k] = true;
-              continue;
-            }
-            const float dy = ((float)py + 0.5f) - s.cy;
-            const float sig = -0.5f * (adx + bdx * dy + s.cc * dy * dy);
-            const float wgt = fminf(s.alpha * __expf(sig), 0.99f);
-            const float wt = wgt * T[k];
-            cr[k] += wt * s.r;
-            cg[k] += wt * s.g;
-            cb[k] += wt * s.b;
-            T[k] = T[k] * (1.0f - wgt);
+          const int x0 = s.bx & 0xFFFF, x1 = s.bx >> 16, y0 = s.by & 0xFFFF, y1 = s.by >> 16;
+          if (px < x0 || px >= x1 || py < y0 || py >= y1) continue;
+          if (T < (1.0f / 255.0f)) {
+            done = true;
+            break;
           }
+          const float dx = ((float)px + 0.5f) - s.cx, dy = ((float)py + 0.5f) - s.cy;
+          const float sig = -0.5f * (s.ca * dx * dx + 2.0f * s.cb * dy * dx + s.cc * dy * dy);
+          const float wgt = fminf(s.alpha * __expf(sig), 0.99f);
+          const float wt = wgt * T;
+          cr += wt * s.r;
+          cg += wt * s.g;
+          cb += wt * s.b;
+          T = T * (1.0f - wgt);
         }
       }
-      all_done = true;
-#pragma unroll
-      for (int k = 0; k < PPT; ++k) {
-        if (!done[k] && T[k] < (1.0f / 255.0f)) done[k] = true;
-        all_done = all_done && done[k];
-      }
+      if (!done && T < (1.0f / 255.0f)) done = true;
     }
     __syncthreads();
   }
-#pragma unroll
-  for (int k = 0; k < PPT; ++k) {
-    const int py = py0 + k * ROWS;
-    if (px < w && py < h) {
-      float* p = image + ((size_t)py * w + px) * 3;
-      p[0] = cr[k];
-      p[1] = cg[k];
-      p[2] = cb[k];
-    }
+  if (inside) {
+    float* p = image + ((size_t)py * w + px) * 3;
+    p[0] = cr;
+    p[1] = cg;
+    p[2] = cb;
   }
 }
 
@@ -331,8 +348,9 @@ int32_t tiles_and_blend(const RenderCamera& cam, const uint32_t* vals, const Ren
   if (events && events[2]) VMS_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(events[2]), s));
   auto* kern = exact ? (ts == 16 ? blend_k<true, 16> : blend_k<true, 32>)
                      : (ts == 16 ? blend_k<false, 16> : blend_k<false, 32>);
-  kern<<<n_tiles, kBlendThreads, 0, s>>>(w.ranges, tv, w.rec, cam.width, cam.height, tiles_x,
-                                         image, accumulate);
+  const uint32_t subs = (uint32_t)(ts / 16) * (ts / 16);
+  kern<<<n_tiles * subs, kBlendThreads, 0, s>>>(w.ranges, tv, w.rec, cam.width, cam.height,
+                                                tiles_x, image, accumulate);
   mark("blend", s);
   if (events && events[3]) VMS_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(events[3]), s));
   VMS_LAUNCH_CHECK("tiles_and_blend");

@@ -359,7 +359,8 @@ class VmSession:
     def __init__(self, scene, buffer_pages: int = 500, staging_pages: float = 40,
                  vis_scale: float = 0.25, band=(0.5, 0.8), step: float = 0.05,
                  lod_enabled: bool = True, links_enabled: bool = True, exact: bool = True,
-                 upload_mode: int = 1, timing: bool = True, device=None):
+                 upload_mode: int = 1, timing: bool = True, device=None,
+                 instance_capacity: int | None = None):
         from paper_2506_19415_b200.render import VisibilityBuffers
 
         t = _device.require_cuda()
@@ -403,9 +404,6 @@ class VmSession:
             self.n_cap = self.capacity * self.page_size
             self.pool = t.empty((self.n_cap, RECORD_SIZE), dtype=t.float32, device=self.device)
             self.host = _pinned_records(scene)  # the streaming source (pinned, mapped)
-            self.m_cap = max(16 * self.n_cap, 1 << 20)
-            self._ws_res = None
-            self.render_ws = None
             d = _lib.SessionDesc()
             d.host_records = self.host.data_ptr()
             d.host_rows = int(len(scene.gaussians))
@@ -425,9 +423,10 @@ class VmSession:
             d.vis_ws = self.vis.ws.data_ptr()
             d.exact = int(self.exact)
             d.upload_mode = self.upload_mode
+            # tile-instance capacity; the session regrows it on overflow
+            d.m_cap = int(instance_capacity) if instance_capacity else max(16 * self.n_cap, 1 << 20)
             self._desc = d
             self._h = None
-            self._ensure_ws(256, 256)  # resized on the first frame
             h = self._lib.vms_session_create(ctypes.byref(d))
             if not h:
                 raise InvariantViolation(self._lib.vms_last_error().decode())
@@ -457,31 +456,6 @@ class VmSession:
     def buffer(self):
         return self.pool
 
-    def _ensure_ws(self, width, height):
-        t = _device.torch()
-        key = (width, height, self.m_cap)
-        if self._ws_res == key:
-            return
-        nbytes = self._lib.vms_session_render_ws_bytes(self.capacity, self.page_size, self.m_cap,
-                                                       width, height)
-        self.render_ws = None
-        self.render_ws = t.empty(nbytes, dtype=t.uint8, device=self.device)
-        self._ws_res = key
-        self._desc.render_ws = self.render_ws.data_ptr()
-        self._desc.render_ws_bytes = nbytes
-        self._desc.m_cap = self.m_cap
-        self._desc.width, self._desc.height = width, height
-        if self._h is not None:
-            _lib.check(self._lib.vms_session_set_render_ws(self._h, self.render_ws.data_ptr(),
-                                                           nbytes, self.m_cap, width, height),
-                       "set_render_ws")
-
-    def _grow(self, need):
-        self.m_cap = int(need + need // 4 + (1 << 16))
-        w, h = self._ws_res[0], self._ws_res[1]
-        self._ws_res = None
-        self._ensure_ws(w, h)
-
     def render_frame(self, camera, frame_index: int, out=None):
         """Run one frame.  Returns (image, stats) with the reference's stats
         keys (runtime.py:471-488) plus device counters.  ``out``: None -> a new
@@ -491,7 +465,6 @@ class VmSession:
         t = _device.torch()
         lib = self._lib
         h0 = time.perf_counter()
-        self._ensure_ws(camera.width, camera.height)
         a = self._args
         a.cam = camera.struct(self.dot_mode)
         a.vis_cam = camera.scaled(self.vis_scale).struct(self.dot_mode)
@@ -525,26 +498,10 @@ class VmSession:
             a.host_image = None
         stream = _device.sptr()
         st = self._stats
-        while True:
-            rc = lib.vms_session_frame(self._h, ctypes.byref(a), ctypes.byref(st), stream)
-            if rc != _lib.VMS_ERR_NOMEM:
-                _lib.check(rc, "render_frame")
-                break
-            # tile-instance buffer overflow (this frame when synchronised,
-            # else the previous one): grow, re-render, retry
-            self._grow(int(st.n_need))
-            prev = st.overflow == 2  # the previous frame overflowed (detected late)
-            rc2 = lib.vms_session_rerender(self._h, None if prev else a.host_image, stream)
-            while rc2 == _lib.VMS_ERR_NOMEM:
-                cnt = (ctypes.c_uint32 * 4)()
-                lib.vms_session_counters(self._h, cnt, stream)
-                self._grow(int(cnt[3]))
-                rc2 = lib.vms_session_rerender(self._h, None if prev else a.host_image, stream)
-            _lib.check(rc2, "rerender")
-            if not prev:
-                lib.vms_session_counters(self._h, _CNT, stream)
-                st.n_kept, st.n_inst, st.overflow = _CNT[0], _CNT[1], 0
-                break
+        # one call: visibility, page table, uploads, render (tile-instance
+        # overflows are regrown and re-rendered inside the session)
+        _lib.check(lib.vms_session_frame(self._h, ctypes.byref(a), ctypes.byref(st), stream),
+                   "render_frame")
         usage = st.occupied_entries / self.capacity
         if self.lod_enabled:
             adapt_thresholds(self.controller, usage, frame_index)
@@ -585,16 +542,10 @@ class VmSession:
         return out, stats
 
     def flush(self):
-        """Wait for the last frame and surface a late tile-instance overflow
-        (device-output mode) by growing and re-rendering it."""
+        """Wait for the last frame (device-output mode); returns its device
+        counters (kept splats, tile instances, overflow, needed)."""
         cnt = (ctypes.c_uint32 * 4)()
-        rc = self._lib.vms_session_counters(self._h, cnt, _device.sptr())
-        while rc == _lib.VMS_ERR_NOMEM:
-            self._grow(int(cnt[3]))
-            rc = self._lib.vms_session_rerender(self._h, None, _device.sptr())
-            if rc == _lib.VMS_ERR_NOMEM:
-                self._lib.vms_session_counters(self._h, cnt, _device.sptr())
-        _lib.check(rc, "flush")
+        _lib.check(self._lib.vms_session_counters(self._h, cnt, _device.sptr()), "flush")
         return tuple(int(x) for x in cnt)
 
     def _frame_image(self, camera):
@@ -608,8 +559,6 @@ class VmSession:
         self._images = (key, bufs, i ^ 1)
         return bufs[i]
 
-
-_CNT = (ctypes.c_uint32 * 4)()
 
 
 def _pinned_records(scene):

@@ -402,3 +402,25 @@ def test_c2_render_is_deterministic(cuda, c2_scene):
             h.update(img.tobytes())
         digests.append(h.hexdigest())
     assert digests[0] == digests[1]
+
+
+def test_tile_instance_overflow_recovers(cuda):
+    """A session whose tile-instance buffer is far too small regrows it and
+    re-renders: images identical to a roomy session, in every output mode."""
+    from paper_2506_19415_b200.runtime import VmSession
+
+    sc = _city()
+    path = inputs.city_path(inputs.CITY_SMALL)
+    big = VmSession(sc, buffer_pages=16, staging_pages=6.0, vis_scale=0.5)
+    small = VmSession(sc, buffer_pages=16, staging_pages=6.0, vis_scale=0.5,
+                      instance_capacity=64, timing=False)
+    for f in range(path.frame_count):
+        cam = path.frame_camera(f)
+        ref, _ = big.render_frame(cam, f)
+        if f % 2:
+            img, _ = small.render_frame(cam, f)
+        else:
+            dev, _ = small.render_frame(cam, f, out="device")
+            small.flush()
+            img = dev.cpu().numpy()
+        assert np.array_equal(img, ref), f
