@@ -300,6 +300,10 @@ def run_ours(args, rank, world, local_rank):
         "mean_instances": int(statistics.mean(s["n_instances"] for s in stats_t)),
         "mean_resident_records": int(statistics.mean(s["n_resident_records"] for s in stats_t)),
         "gpu_launches": int(launches),
+        "host_wall_ms": {
+            name: {"median": round(1e3 * statistics.median(x["time_frame_wall"] for x in st), 4),
+                   "max": round(1e3 * max(x["time_frame_wall"] for x in st), 4)}
+            for name, st in (("device", stats), ("e2e", stats_e2e))},
         "clocks": clocks,
     }
     if world == 1 and not args.no_cpu_baseline:

@@ -209,7 +209,7 @@ int32_t vms_rasterize_triangles(const double* tris, const uint32_t* ids, int64_t
 
 size_t vms_radix_workspace_bytes(int64_t n) {
   const size_t m = (size_t)(n > 0 ? n : 1);
-  return sizeof(uint32_t) * m * 4 + sizeof(int64_t) * m + radix_ws_bytes() + 256 * 8;
+  return sizeof(uint32_t) * m * 4 + sizeof(int64_t) * m + radix_ws_bytes((uint32_t)m) + 256 * 8;
 }
 
 int32_t vms_radix_sort_pairs(uint32_t* keys, int64_t* values, int64_t n, void* workspace,
@@ -231,11 +231,11 @@ int32_t vms_radix_sort_pairs(uint32_t* keys, int64_t* values, int64_t n, void* w
   uint32_t* k1 = carve<uint32_t>(p, m);
   uint32_t* v1 = carve<uint32_t>(p, m);
   int64_t* tmp = carve<int64_t>(p, m);
-  void* rws = carve<char>(p, radix_ws_bytes());
+  void* rws = carve<char>(p, radix_ws_bytes(m));
   VMS_CUDA(cudaMemcpyAsync(k0, keys, sizeof(uint32_t) * m, cudaMemcpyDeviceToDevice, s));
   iota_k<<<ceil_div<uint32_t>(m, 256), 256, 0, s>>>(v0, m);
   int alt = 0;
-  int32_t st = radix_sort_u32(k0, v0, k1, v1, nullptr, m, 0, 32, &alt, rws, s);
+  int32_t st = radix_sort_u32(k0, v0, k1, v1, nullptr, m, m, 0, 32, &alt, rws, s);
   if (st) return st;
   uint32_t* ks = alt ? k1 : k0;
   uint32_t* vs = alt ? v1 : v0;

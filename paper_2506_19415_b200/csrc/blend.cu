@@ -159,11 +159,42 @@ __global__ void ranges_k(const uint32_t* __restrict__ tk, const RenderCounters* 
 // inner loop has no f32->f64 conversions of splat data.
 struct SplatF64 {
   double cx, cy, ca, cb2, cc, al, r, g, b;
+  double skip;  // sigma below which alpha * exp(sigma) < 2^-36 (no effect on f32 T)
   int x0, x1, y0, y1;
 };
 
+// Longest-list-first tile schedule: tiles bucketed by floor(log2(list length))
+// in descending order (one CTA; the order only affects scheduling, never
+// results - tiles are independent).
+__global__ void __launch_bounds__(1024) tile_order_k(const uint32_t* __restrict__ ranges,
+                                                     uint32_t n_tiles,
+                                                     uint32_t* __restrict__ order) {
+  __shared__ uint32_t hist[33];
+  __shared__ uint32_t base[33];
+  if (threadIdx.x < 33) hist[threadIdx.x] = 0;
+  __syncthreads();
+  for (uint32_t t = threadIdx.x; t < n_tiles; t += blockDim.x) {
+    const uint32_t len = ranges[2 * t + 1] - ranges[2 * t];
+    atomicAdd(&hist[len ? 32 - __clz(len) : 0], 1u);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t run = 0;
+    for (int b = 32; b >= 0; --b) {
+      base[b] = run;
+      run += hist[b];
+    }
+  }
+  __syncthreads();
+  for (uint32_t t = threadIdx.x; t < n_tiles; t += blockDim.x) {
+    const uint32_t len = ranges[2 * t + 1] - ranges[2 * t];
+    order[atomicAdd(&base[len ? 32 - __clz(len) : 0], 1u)] = t;
+  }
+}
+
 template <bool kExact, int TS>
 __global__ void __launch_bounds__(kBlendThreads) blend_k(const uint32_t* __restrict__ ranges,
+                                                         const uint32_t* __restrict__ order,
                                                          const uint32_t* __restrict__ tv,
                                                          const BlendRec* __restrict__ rec,
                                                          int w, int h, int tiles_x,
@@ -173,7 +204,7 @@ __global__ void __launch_bounds__(kBlendThreads) blend_k(const uint32_t* __restr
   using Staged = typename std::conditional<kExact, SplatF64, BlendRec>::type;
   __shared__ Staged sp[kBlendThreads];
   __shared__ uint32_t wsum[kBlendThreads / 32];
-  const int tile = blockIdx.x / (SUB * SUB), sub = blockIdx.x % (SUB * SUB);
+  const int tile = order[blockIdx.x / (SUB * SUB)], sub = blockIdx.x % (SUB * SUB);
   const int sx0 = (tile % tiles_x) * TS + (sub % SUB) * 16;
   const int sy0 = (tile / tiles_x) * TS + (sub / SUB) * 16;
   const int px = sx0 + (threadIdx.x & 15), py = sy0 + (threadIdx.x >> 4);
@@ -218,6 +249,7 @@ __global__ void __launch_bounds__(kBlendThreads) blend_k(const uint32_t* __restr
         d.cb2 = 2.0 * (double)r.cb;  // exact: power-of-two scaling
         d.cc = r.cc;
         d.al = r.alpha;
+        d.skip = r.alpha > 0.f ? log(0x1p-36 / d.al) : 1e300;
         d.r = r.r;
         d.g = r.g;
         d.b = r.b;
@@ -247,6 +279,9 @@ __global__ void __launch_bounds__(kBlendThreads) blend_k(const uint32_t* __restr
           const double sig = -0.5 * __dadd_rn(__dadd_rn(__dmul_rn(__dmul_rn(s.ca, dx), dx),
                                                         __dmul_rn(__dmul_rn(s.cb2, dy), dx)),
                                               __dmul_rn(__dmul_rn(s.cc, dy), dy));
+          // weight < 2^-36: T is unchanged bit for bit and the colour moves by
+          // < 2^-36 (far tails of elongated splats) - skip the FP64 exp
+          if (sig < s.skip) continue;
           double wgt = __dmul_rn(s.al, exp(sig));
           if (wgt > 0.99) wgt = 0.99;
           const double wt = __dmul_rn(wgt, t);
@@ -329,7 +364,8 @@ int32_t tiles_and_blend(const RenderCamera& cam, const uint32_t* vals, const Ren
   const int T = 256;
   dup_count_k<<<4 * kSMs, T, 0, s>>>(vals, w.rec, w.ctr, shift, w.cnt);
   mark("dup_count", s);
-  int32_t st = scan_exclusive_u32(w.cnt, w.off, &w.ctr->n_kept, 0, &w.ctr->n_inst, w.scan_ws, s);
+  int32_t st = scan_exclusive_u32(w.cnt, w.off, &w.ctr->n_kept, 0, w.n_cap, &w.ctr->n_inst,
+                                  w.scan_ws, s);
   if (st) return st;
   dup_emit_k<<<4 * kSMs, T, 0, s>>>(vals, w.rec, w.off, w.ctr, w.m_cap, tiles_x, shift, w.tk0,
                                     w.tv0);
@@ -337,7 +373,7 @@ int32_t tiles_and_blend(const RenderCamera& cam, const uint32_t* vals, const Ren
   clamp_inst_k<<<1, 1, 0, s>>>(w.ctr, w.m_cap);
   mark("clamp", s);
   int alt = 0;
-  st = radix_sort_u32(w.tk0, w.tv0, w.tk1, w.tv1, &w.ctr->n_inst, 0, 0, tile_bits(n_tiles), &alt,
+  st = radix_sort_u32(w.tk0, w.tv0, w.tk1, w.tv1, &w.ctr->n_inst, 0, w.m_cap, 0, tile_bits(n_tiles), &alt,
                       w.radix_ws, s);
   if (st) return st;
   const uint32_t* tk = alt ? w.tk1 : w.tk0;
@@ -345,11 +381,13 @@ int32_t tiles_and_blend(const RenderCamera& cam, const uint32_t* vals, const Ren
   VMS_CUDA(cudaMemsetAsync(w.ranges, 0, sizeof(uint32_t) * 2 * n_tiles, s));
   ranges_k<<<8 * kSMs, T, 0, s>>>(tk, w.ctr, w.ranges);
   mark("ranges", s);
+  tile_order_k<<<1, 1024, 0, s>>>(w.ranges, n_tiles, w.order);
+  mark("tile_order", s);
   if (events && events[2]) VMS_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(events[2]), s));
   auto* kern = exact ? (ts == 16 ? blend_k<true, 16> : blend_k<true, 32>)
                      : (ts == 16 ? blend_k<false, 16> : blend_k<false, 32>);
   const uint32_t subs = (uint32_t)(ts / 16) * (ts / 16);
-  kern<<<n_tiles * subs, kBlendThreads, 0, s>>>(w.ranges, tv, w.rec, cam.width, cam.height,
+  kern<<<n_tiles * subs, kBlendThreads, 0, s>>>(w.ranges, w.order, tv, w.rec, cam.width, cam.height,
                                                 tiles_x, image, accumulate);
   mark("blend", s);
   if (events && events[3]) VMS_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(events[3]), s));
@@ -365,9 +403,9 @@ size_t render_ws_bytes(uint32_t n_cap, uint32_t m_cap, uint32_t n_tiles) {
   b += sizeof(BlendRec) * (size_t)n_cap;       // rec
   b += sizeof(uint32_t) * (size_t)n_cap * 6;   // k0 v0 k1 v1 cnt off
   b += sizeof(uint32_t) * (size_t)m_cap * 4;   // tk0 tv0 tk1 tv1
-  b += sizeof(uint32_t) * 2 * (size_t)n_tiles; // ranges
+  b += sizeof(uint32_t) * 3 * (size_t)n_tiles; // ranges + order
   b += sizeof(RenderCounters);
-  b += scan_ws_bytes() + radix_ws_bytes();
+  b += scan_ws_bytes(n_cap) + radix_ws_bytes(n_cap > m_cap ? n_cap : m_cap);
   return b + 256 * 20;
 }
 
@@ -391,9 +429,10 @@ RenderWs render_carve(void* ws, uint32_t n_cap, uint32_t m_cap, uint32_t n_tiles
   w.tk1 = carve<uint32_t>(p, m_cap);
   w.tv1 = carve<uint32_t>(p, m_cap);
   w.ranges = carve<uint32_t>(p, 2 * (size_t)n_tiles);
+  w.order = carve<uint32_t>(p, (size_t)n_tiles);
   w.ctr = carve<RenderCounters>(p, 1);
-  w.scan_ws = carve<char>(p, scan_ws_bytes());
-  w.radix_ws = carve<char>(p, radix_ws_bytes());
+  w.scan_ws = carve<char>(p, scan_ws_bytes(n_cap));
+  w.radix_ws = carve<char>(p, radix_ws_bytes(n_cap > m_cap ? n_cap : m_cap));
   return w;
 }
 
@@ -403,7 +442,7 @@ int32_t render_finish(const RenderCamera& cam, uint32_t n_splats, const RenderWs
   const int T = 256;
   VMS_CUDA(cudaMemsetAsync(w.ctr, 0, sizeof(RenderCounters), s));
   if (n_splats) {
-    int32_t st = scan_exclusive_u32(w.flag, w.pos, nullptr, n_splats, &w.ctr->n_kept,
+    int32_t st = scan_exclusive_u32(w.flag, w.pos, nullptr, n_splats, n_splats, &w.ctr->n_kept,
                                     w.scan_ws, s);
     if (st) return st;
     compact_k<<<ceil_div<uint32_t>(n_splats, T), T, 0, s>>>(w.flag, w.pos, w.key_g, n_splats,
@@ -412,7 +451,7 @@ int32_t render_finish(const RenderCamera& cam, uint32_t n_splats, const RenderWs
   }
   int alt = 0;
   // keys are IEEE bits of positive f32 depths: bit 31 is always clear
-  int32_t st = radix_sort_u32(w.k0, w.v0, w.k1, w.v1, &w.ctr->n_kept, 0, 0, 31, &alt,
+  int32_t st = radix_sort_u32(w.k0, w.v0, w.k1, w.v1, &w.ctr->n_kept, 0, w.n_cap, 0, 31, &alt,
                               w.radix_ws, s);
   if (st) return st;
   if (events && events[1]) VMS_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(events[1]), s));
@@ -431,7 +470,8 @@ int32_t composite_ordered(const float* centers, const float* conics, const float
     // splats with an empty clamped box are dropped; the rest keep their order
     pack_ordered_k<<<ceil_div<uint32_t>(n, T), T, 0, s>>>(centers, conics, colors, alphas, bounds,
                                                           n, w, h, ws.rec, ws.v1, ws.flag);
-    int32_t st = scan_exclusive_u32(ws.flag, ws.pos, nullptr, n, &ws.ctr->n_kept, ws.scan_ws, s);
+    int32_t st = scan_exclusive_u32(ws.flag, ws.pos, nullptr, n, n, &ws.ctr->n_kept, ws.scan_ws,
+                                    s);
     if (st) return st;
     compact_k<<<ceil_div<uint32_t>(n, T), T, 0, s>>>(ws.flag, ws.pos, ws.v1, n, ws.k0, ws.v0);
   }

@@ -1,10 +1,10 @@
 // Count-agnostic scan and stable LSD radix sort for sm_100a.
 //
-// Both primitives run on a fixed grid (kPrimGrid CTAs) and read the element
-// count from device memory, so a frame never stalls on a device->host read
-// of an intermediate size.  Each CTA owns one contiguous range of whole
-// tiles; ranges are processed in order, which is what makes the radix sort
-// stable (reduce-then-scan, Merrill-style).
+// Both primitives read the element count from device memory (a frame never
+// stalls on a device->host read of an intermediate size) and run as
+// single-pass decoupled look-back kernels on a persistent grid: one launch
+// per scan, one histogram launch + one launch per 8-bit radix pass
+// (onesweep).  Tiles are claimed in order, so the sort is stable.
 //
 // Radix ranking: per warp, __match_any_sync groups lanes holding the same
 // digit; lane rank = popc(peers & lanemask_lt) + per-warp running count.
@@ -17,8 +17,6 @@
 namespace vms {
 
 namespace {
-
-constexpr int kScanBlock = 1024;
 
 __device__ __forceinline__ uint32_t load_n(const uint32_t* n_dev, uint32_t n_host) {
   return n_dev ? *n_dev : n_host;
@@ -57,211 +55,296 @@ __device__ __forceinline__ uint32_t block_exclusive(uint32_t v, uint32_t* scratc
   return res;
 }
 
-__device__ __forceinline__ void block_range(uint32_t n, uint32_t tile, uint32_t* lo,
-                                            uint32_t* hi) {
-  uint32_t tiles = (n + tile - 1) / tile;
-  uint32_t per = (tiles + gridDim.x - 1) / gridDim.x;
-  uint32_t a = blockIdx.x * per * tile;
-  uint32_t b = a + per * tile;
-  *lo = a < n ? a : n;
-  *hi = b < n ? b : n;
-}
-
-// ---------------------------------------------------------------- scan
-__global__ void __launch_bounds__(kScanBlock) scan_reduce_k(const uint32_t* in,
-                                                             const uint32_t* n_dev,
-                                                             uint32_t n_host,
-                                                             uint32_t* partial) {
-  __shared__ uint32_t red[33];
-  uint32_t n = load_n(n_dev, n_host), lo, hi;
-  block_range(n, kScanBlock, &lo, &hi);
-  uint32_t s = 0;
-  for (uint32_t i = lo + threadIdx.x; i < hi; i += kScanBlock) s += in[i];
-  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    uint32_t t = red[threadIdx.x];
-    for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-    if (threadIdx.x == 0) partial[blockIdx.x] = t;
-  }
-}
-
-// Exclusive scan of `count` values in place by one CTA (count arbitrary).
-__global__ void __launch_bounds__(kScanBlock) scan_single_k(uint32_t* data, uint32_t count,
-                                                             uint32_t* total) {
-  __shared__ uint32_t scratch[33];
-  uint32_t run = 0;
-  for (uint32_t base = 0; base < count; base += kScanBlock) {
-    uint32_t i = base + threadIdx.x;
-    uint32_t v = i < count ? data[i] : 0u;
-    uint32_t tot;
-    uint32_t ex = block_exclusive<kScanBlock>(v, scratch, &tot);
-    if (i < count) data[i] = run + ex;
-    run += tot;
-  }
-  if (threadIdx.x == 0 && total) *total = run;
-}
-
-__global__ void __launch_bounds__(kScanBlock) scan_down_k(const uint32_t* in, uint32_t* out,
-                                                           const uint32_t* n_dev,
-                                                           uint32_t n_host,
-                                                           const uint32_t* partial) {
-  __shared__ uint32_t scratch[33];
-  uint32_t n = load_n(n_dev, n_host), lo, hi;
-  block_range(n, kScanBlock, &lo, &hi);
-  uint32_t run = partial[blockIdx.x];
-  for (uint32_t base = lo; base < hi; base += kScanBlock) {
-    uint32_t i = base + threadIdx.x;
-    uint32_t v = i < hi ? in[i] : 0u;
-    uint32_t tot;
-    uint32_t ex = block_exclusive<kScanBlock>(v, scratch, &tot);
-    if (i < hi) out[i] = run + ex;
-    run += tot;
-  }
-}
-
 // ---------------------------------------------------------------- radix
 constexpr int kRBlock = 256;  // threads; one per digit bin
 constexpr int kRWarps = kRBlock / 32;
 constexpr int kRItems = 8;
 constexpr int kRTile = kRBlock * kRItems;  // 2048 pairs per tile
 
-__global__ void __launch_bounds__(kRBlock) radix_upsweep_k(const uint32_t* keys,
-                                                           const uint32_t* n_dev,
-                                                           uint32_t n_host, int shift,
-                                                           uint32_t mask,
-                                                           uint32_t* counts) {
-  __shared__ uint32_t hist[kRWarps][256];
-  for (int i = threadIdx.x; i < kRWarps * 256; i += kRBlock) (&hist[0][0])[i] = 0;
-  __syncthreads();
-  uint32_t n = load_n(n_dev, n_host), lo, hi;
-  block_range(n, kRTile, &lo, &hi);
-  const int warp = threadIdx.x >> 5;
-  for (uint32_t i = lo + threadIdx.x; i < hi; i += kRBlock)
-    atomicAdd(&hist[warp][(keys[i] >> shift) & mask], 1u);
-  __syncthreads();
-  uint32_t s = 0;
-#pragma unroll
-  for (int w = 0; w < kRWarps; ++w) s += hist[w][threadIdx.x];
-  counts[threadIdx.x * gridDim.x + blockIdx.x] = s;  // digit-major
+// ------------------------------------------------ single-pass primitives
+// Decoupled look-back (Merrill & Garland): tiles are claimed in order through
+// an atomic counter by a persistent grid, each tile publishes its aggregate,
+// walks back over its predecessors' published values until it meets an
+// inclusive prefix, and publishes its own.  One launch per scan and per
+// radix pass instead of reduce / scan / downsweep.  Status words: 2-bit flag
+// (0 = empty, 1 = aggregate, 2 = inclusive prefix) + 30-bit value; the caller
+// zeroes status + counter (one memset per primitive call).
+constexpr uint32_t kFlagA = 1u << 30, kFlagP = 2u << 30, kValMask = (1u << 30) - 1u;
+
+__device__ __forceinline__ uint32_t ld_status(const uint32_t* p) {
+  return *reinterpret_cast<const volatile uint32_t*>(p);
+}
+__device__ __forceinline__ void st_status(uint32_t* p, uint32_t v) {
+  *reinterpret_cast<volatile uint32_t*>(p) = v;
 }
 
-__global__ void __launch_bounds__(kRBlock) radix_downsweep_k(
+// exclusive prefix of tile t from the statuses of tiles t-1, t-2, ...
+__device__ __forceinline__ uint32_t look_back(const uint32_t* status, uint32_t t, uint32_t stride) {
+  uint32_t excl = 0;
+  for (int64_t j = (int64_t)t - 1; j >= 0; --j) {
+    uint32_t v;
+    do {
+      v = ld_status(status + (size_t)j * stride);
+    } while ((v & ~kValMask) == 0u);
+    excl += v & kValMask;
+    if (v & kFlagP) break;
+  }
+  return excl;
+}
+
+constexpr int kLbThreads = 512;
+constexpr int kLbItems = 8;
+constexpr int kLbTile = kLbThreads * kLbItems;  // 4096
+
+__global__ void __launch_bounds__(kLbThreads) scan_lb_k(const uint32_t* __restrict__ in,
+                                                        uint32_t* __restrict__ out,
+                                                        const uint32_t* n_dev, uint32_t n_host,
+                                                        uint32_t* total, uint32_t* status,
+                                                        uint32_t* counter) {
+  __shared__ uint32_t sdata[kLbTile + kLbTile / 32];
+  __shared__ uint32_t scratch[33];
+  __shared__ uint32_t s_tile, s_prefix;
+  const uint32_t n = load_n(n_dev, n_host);
+  const uint32_t n_tiles = (n + kLbTile - 1) / kLbTile;
+  if (n == 0) {
+    if (blockIdx.x == 0 && threadIdx.x == 0 && total) *total = 0;
+    return;
+  }
+  for (;;) {
+    if (threadIdx.x == 0) s_tile = atomicAdd(counter, 1u);
+    __syncthreads();
+    const uint32_t t = s_tile;
+    if (t >= n_tiles) break;
+    const uint32_t base = t * kLbTile;
+#pragma unroll
+    for (int it = 0; it < kLbItems; ++it) {
+      const uint32_t j = it * kLbThreads + threadIdx.x;
+      sdata[j + (j >> 5)] = base + j < n ? in[base + j] : 0u;
+    }
+    __syncthreads();
+    uint32_t v[kLbItems], sum = 0;
+#pragma unroll
+    for (int it = 0; it < kLbItems; ++it) {
+      const uint32_t j = threadIdx.x * kLbItems + it;
+      v[it] = sdata[j + (j >> 5)];
+      sum += v[it];
+    }
+    uint32_t agg;
+    uint32_t ex = block_exclusive<kLbThreads>(sum, scratch, &agg);
+    if (threadIdx.x == 0) {
+      uint32_t prefix = 0;
+      if (t == 0) {
+        st_status(status, kFlagP | agg);
+      } else {
+        st_status(status + t, kFlagA | agg);
+        prefix = look_back(status, t, 1);
+        st_status(status + t, kFlagP | ((prefix + agg) & kValMask));
+      }
+      s_prefix = prefix;
+      if (t == n_tiles - 1 && total) *total = prefix + agg;
+    }
+    __syncthreads();
+    ex += s_prefix;
+#pragma unroll
+    for (int it = 0; it < kLbItems; ++it) {
+      const uint32_t j = threadIdx.x * kLbItems + it;
+      sdata[j + (j >> 5)] = ex;
+      ex += v[it];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int it = 0; it < kLbItems; ++it) {
+      const uint32_t j = it * kLbThreads + threadIdx.x;
+      if (base + j < n) out[base + j] = sdata[j + (j >> 5)];
+    }
+    __syncthreads();
+  }
+}
+
+// all passes' digit histograms in one read of the keys
+__global__ void __launch_bounds__(kRBlock) radix_hist_k(const uint32_t* __restrict__ keys,
+                                                        const uint32_t* n_dev, uint32_t n_host,
+                                                        int begin_bit, int end_bit,
+                                                        uint32_t* __restrict__ ghist) {
+  __shared__ uint32_t h[4][256];
+  for (int i = threadIdx.x; i < 4 * 256; i += kRBlock) (&h[0][0])[i] = 0;
+  __syncthreads();
+  const uint32_t n = load_n(n_dev, n_host);
+  const int passes = (end_bit - begin_bit + 7) / 8;
+  for (uint32_t i = blockIdx.x * kRBlock + threadIdx.x; i < n; i += gridDim.x * kRBlock) {
+    const uint32_t k = keys[i];
+    for (int p = 0; p < passes; ++p) {
+      const int b = begin_bit + 8 * p;
+      const int bits = end_bit - b < 8 ? end_bit - b : 8;
+      atomicAdd(&h[p][(k >> b) & ((1u << bits) - 1u)], 1u);
+    }
+  }
+  __syncthreads();
+  for (int p = 0; p < passes; ++p) {
+    const uint32_t c = h[p][threadIdx.x];
+    if (c) atomicAdd(&ghist[p * 256 + threadIdx.x], c);
+  }
+}
+
+__global__ void __launch_bounds__(kRBlock) radix_onesweep_k(
     const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin,
     uint32_t* __restrict__ kout, uint32_t* __restrict__ vout, const uint32_t* n_dev,
-    uint32_t n_host, int shift, uint32_t mask, const uint32_t* __restrict__ offsets) {
+    uint32_t n_host, int shift, uint32_t mask, const uint32_t* __restrict__ hist,
+    uint32_t* status, uint32_t* counter) {
   __shared__ uint32_t wcnt[kRWarps][257];
   __shared__ uint32_t skey[kRTile];
   __shared__ uint32_t sval[kRTile];
+  __shared__ uint32_t dbase[256];
   __shared__ uint32_t run[256];
   __shared__ uint32_t tpre[256];
   __shared__ uint32_t scratch[33];
+  __shared__ uint32_t s_tile;
 
-  uint32_t n = load_n(n_dev, n_host), lo, hi;
-  block_range(n, kRTile, &lo, &hi);
+  const uint32_t n = load_n(n_dev, n_host);
+  const uint32_t n_tiles = (n + kRTile - 1) / kRTile;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  run[threadIdx.x] = offsets[threadIdx.x * gridDim.x + blockIdx.x];
-
-  for (uint32_t base = lo; base < hi; base += kRTile) {
+  {
+    uint32_t all;
+    dbase[threadIdx.x] = block_exclusive<kRBlock>(hist[threadIdx.x], scratch, &all);
+  }
+  for (;;) {
+    if (threadIdx.x == 0) s_tile = atomicAdd(counter, 1u);
     for (int i = threadIdx.x; i < kRWarps * 257; i += kRBlock) (&wcnt[0][0])[i] = 0;
     __syncthreads();
+    const uint32_t t = s_tile;
+    if (t >= n_tiles) break;
+    const uint32_t base = t * kRTile;
+    const uint32_t hi = min(n, base + kRTile);
     uint32_t k[kRItems], v[kRItems], d[kRItems], rk[kRItems];
     const uint32_t wbase = base + warp * 32 * kRItems;
 #pragma unroll
     for (int it = 0; it < kRItems; ++it) {
-      uint32_t idx = wbase + it * 32 + lane;
-      bool ok = idx < hi;
+      const uint32_t idx = wbase + it * 32 + lane;
+      const bool ok = idx < hi;
       k[it] = ok ? kin[idx] : 0u;
       v[it] = ok ? vin[idx] : 0u;
       d[it] = ok ? ((k[it] >> shift) & mask) : 256u;
     }
 #pragma unroll
     for (int it = 0; it < kRItems; ++it) {
-      uint32_t peers = __match_any_sync(0xffffffffu, d[it]);
-      uint32_t before = wcnt[warp][d[it]];
+      const uint32_t peers = __match_any_sync(0xffffffffu, d[it]);
+      const uint32_t before = wcnt[warp][d[it]];
       rk[it] = before + __popc(peers & lanemask_lt());
       __syncwarp();
       if (lane == __ffs(peers) - 1) wcnt[warp][d[it]] = before + __popc(peers);
       __syncwarp();
     }
     __syncthreads();
-    // per digit: exclusive prefix over warps, tile total
     uint32_t tot = 0;
 #pragma unroll
     for (int w = 0; w < kRWarps; ++w) {
-      uint32_t c = wcnt[w][threadIdx.x];
+      const uint32_t c = wcnt[w][threadIdx.x];
       wcnt[w][threadIdx.x] = tot;
       tot += c;
     }
+    // publish this tile's digit counts, look back for the digit prefix
+    uint32_t* my = status + (size_t)t * 256 + threadIdx.x;
+    uint32_t excl = 0;
+    if (t == 0) {
+      st_status(my, kFlagP | tot);
+    } else {
+      st_status(my, kFlagA | tot);
+      excl = look_back(status + threadIdx.x, t, 256);
+      st_status(my, kFlagP | ((excl + tot) & kValMask));
+    }
+    run[threadIdx.x] = dbase[threadIdx.x] + excl;
     uint32_t all;
-    uint32_t pre = block_exclusive<kRBlock>(tot, scratch, &all);
-    tpre[threadIdx.x] = pre;
+    tpre[threadIdx.x] = block_exclusive<kRBlock>(tot, scratch, &all);
     __syncthreads();
 #pragma unroll
     for (int it = 0; it < kRItems; ++it) {
       if (d[it] < 256u) {
-        uint32_t lp = tpre[d[it]] + wcnt[warp][d[it]] + rk[it];
+        const uint32_t lp = tpre[d[it]] + wcnt[warp][d[it]] + rk[it];
         skey[lp] = k[it];
         sval[lp] = v[it];
       }
     }
     __syncthreads();
-    const uint32_t cnt = min(hi - base, (uint32_t)kRTile);
+    const uint32_t cnt = hi - base;
     for (uint32_t j = threadIdx.x; j < cnt; j += kRBlock) {
-      uint32_t kk = skey[j];
-      uint32_t dd = (kk >> shift) & mask;
-      uint32_t pos = run[dd] + (j - tpre[dd]);
+      const uint32_t kk = skey[j];
+      const uint32_t dd = (kk >> shift) & mask;
+      const uint32_t pos = run[dd] + (j - tpre[dd]);
       kout[pos] = kk;
       vout[pos] = sval[j];
     }
     __syncthreads();
-    run[threadIdx.x] += tot;
-    __syncthreads();
   }
+}
+
+int persistent_grid(const void* kern, int threads, int cap) {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = kSMs;
+  }
+  int per = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, threads, 0);
+  if (per <= 0) per = 1;
+  const int g = sms * per;
+  return cap > 0 && cap < g ? cap : g;
 }
 
 }  // namespace
 
-size_t scan_ws_bytes() { return sizeof(uint32_t) * (kPrimGrid + 32); }
+size_t scan_ws_bytes(uint32_t n_max) {
+  return sizeof(uint32_t) * (((size_t)n_max + kLbTile - 1) / kLbTile + 64);
+}
 
 int32_t scan_exclusive_u32(const uint32_t* in, uint32_t* out, const uint32_t* n_dev,
-                           uint32_t n_host, uint32_t* total, void* ws, cudaStream_t s) {
-  uint32_t* partial = static_cast<uint32_t*>(ws);
-  scan_reduce_k<<<kPrimGrid, kScanBlock, 0, s>>>(in, n_dev, n_host, partial);
-  mark("scan_reduce", s);
-  scan_single_k<<<1, kScanBlock, 0, s>>>(partial, kPrimGrid, total);
-  mark("scan_single", s);
-  scan_down_k<<<kPrimGrid, kScanBlock, 0, s>>>(in, out, n_dev, n_host, partial);
-  mark("scan_down", s);
+                           uint32_t n_host, uint32_t n_max, uint32_t* total, void* ws,
+                           cudaStream_t s) {
+  const uint32_t max_tiles = (n_max + kLbTile - 1) / kLbTile;
+  uint32_t* counter = static_cast<uint32_t*>(ws);
+  uint32_t* status = counter + 32;
+  VMS_CUDA(cudaMemsetAsync(ws, 0, scan_ws_bytes(n_max), s));
+  const int grid = persistent_grid((const void*)scan_lb_k, kLbThreads, max_tiles ? max_tiles : 1);
+  scan_lb_k<<<grid, kLbThreads, 0, s>>>(in, out, n_dev, n_host, total, status, counter);
+  mark("scan", s);
   VMS_LAUNCH_CHECK("scan_exclusive_u32");
   return VMS_OK;
 }
 
-size_t radix_ws_bytes() { return sizeof(uint32_t) * (256 * kPrimGrid + 64) + scan_ws_bytes() + 256; }
+size_t radix_ws_bytes(uint32_t n_max) {
+  const size_t tiles = ((size_t)n_max + kRTile - 1) / kRTile;
+  return sizeof(uint32_t) * (64 + 4 * 256 + 4 * 256 * tiles) + 256;
+}
 
 int32_t radix_sort_u32(uint32_t* k0, uint32_t* v0, uint32_t* k1, uint32_t* v1,
-                       const uint32_t* n_dev, uint32_t n_host, int begin_bit, int end_bit,
-                       int* in_alt, void* ws, cudaStream_t s) {
-  uint32_t* counts = static_cast<uint32_t*>(ws);
-  void* scan_ws = reinterpret_cast<char*>(ws) +
-                  ((sizeof(uint32_t) * (256 * kPrimGrid + 64) + 255) & ~size_t(255));
+                       const uint32_t* n_dev, uint32_t n_host, uint32_t n_max, int begin_bit,
+                       int end_bit, int* in_alt, void* ws, cudaStream_t s) {
+  const int passes = (end_bit - begin_bit + 7) / 8;
+  if (passes > 4) {
+    set_error("radix_sort_u32: at most 32 key bits");
+    return VMS_ERR_INVALID;
+  }
+  const size_t tiles = ((size_t)n_max + kRTile - 1) / kRTile;
+  uint32_t* counters = static_cast<uint32_t*>(ws);  // one per pass
+  uint32_t* ghist = counters + 64;                  // [passes][256]
+  uint32_t* status = ghist + 4 * 256;               // [passes][tiles][256]
+  VMS_CUDA(cudaMemsetAsync(ws, 0, sizeof(uint32_t) * (64 + 4 * 256 + passes * 256 * tiles), s));
+  const int hgrid = persistent_grid((const void*)radix_hist_k, kRBlock, 0);
+  radix_hist_k<<<hgrid, kRBlock, 0, s>>>(k0, n_dev, n_host, begin_bit, end_bit, ghist);
+  mark("radix_hist", s);
+  const int grid = persistent_grid((const void*)radix_onesweep_k, kRBlock, tiles ? (int)tiles : 1);
   int alt = 0;
-  for (int b = begin_bit; b < end_bit; b += 8) {
-    int bits = end_bit - b < 8 ? end_bit - b : 8;
-    uint32_t mask = (1u << bits) - 1u;
+  for (int p = 0; p < passes; ++p) {
+    const int b = begin_bit + 8 * p;
+    const int bits = end_bit - b < 8 ? end_bit - b : 8;
+    const uint32_t mask = (1u << bits) - 1u;
     uint32_t *ki = alt ? k1 : k0, *vi = alt ? v1 : v0;
     uint32_t *ko = alt ? k0 : k1, *vo = alt ? v0 : v1;
-    radix_upsweep_k<<<kPrimGrid, kRBlock, 0, s>>>(ki, n_dev, n_host, b, mask, counts);
-    mark("radix_up", s);
-    // digit-major counts -> global (digit, block) offsets; only the digits
-    // this pass can produce are scanned
-    int32_t st = scan_exclusive_u32(counts, counts, nullptr, (mask + 1u) * kPrimGrid, nullptr,
-                                    scan_ws, s);
-    if (st) return st;
-    radix_downsweep_k<<<kPrimGrid, kRBlock, 0, s>>>(ki, vi, ko, vo, n_dev, n_host, b, mask,
-                                                    counts);
-    mark("radix_down", s);
+    radix_onesweep_k<<<grid, kRBlock, 0, s>>>(ki, vi, ko, vo, n_dev, n_host, b, mask,
+                                              ghist + p * 256, status + (size_t)p * 256 * tiles,
+                                              counters + p);
+    mark("radix_pass", s);
     alt ^= 1;
   }
   VMS_LAUNCH_CHECK("radix_sort_u32");

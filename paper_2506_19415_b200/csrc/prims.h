@@ -8,22 +8,21 @@
 
 namespace vms {
 
-// Fixed grid used by the count-agnostic primitives: 2 CTAs per SM.
-constexpr int kPrimGrid = 296;
-
 // Exclusive scan of n u32 values; n = *n_dev when n_dev != nullptr, else
 // n_host.  *total (device, optional) receives the sum.  ws needs
 // scan_ws_bytes() bytes.
-size_t scan_ws_bytes();
+// n_max: upper bound on n (sizes the look-back status array in ws).
+size_t scan_ws_bytes(uint32_t n_max);
 int32_t scan_exclusive_u32(const uint32_t* in, uint32_t* out, const uint32_t* n_dev,
-                           uint32_t n_host, uint32_t* total, void* ws, cudaStream_t s);
+                           uint32_t n_host, uint32_t n_max, uint32_t* total, void* ws,
+                           cudaStream_t s);
 
 // Stable LSD radix sort of (u32 key, u32 value) pairs over key bits
 // [begin_bit, end_bit).  Ping-pongs between (k0,v0) and (k1,v1); returns via
 // *in_alt whether the sorted result ended in (k1, v1).  n as for the scan.
-size_t radix_ws_bytes();
+size_t radix_ws_bytes(uint32_t n_max);
 int32_t radix_sort_u32(uint32_t* k0, uint32_t* v0, uint32_t* k1, uint32_t* v1,
-                       const uint32_t* n_dev, uint32_t n_host, int begin_bit,
+                       const uint32_t* n_dev, uint32_t n_host, uint32_t n_max, int begin_bit,
                        int end_bit, int* in_alt, void* ws, cudaStream_t s);
 
 }  // namespace vms

@@ -48,6 +48,7 @@ struct RenderWs {
   uint32_t *cnt, *off;
   uint32_t *tk0, *tv0, *tk1, *tv1;
   uint32_t* ranges;  // 2 per tile
+  uint32_t* order;   // blend schedule: tiles, longest list first
   RenderCounters* ctr;
   void* scan_ws;
   void* radix_ws;

@@ -332,7 +332,7 @@ size_t vis_ws_bytes(uint32_t n_faces, uint32_t page_count) {
   b += sizeof(VisTri) * ((size_t)n_faces * 2 + 1);   // clipped triangles
   b += sizeof(uint32_t) * (page_count + 1) * 3;      // base, depth, flags/pos
   b += sizeof(uint8_t) * (page_count + 1);           // direct
-  b += scan_ws_bytes() + 1024;
+  b += scan_ws_bytes(n_faces > page_count + 1 ? n_faces : page_count + 1) + 1024;
   return b + 8 * 256;
 }
 
@@ -365,7 +365,7 @@ VisWs carve_ws(void* ws, uint32_t nf, uint32_t P) {
   w.depth = carve<uint32_t>(p, P + 1);
   w.pos = carve<uint32_t>(p, P + 1);
   w.direct = carve<uint8_t>(p, P + 1);
-  w.scan = carve<char>(p, scan_ws_bytes());
+  w.scan = carve<char>(p, scan_ws_bytes(nf > P + 1 ? nf : P + 1));
   return w;
 }
 }  // namespace
@@ -385,7 +385,8 @@ int32_t vis_frame(const VisArgs& a, cudaStream_t s) {
     vis_count_k<<<ceil_div<uint32_t>(a.n_faces, T), T, 0, s>>>(a.cam, a.verts, a.faces,
                                                                 a.n_faces, w.counts);
     mark("vis_count", s);
-    int32_t st = scan_exclusive_u32(w.counts, w.offsets, nullptr, a.n_faces, w.n_tris, w.scan, s);
+    int32_t st = scan_exclusive_u32(w.counts, w.offsets, nullptr, a.n_faces, a.n_faces, w.n_tris,
+                                    w.scan, s);
     if (st) return st;
     vis_emit_k<<<ceil_div<uint32_t>(a.n_faces, T), T, 0, s>>>(
         a.cam, a.verts, a.faces, a.face_page, a.n_faces, w.offsets, w.tris);
@@ -406,7 +407,8 @@ int32_t vis_frame(const VisArgs& a, cudaStream_t s) {
   vis_flags_k<<<ceil_div<uint32_t>(a.page_count + 1, T), T, 0, s>>>(w.depth, a.page_count,
                                                                      w.pos);
   mark("vis_flags", s);
-  int32_t st = scan_exclusive_u32(w.pos, w.pos, nullptr, a.page_count + 1, w.n_req, w.scan, s);
+  int32_t st = scan_exclusive_u32(w.pos, w.pos, nullptr, a.page_count + 1, a.page_count + 1,
+                                  w.n_req, w.scan, s);
   if (st) return st;
   vis_required_k<<<ceil_div<uint32_t>(a.page_count + 1, T), T, 0, s>>>(
       w.depth, w.direct, w.pos, a.page_count, a.lod, a.out);
