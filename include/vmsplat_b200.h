@@ -153,9 +153,9 @@ int64_t vms_profile_report(char* buf, int64_t len);
 
 /* composite_splats (kernels/__init__.py:24-33, _core.pyx:24-78): blend n
  * caller-ordered splats into image (h, w, 3) f32 in place.  n_instances is
- * an upper bound on the 16x16-tile instances (sum over splats of the tiles
- * their clamped box touches); a smaller true count is fine, a larger one
- * fails with VMS_ERR_NOMEM and leaves image unchanged. */
+ * the tile-instance capacity (sum over splats of the blend tiles their
+ * clamped box touches); an undersized capacity still gives the exact image,
+ * blended from the ordered splat list instead of per-tile lists (slower). */
 size_t vms_composite_workspace_bytes(int64_t n, int64_t n_instances, int32_t h, int32_t w);
 int32_t vms_composite_splats(const float* centers, const float* conics, const float* colors,
                              const float* alphas, const int32_t* bounds, int64_t n,
@@ -314,13 +314,16 @@ void vms_session_destroy(vms_session* s);
 vms_pagetable* vms_session_table(vms_session* s);
 int32_t vms_session_set_render_ws(vms_session* s, void* ws, uint64_t bytes, uint32_t m_cap,
                                   int32_t width, int32_t height);
-/* VMS_ERR_NOMEM: the tile-instance buffer overflowed (stats->n_need says how
- * many are needed) - either in this frame (when the call synchronised) or in
- * the previous one; grow the workspace, vms_session_rerender(), and for a
- * previous-frame overflow repeat this call (nothing was mutated). */
+/* One frame (runtime.py:436-489).  Returns once the frame is enqueued: the
+ * visibility pass and the host page table are done, the render is in flight
+ * on `stream` (replayed from a CUDA graph).  With host_image or timing set the
+ * call also waits for the render and fills the device counters.  A frame
+ * whose tile instances overflow the buffer is still blended exactly (through
+ * the depth-sorted splat list, slower); the session grows the buffer for the
+ * frames after it. */
 int32_t vms_session_frame(vms_session* s, const vms_frame_args* args, vms_frame_stats* stats,
                           void* stream);
-int32_t vms_session_rerender(vms_session* s, float* host_image, void* stream);
+/* Wait for the last frame; out4 = its n_kept, n_inst, overflow, n_need. */
 int32_t vms_session_counters(vms_session* s, uint32_t* out4, void* stream);
 
 #ifdef __cplusplus

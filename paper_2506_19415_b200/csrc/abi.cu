@@ -355,10 +355,17 @@ int32_t vms_render(const vms_render_args* a, void* stream) {
       tile_count(a->cam.width, a->cam.height);
   RenderWs w = render_carve(a->workspace, a->n_cap, a->m_cap, tiles);
   mark("begin", s);
-  int32_t st = render_preprocess(a->pool, a->chunks, a->n_chunks, a->cam, w, s);
+  FrameDev f{};
+  f.cam = a->cam;
+  f.image = a->image;
+  f.n_chunks = a->n_chunks;
+  f.n_splats = a->n_splats;
+  int32_t st = render_upload_frame(w, f, s);
+  if (st) return st;
+  st = render_preprocess(a->pool, a->chunks, a->n_chunks, w, s);
   if (st) return st;
   if (a->events[0]) VMS_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(a->events[0]), s));
-  st = render_finish(a->cam, a->n_splats, w, a->image, a->accumulate, a->exact, a->events, s);
+  st = render_finish(a->cam.width, a->cam.height, w, a->accumulate, a->exact, a->events, false, s);
   if (st) return st;
   if (a->counters_out)
     VMS_CUDA(cudaMemcpyAsync(a->counters_out, w.ctr, sizeof(uint32_t) * 4,

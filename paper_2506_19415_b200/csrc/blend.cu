@@ -51,13 +51,15 @@ T* carve(char*& p, size_t n) {
 }
 
 __global__ void compact_k(const uint32_t* __restrict__ flag, const uint32_t* __restrict__ pos,
-                          const uint32_t* __restrict__ key_g, uint32_t n,
+                          const uint32_t* __restrict__ key_g, const uint32_t* n_dev, uint32_t n_host,
                           uint32_t* __restrict__ k0, uint32_t* __restrict__ v0) {
-  uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
-  if (g >= n || !flag[g]) return;
-  const uint32_t o = pos[g];
-  k0[o] = key_g[g];
-  v0[o] = g;
+  const uint32_t n = n_dev ? *n_dev : n_host;
+  for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < n; g += gridDim.x * blockDim.x) {
+    if (!flag[g]) continue;
+    const uint32_t o = pos[g];
+    k0[o] = key_g[g];
+    v0[o] = g;
+  }
 }
 
 __device__ __forceinline__ void tile_rect(const BlendRec& r, int shift, int* tx0, int* tx1,
@@ -192,13 +194,21 @@ __global__ void __launch_bounds__(1024) tile_order_k(const uint32_t* __restrict_
   }
 }
 
+// Tile-instance overflow (the frame needs more instances than the buffer
+// holds): the tile lists were not built, and every CTA walks the whole
+// depth-sorted splat list `vals` instead, filtering by its own sub-tile - the
+// same per-tile order, so the image is identical, only slower.  The host
+// sees the overflow counter afterwards and grows the buffer for later frames.
 template <bool kExact, int TS>
 __global__ void __launch_bounds__(kBlendThreads) blend_k(const uint32_t* __restrict__ ranges,
                                                          const uint32_t* __restrict__ order,
-                                                         const uint32_t* __restrict__ tv,
+                                                         const uint32_t* __restrict__ tv_tiles,
+                                                         const uint32_t* __restrict__ vals,
+                                                         const RenderCounters* __restrict__ ctr,
                                                          const BlendRec* __restrict__ rec,
                                                          int w, int h, int tiles_x,
-                                                         float* __restrict__ image,
+                                                         float* image_arg,
+                                                         const FrameDev* __restrict__ fd,
                                                          int accumulate) {
   constexpr int SUB = TS / 16;  // sub-tiles per tile edge
   using Staged = typename std::conditional<kExact, SplatF64, BlendRec>::type;
@@ -209,7 +219,11 @@ __global__ void __launch_bounds__(kBlendThreads) blend_k(const uint32_t* __restr
   const int sy0 = (tile / tiles_x) * TS + (sub / SUB) * 16;
   const int px = sx0 + (threadIdx.x & 15), py = sy0 + (threadIdx.x >> 4);
   const bool inside = px < w && py < h;
-  const uint32_t start = ranges[2 * tile], end = ranges[2 * tile + 1];
+  const bool spill = ctr->overflow != 0u;
+  const uint32_t start = spill ? 0u : ranges[2 * tile];
+  const uint32_t end = spill ? ctr->n_kept : ranges[2 * tile + 1];
+  const uint32_t* __restrict__ tv = spill ? vals : tv_tiles;
+  float* __restrict__ image = image_arg ? image_arg : fd->image;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   float cr = 0.f, cg = 0.f, cb = 0.f, T = 1.f;
   if (accumulate && inside) {
@@ -355,11 +369,17 @@ int tile_bits(uint32_t n_tiles) {
   return b;
 }
 
-int32_t tiles_and_blend(const RenderCamera& cam, const uint32_t* vals, const RenderWs& w,
+void record(void* const* events, int i, bool external, cudaStream_t s) {
+  if (events && events[i])
+    cudaEventRecordWithFlags(static_cast<cudaEvent_t>(events[i]), s,
+                             external ? cudaEventRecordExternal : cudaEventRecordDefault);
+}
+
+int32_t tiles_and_blend(int width, int height, const uint32_t* vals, const RenderWs& w,
                         float* image, int accumulate, int exact, void* const* events,
-                        cudaStream_t s) {
+                        bool external, cudaStream_t s) {
   const int ts = tile_size(), shift = ts == 16 ? 4 : 5;
-  const int tiles_x = ceil_div(cam.width, ts), tiles_y = ceil_div(cam.height, ts);
+  const int tiles_x = ceil_div(width, ts), tiles_y = ceil_div(height, ts);
   const uint32_t n_tiles = (uint32_t)tiles_x * tiles_y;
   const int T = 256;
   dup_count_k<<<4 * kSMs, T, 0, s>>>(vals, w.rec, w.ctr, shift, w.cnt);
@@ -383,14 +403,14 @@ int32_t tiles_and_blend(const RenderCamera& cam, const uint32_t* vals, const Ren
   mark("ranges", s);
   tile_order_k<<<1, 1024, 0, s>>>(w.ranges, n_tiles, w.order);
   mark("tile_order", s);
-  if (events && events[2]) VMS_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(events[2]), s));
+  record(events, 2, external, s);
   auto* kern = exact ? (ts == 16 ? blend_k<true, 16> : blend_k<true, 32>)
                      : (ts == 16 ? blend_k<false, 16> : blend_k<false, 32>);
   const uint32_t subs = (uint32_t)(ts / 16) * (ts / 16);
-  kern<<<n_tiles * subs, kBlendThreads, 0, s>>>(w.ranges, w.order, tv, w.rec, cam.width, cam.height,
-                                                tiles_x, image, accumulate);
+  kern<<<n_tiles * subs, kBlendThreads, 0, s>>>(w.ranges, w.order, tv, vals, w.ctr, w.rec, width,
+                                                height, tiles_x, image, w.fd, accumulate);
   mark("blend", s);
-  if (events && events[3]) VMS_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(events[3]), s));
+  record(events, 3, external, s);
   VMS_LAUNCH_CHECK("tiles_and_blend");
   return VMS_OK;
 }
@@ -404,7 +424,7 @@ size_t render_ws_bytes(uint32_t n_cap, uint32_t m_cap, uint32_t n_tiles) {
   b += sizeof(uint32_t) * (size_t)n_cap * 6;   // k0 v0 k1 v1 cnt off
   b += sizeof(uint32_t) * (size_t)m_cap * 4;   // tk0 tv0 tk1 tv1
   b += sizeof(uint32_t) * 3 * (size_t)n_tiles; // ranges + order
-  b += sizeof(RenderCounters);
+  b += sizeof(RenderCounters) + sizeof(FrameDev);
   b += scan_ws_bytes(n_cap) + radix_ws_bytes(n_cap > m_cap ? n_cap : m_cap);
   return b + 256 * 20;
 }
@@ -431,40 +451,40 @@ RenderWs render_carve(void* ws, uint32_t n_cap, uint32_t m_cap, uint32_t n_tiles
   w.ranges = carve<uint32_t>(p, 2 * (size_t)n_tiles);
   w.order = carve<uint32_t>(p, (size_t)n_tiles);
   w.ctr = carve<RenderCounters>(p, 1);
+  w.fd = carve<FrameDev>(p, 1);
   w.scan_ws = carve<char>(p, scan_ws_bytes(n_cap));
   w.radix_ws = carve<char>(p, radix_ws_bytes(n_cap > m_cap ? n_cap : m_cap));
   return w;
 }
 
-int32_t render_finish(const RenderCamera& cam, uint32_t n_splats, const RenderWs& w,
-                      float* image, int accumulate, int exact, void* const* events,
-                      cudaStream_t s) {
+int32_t render_upload_frame(const RenderWs& w, const FrameDev& f, cudaStream_t s) {
+  VMS_CUDA(cudaMemcpyAsync(w.fd, &f, sizeof(FrameDev), cudaMemcpyHostToDevice, s));
+  return VMS_OK;
+}
+
+int32_t render_finish(int width, int height, const RenderWs& w, int accumulate, int exact,
+                      void* const* events, bool external, cudaStream_t s) {
   const int T = 256;
   VMS_CUDA(cudaMemsetAsync(w.ctr, 0, sizeof(RenderCounters), s));
-  if (n_splats) {
-    int32_t st = scan_exclusive_u32(w.flag, w.pos, nullptr, n_splats, n_splats, &w.ctr->n_kept,
-                                    w.scan_ws, s);
-    if (st) return st;
-    compact_k<<<ceil_div<uint32_t>(n_splats, T), T, 0, s>>>(w.flag, w.pos, w.key_g, n_splats,
-                                                             w.k0, w.v0);
-    mark("compact", s);
-  }
+  int32_t st = scan_exclusive_u32(w.flag, w.pos, &w.fd->n_splats, 0, w.n_cap, &w.ctr->n_kept,
+                                  w.scan_ws, s);
+  if (st) return st;
+  compact_k<<<8 * kSMs, T, 0, s>>>(w.flag, w.pos, w.key_g, &w.fd->n_splats, 0, w.k0, w.v0);
+  mark("compact", s);
   int alt = 0;
   // keys are IEEE bits of positive f32 depths: bit 31 is always clear
-  int32_t st = radix_sort_u32(w.k0, w.v0, w.k1, w.v1, &w.ctr->n_kept, 0, w.n_cap, 0, 31, &alt,
-                              w.radix_ws, s);
+  st = radix_sort_u32(w.k0, w.v0, w.k1, w.v1, &w.ctr->n_kept, 0, w.n_cap, 0, 31, &alt,
+                      w.radix_ws, s);
   if (st) return st;
-  if (events && events[1]) VMS_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(events[1]), s));
-  return tiles_and_blend(cam, alt ? w.v1 : w.v0, w, image, accumulate, exact, events, s);
+  record(events, 1, external, s);
+  return tiles_and_blend(width, height, alt ? w.v1 : w.v0, w, nullptr, accumulate, exact, events,
+                         external, s);
 }
 
 int32_t composite_ordered(const float* centers, const float* conics, const float* colors,
                           const float* alphas, const int32_t* bounds, uint32_t n, float* image,
                           int h, int w, int exact, const RenderWs& ws, cudaStream_t s) {
   const int T = 256;
-  RenderCamera cam = {};
-  cam.width = w;
-  cam.height = h;
   VMS_CUDA(cudaMemsetAsync(ws.ctr, 0, sizeof(RenderCounters), s));
   if (n) {
     // splats with an empty clamped box are dropped; the rest keep their order
@@ -473,9 +493,10 @@ int32_t composite_ordered(const float* centers, const float* conics, const float
     int32_t st = scan_exclusive_u32(ws.flag, ws.pos, nullptr, n, n, &ws.ctr->n_kept, ws.scan_ws,
                                     s);
     if (st) return st;
-    compact_k<<<ceil_div<uint32_t>(n, T), T, 0, s>>>(ws.flag, ws.pos, ws.v1, n, ws.k0, ws.v0);
+    compact_k<<<ceil_div<uint32_t>(n, T), T, 0, s>>>(ws.flag, ws.pos, ws.v1, nullptr, n, ws.k0,
+                                                     ws.v0);
   }
-  return tiles_and_blend(cam, ws.v0, ws, image, 1, exact, nullptr, s);
+  return tiles_and_blend(w, h, ws.v0, ws, image, 1, exact, nullptr, false, s);
 }
 
 }  // namespace vms

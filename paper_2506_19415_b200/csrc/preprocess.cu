@@ -167,9 +167,13 @@ __device__ __forceinline__ void project_one(const float* r, const RenderCamera& 
 }
 
 __global__ void __launch_bounds__(kChunkRecords) preprocess_k(
-    const float* __restrict__ pool, const Chunk* __restrict__ chunks, RenderCamera cam,
-    uint32_t* __restrict__ key_g, uint32_t* __restrict__ flag, BlendRec* __restrict__ rec) {
+    const float* __restrict__ pool, const Chunk* __restrict__ chunks,
+    const FrameDev* __restrict__ fd, uint32_t* __restrict__ key_g, uint32_t* __restrict__ flag,
+    BlendRec* __restrict__ rec) {
   __shared__ __align__(16) float srec[kChunkRecords * kRecordFloats];
+  __shared__ RenderCamera cam;
+  if (blockIdx.x >= fd->n_chunks) return;  // grid sized for the largest table
+  if (threadIdx.x == 0) cam = fd->cam;
   const Chunk ch = chunks[blockIdx.x];
   const float* src = pool + (size_t)ch.row * kRecordFloats;
   const uint32_t nf = ch.count * kRecordFloats;
@@ -247,10 +251,10 @@ __global__ void sh_k(const double* __restrict__ coeffs, const double* __restrict
 
 }  // namespace
 
-int32_t render_preprocess(const float* pool, const Chunk* chunks, uint32_t n_chunks,
-                          const RenderCamera& cam, const RenderWs& w, cudaStream_t s) {
-  if (n_chunks == 0) return VMS_OK;
-  preprocess_k<<<n_chunks, kChunkRecords, 0, s>>>(pool, chunks, cam, w.key_g, w.flag, w.rec);
+int32_t render_preprocess(const float* pool, const Chunk* chunks, uint32_t max_chunks,
+                          const RenderWs& w, cudaStream_t s) {
+  if (max_chunks == 0) return VMS_OK;
+  preprocess_k<<<max_chunks, kChunkRecords, 0, s>>>(pool, chunks, w.fd, w.key_g, w.flag, w.rec);
   mark("preprocess", s);
   VMS_LAUNCH_CHECK("render_preprocess");
   return VMS_OK;

@@ -162,15 +162,25 @@ __global__ void __launch_bounds__(kLbThreads) scan_lb_k(const uint32_t* __restri
 }
 
 // all passes' digit histograms in one read of the keys
+// Also zeroes the look-back status words the passes will use (sized by the
+// device-side count, so the host never clears a buffer sized for the worst
+// case).
 __global__ void __launch_bounds__(kRBlock) radix_hist_k(const uint32_t* __restrict__ keys,
                                                         const uint32_t* n_dev, uint32_t n_host,
                                                         int begin_bit, int end_bit,
-                                                        uint32_t* __restrict__ ghist) {
+                                                        uint32_t* __restrict__ ghist,
+                                                        uint32_t* __restrict__ status,
+                                                        size_t pass_stride) {
   __shared__ uint32_t h[4][256];
   for (int i = threadIdx.x; i < 4 * 256; i += kRBlock) (&h[0][0])[i] = 0;
   __syncthreads();
   const uint32_t n = load_n(n_dev, n_host);
   const int passes = (end_bit - begin_bit + 7) / 8;
+  const size_t used = (size_t)((n + kRTile - 1) / kRTile) * 256;
+  for (int p = 0; p < passes; ++p)
+    for (size_t i = blockIdx.x * (size_t)kRBlock + threadIdx.x; i < used;
+         i += (size_t)gridDim.x * kRBlock)
+      status[p * pass_stride + i] = 0u;
   for (uint32_t i = blockIdx.x * kRBlock + threadIdx.x; i < n; i += gridDim.x * kRBlock) {
     const uint32_t k = keys[i];
     for (int p = 0; p < passes; ++p) {
@@ -285,9 +295,23 @@ int persistent_grid(const void* kern, int threads, int cap) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (sms <= 0) sms = kSMs;
   }
+  // occupancy per (kernel, block size), queried once (also keeps the query
+  // out of graph captures)
+  static const void* keys[16] = {};
+  static int vals[16] = {};
   int per = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, threads, 0);
-  if (per <= 0) per = 1;
+  for (int i = 0; i < 16; ++i)
+    if (keys[i] == kern && vals[i] >> 16 == threads) per = vals[i] & 0xFFFF;
+  if (!per) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, threads, 0);
+    if (per <= 0) per = 1;
+    for (int i = 0; i < 16; ++i)
+      if (!keys[i]) {
+        keys[i] = kern;
+        vals[i] = (threads << 16) | per;
+        break;
+      }
+  }
   const int g = sms * per;
   return cap > 0 && cap < g ? cap : g;
 }
@@ -329,9 +353,10 @@ int32_t radix_sort_u32(uint32_t* k0, uint32_t* v0, uint32_t* k1, uint32_t* v1,
   uint32_t* counters = static_cast<uint32_t*>(ws);  // one per pass
   uint32_t* ghist = counters + 64;                  // [passes][256]
   uint32_t* status = ghist + 4 * 256;               // [passes][tiles][256]
-  VMS_CUDA(cudaMemsetAsync(ws, 0, sizeof(uint32_t) * (64 + 4 * 256 + passes * 256 * tiles), s));
+  VMS_CUDA(cudaMemsetAsync(ws, 0, sizeof(uint32_t) * (64 + 4 * 256), s));
   const int hgrid = persistent_grid((const void*)radix_hist_k, kRBlock, 0);
-  radix_hist_k<<<hgrid, kRBlock, 0, s>>>(k0, n_dev, n_host, begin_bit, end_bit, ghist);
+  radix_hist_k<<<hgrid, kRBlock, 0, s>>>(k0, n_dev, n_host, begin_bit, end_bit, ghist, status,
+                                         256 * tiles);
   mark("radix_hist", s);
   const int grid = persistent_grid((const void*)radix_onesweep_k, kRBlock, tiles ? (int)tiles : 1);
   int alt = 0;

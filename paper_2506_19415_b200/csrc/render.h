@@ -31,6 +31,18 @@ struct __align__(16) BlendRec {
   uint32_t pad_;
 };
 
+// Per-frame values every render kernel reads from device memory, so that a
+// frame's launch sequence is identical from frame to frame and can be
+// captured once into a CUDA graph (the host uploads this block, the chunk
+// table and the page copies before each graph launch).
+struct FrameDev {
+  vms_camera cam;
+  float* image;       // (h, w, 3) f32 output of this frame
+  uint32_t n_chunks;  // chunk-table rows in use
+  uint32_t n_splats;  // gather indices in use (resident records)
+  uint32_t pad_[2];
+};
+
 // Frame counters living in device memory.
 struct RenderCounters {
   uint32_t n_kept;
@@ -50,6 +62,7 @@ struct RenderWs {
   uint32_t* ranges;  // 2 per tile
   uint32_t* order;   // blend schedule: tiles, longest list first
   RenderCounters* ctr;
+  FrameDev* fd;
   void* scan_ws;
   void* radix_ws;
 };
@@ -58,15 +71,21 @@ size_t render_ws_bytes(uint32_t n_cap, uint32_t m_cap, uint32_t n_tiles);
 RenderWs render_carve(void* ws, uint32_t n_cap, uint32_t m_cap, uint32_t n_tiles);
 
 // Preprocess (EWA + SH, FP64) of every record named by the chunk table;
-// writes key_g / flag / rec at gather indices.
-int32_t render_preprocess(const float* pool, const Chunk* chunks, uint32_t n_chunks,
-                          const RenderCamera& cam, const RenderWs& w, cudaStream_t s);
+// writes key_g / flag / rec at gather indices.  Camera and chunk count come
+// from w.fd; max_chunks bounds the grid (CTAs past fd->n_chunks exit).
+int32_t render_preprocess(const float* pool, const Chunk* chunks, uint32_t max_chunks,
+                          const RenderWs& w, cudaStream_t s);
 
 // From preprocessed splats to an image: compaction, depth sort, tile
-// duplication, tile sort, ranges, blend.  n_splats = gather indices in use.
-int32_t render_finish(const RenderCamera& cam, uint32_t n_splats, const RenderWs& w,
-                      float* image, int accumulate, int exact, void* const* events,
-                      cudaStream_t s);
+// duplication, tile sort, ranges, blend.  Splat count and image pointer come
+// from w.fd; width/height fix the tile grid.  `events` (optional, 4) are
+// recorded after preprocess-side stages; `external` marks them as graph
+// event-record nodes when the sequence is being captured.
+int32_t render_finish(int width, int height, const RenderWs& w, int accumulate, int exact,
+                      void* const* events, bool external, cudaStream_t s);
+
+// Stage FrameDev from host memory (pageable or pinned) into w.fd.
+int32_t render_upload_frame(const RenderWs& w, const FrameDev& f, cudaStream_t s);
 
 // project_records / compute_keys over a contiguous record array; any output
 // pointer may be null except that centers..kept come together.

@@ -1,21 +1,32 @@
 // Per-frame orchestration in C++: VmSession.render_frame
 // (pkg/src/vmsplat/runtime.py:436-489) as ONE host call per frame, pipelined
-// with the previous frame's render:
+// two frames deep with the renders already in flight:
 //
-//   vis stream  : [vis n+1 K1-K4] -> event -> host: page table n+1, copy plan,
-//                 chunk table n+1                      (overlaps render n)
-//   copy stream : [upload_k n+1: pinned host -> staging]  (overlaps render n)
-//   main stream : [render n] ... | host waits render n, checks its counters |
-//                 [scatter staging -> pool] [chunks H2D] [render n+1] ...
+//   vis stream  (high priority) : [vis graph n+1] -> event -> host: page table
+//                  n+1, copy plan, chunk table n+1       (overlaps render n)
+//   copy stream : [upload_k n+1: pinned host -> staging] (overlaps render n)
+//   main stream : [render n] [scatter staging -> pool] [frame block + chunk
+//                  table H2D] [render graph n+1] [counters D2H] ...
+//
+// Every render kernel reads the per-frame values (camera, image pointer,
+// chunk and splat counts) from a device block (FrameDev), so the whole
+// render - preprocess, compaction, depth sort, tile duplication, tile sort,
+// ranges, blend, ~30 launches - is captured ONCE into a CUDA graph per
+// (resolution, instance capacity, timing) and replayed with one launch per
+// frame; the visibility pass likewise.  The host never waits for a render
+// except to recycle the pinned buffers of the frame two back.
 //
 // Exactness: the visibility pass only reads the immutable mesh, the page table
 // is updated strictly in frame order on the host, and pool slots are only
-// rewritten (scatter) after the previous render has finished, so results are
-// identical to the sequential reference order.  The host waits for render n
-// before enqueueing render n+1: if render n overflowed its tile-instance
-// buffer, the pool still holds frame n's pages and render n is redone with a
-// larger buffer (rare slow path; the session owns and regrows its scratch).
+// rewritten (scatter, main stream) after the previous render in stream order,
+// so results are identical to the sequential reference order.  A frame whose
+// tile instances overflow the buffer is still blended exactly (blend_k falls
+// back to the depth-sorted splat list); the host sees the overflow counter
+// when it recycles that frame's buffers and grows the buffer (re-capturing
+// the graph) for the frames after it.
 #include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -23,11 +34,24 @@
 #include "render.h"
 #include "vis.h"
 
+namespace {
+struct Graph {
+  cudaGraphExec_t exec = nullptr;
+  int w = 0, h = 0;
+  uint32_t m_cap = 0;
+  void reset() {
+    if (exec) cudaGraphExecDestroy(exec);
+    exec = nullptr;
+  }
+};
+}  // namespace
+
 struct vms_session {
   vms_session_desc d;
   vms_pagetable* pt = nullptr;
-  cudaStream_t vis_stream = nullptr, copy_stream = nullptr;
-  cudaEvent_t ev_vis = nullptr, ev_copy = nullptr, ev_render = nullptr, ev_staging = nullptr;
+  cudaStream_t vis_stream = nullptr, copy_stream = nullptr, cap_stream = nullptr;
+  cudaEvent_t ev_vis = nullptr, ev_copy = nullptr, ev_staging = nullptr;
+  cudaEvent_t ev_done[2] = {nullptr, nullptr};
   cudaEvent_t tev[10] = {};
   // pinned host memory
   uint32_t* req_pid = nullptr;
@@ -35,33 +59,33 @@ struct vms_session {
   uint8_t* req_direct = nullptr;
   uint8_t* req_level = nullptr;
   uint32_t* req_meta = nullptr;
+  vms::VisFrameDev* vis_fd_h = nullptr;
   vms_copy* copies[2] = {nullptr, nullptr};    // host -> staging (per frame parity)
   vms_copy* scatter_h[2] = {nullptr, nullptr};  // staging -> pool offsets
   vms_chunk* chunks_h[2] = {nullptr, nullptr};
-  uint32_t* counters = nullptr;  // n_kept, n_inst, overflow, n_need of the last render
+  vms::FrameDev* fd_h[2] = {nullptr, nullptr};
+  uint32_t* counters_h[2] = {nullptr, nullptr};  // n_kept, n_inst, overflow, n_need
+  bool pending[2] = {false, false};
+  int last_par = -1;
   // device memory owned by the session
   vms_copy* scatter_d = nullptr;
-  vms_chunk* chunks_d[2] = {nullptr, nullptr};
+  vms_chunk* chunks_d = nullptr;
   void* ws = nullptr;  // render workspace
   size_t ws_bytes = 0;
-  uint32_t m_cap = 0;
+  uint32_t m_cap = 0, m_want = 0;
+  uint32_t m_limit = 1u << 26;  // largest tile-instance buffer the session grows to
+  bool trace = false;
   int ws_w = 0, ws_h = 0;
   char* staging = nullptr;
   size_t staging_bytes = 0;
   int64_t max_chunks = 0;
   int parity = 0;
+  bool use_graphs = true;
+  Graph vis_graph, render_graph[2];  // render: [timing]
   std::vector<uint64_t> level_start;  // first row of each level block
   std::vector<uint32_t> plan_pid;
   std::vector<uint8_t> plan_level;
   std::vector<int32_t> plan_entry, plan_slot;
-  // last render (for overflow recovery)
-  bool have_last = false;
-  vms_camera last_cam{};
-  float* last_image = nullptr;
-  float* last_host_image = nullptr;
-  uint32_t last_chunks = 0, last_res = 0;
-  int last_parity = 0;
-  bool last_timing = false;
 };
 
 namespace vms {
@@ -69,21 +93,24 @@ namespace {
 
 void free_session(vms_session* s) {
   if (!s) return;
+  s->vis_graph.reset();
+  s->render_graph[0].reset();
+  s->render_graph[1].reset();
   if (s->pt) vms_pt_destroy(s->pt);
-  for (cudaStream_t x : {s->vis_stream, s->copy_stream})
+  for (cudaStream_t x : {s->vis_stream, s->copy_stream, s->cap_stream})
     if (x) cudaStreamDestroy(x);
-  for (cudaEvent_t e : {s->ev_vis, s->ev_copy, s->ev_render, s->ev_staging})
+  for (cudaEvent_t e : {s->ev_vis, s->ev_copy, s->ev_staging, s->ev_done[0], s->ev_done[1]})
     if (e) cudaEventDestroy(e);
   for (cudaEvent_t e : s->tev)
     if (e) cudaEventDestroy(e);
   for (void* p : {(void*)s->req_pid, (void*)s->req_enc, (void*)s->req_direct,
-                  (void*)s->req_level, (void*)s->req_meta, (void*)s->copies[0],
-                  (void*)s->copies[1], (void*)s->scatter_h[0], (void*)s->scatter_h[1],
-                  (void*)s->chunks_h[0], (void*)s->chunks_h[1],
-                  (void*)s->counters})
+                  (void*)s->req_level, (void*)s->req_meta, (void*)s->vis_fd_h,
+                  (void*)s->copies[0], (void*)s->copies[1], (void*)s->scatter_h[0],
+                  (void*)s->scatter_h[1], (void*)s->chunks_h[0], (void*)s->chunks_h[1],
+                  (void*)s->fd_h[0], (void*)s->fd_h[1], (void*)s->counters_h[0],
+                  (void*)s->counters_h[1]})
     if (p) cudaFreeHost(p);
-  for (void* p : {(void*)s->scatter_d, (void*)s->chunks_d[0], (void*)s->chunks_d[1], s->ws,
-                  (void*)s->staging})
+  for (void* p : {(void*)s->scatter_d, (void*)s->chunks_d, s->ws, (void*)s->staging})
     if (p) cudaFree(p);
   delete s;
 }
@@ -98,6 +125,7 @@ cudaError_t host_alloc(T** p, size_t n) {
 // Slow path only: first frame, resolution change, tile-instance overflow.
 int32_t ensure_ws(vms_session* s, int w, int h, uint32_t m_cap) {
   if (s->ws && s->ws_w == w && s->ws_h == h && s->m_cap >= m_cap) return VMS_OK;
+  const auto t0 = std::chrono::steady_clock::now();
   const uint32_t n_cap = s->d.capacity * s->d.page_size;
   const size_t bytes = render_ws_bytes(n_cap, m_cap, tile_count(w, h));
   if (s->ws) {
@@ -105,11 +133,17 @@ int32_t ensure_ws(vms_session* s, int w, int h, uint32_t m_cap) {
     VMS_CUDA(cudaFree(s->ws));
     s->ws = nullptr;
   }
+  s->render_graph[0].reset();
+  s->render_graph[1].reset();
   VMS_CUDA(cudaMalloc(&s->ws, bytes));
   s->ws_bytes = bytes;
   s->m_cap = m_cap;
   s->ws_w = w;
   s->ws_h = h;
+  if (s->trace)
+    fprintf(stderr, "[vmsplat] render workspace %dx%d, %u instances, %.1f MB: %.3f ms\n", w, h,
+            m_cap, bytes / 1e6,
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
   return VMS_OK;
 }
 
@@ -144,55 +178,76 @@ __global__ void scatter_k(const vms_copy* __restrict__ list, int64_t n,
   }
 }
 
-int32_t launch_render(vms_session* s, const vms_camera& cam, float* image, int par,
-                      uint32_t n_chunks, uint32_t n_res, bool timing, cudaStream_t st) {
-  int32_t rc = ensure_ws(s, cam.width, cam.height, s->m_cap ? s->m_cap : s->d.m_cap);
-  if (rc) return rc;
-  RenderWs w = render_carve(s->ws, s->d.capacity * s->d.page_size, s->m_cap,
-                            tile_count(cam.width, cam.height));
-  void* ev[4] = {nullptr, nullptr, nullptr, nullptr};
-  if (timing)
-    for (int i = 0; i < 4; ++i) ev[i] = s->tev[4 + i];
-  mark("begin", st);
-  rc = render_preprocess(s->d.pool, s->chunks_d[par], n_chunks, cam, w, st);
-  if (rc) return rc;
-  if (timing) VMS_CUDA(cudaEventRecord(s->tev[4], st));
-  rc = render_finish(cam, n_res, w, image, 0, s->d.exact, ev, st);
-  if (rc) return rc;
-  VMS_CUDA(cudaMemcpyAsync(s->counters, w.ctr, sizeof(uint32_t) * 4, cudaMemcpyDeviceToHost, st));
-  VMS_CUDA(cudaEventRecord(s->ev_render, st));
-  s->have_last = true;
-  s->last_cam = cam;
-  s->last_image = image;
-  s->last_chunks = n_chunks;
-  s->last_res = n_res;
-  s->last_parity = par;
+// A stream-ordered launch sequence, either replayed from a graph captured
+// once (key: resolution + instance capacity) or enqueued directly (profiling
+// mode: per-launch event marks are not capturable).
+template <typename F>
+int32_t run_captured(vms_session* s, Graph& g, int w, int h, uint32_t m_cap, F&& enqueue,
+                     cudaStream_t st) {
+  if (!s->use_graphs || g_profile) return enqueue(st, false);
+  if (g.exec && (g.w != w || g.h != h || g.m_cap != m_cap)) g.reset();
+  if (!g.exec) {
+    const auto t0 = std::chrono::steady_clock::now();
+    VMS_CUDA(cudaStreamBeginCapture(s->cap_stream, cudaStreamCaptureModeThreadLocal));
+    int32_t rc = enqueue(s->cap_stream, true);
+    cudaGraph_t graph = nullptr;
+    cudaError_t e = cudaStreamEndCapture(s->cap_stream, &graph);
+    if (rc) {
+      if (graph) cudaGraphDestroy(graph);
+      return rc;
+    }
+    if (e != cudaSuccess) return cuda_status(e, "graph capture");
+    e = cudaGraphInstantiate(&g.exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (e != cudaSuccess) {
+      g.exec = nullptr;
+      return cuda_status(e, "graph instantiate");
+    }
+    g.w = w;
+    g.h = h;
+    g.m_cap = m_cap;
+    if (s->trace)
+      fprintf(stderr, "[vmsplat] graph capture %dx%d m_cap %u: %.3f ms\n", w, h, m_cap,
+              std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0)
+                  .count());
+  }
+  VMS_CUDA(cudaGraphLaunch(g.exec, st));
   return VMS_OK;
 }
 
-// Wait for the last render; on tile-instance overflow grow and redo it (the
-// pool still holds that frame's pages).  Returns with the render complete.
-int32_t settle_last(vms_session* s, cudaStream_t st) {
-  if (!s->have_last) return VMS_OK;
-  VMS_CUDA(cudaEventSynchronize(s->ev_render));
-  int guard = 0;
-  while (s->counters[2]) {
-    if (++guard > 8) {
-      set_error("tile-instance buffer keeps overflowing (%u needed)", s->counters[3]);
-      return VMS_ERR_NOMEM;
-    }
-    const uint32_t need = s->counters[3];
-    int32_t rc = ensure_ws(s, s->last_cam.width, s->last_cam.height, need + need / 4 + (1u << 16));
+int32_t launch_render(vms_session* s, int w, int h, bool timing, cudaStream_t st) {
+  RenderWs ws = render_carve(s->ws, s->d.capacity * s->d.page_size, s->m_cap, tile_count(w, h));
+  const uint32_t max_chunks = (uint32_t)s->max_chunks;
+  auto enqueue = [&](cudaStream_t q, bool captured) -> int32_t {
+    void* ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    if (timing)
+      for (int i = 0; i < 4; ++i) ev[i] = s->tev[4 + i];
+    mark("begin", q);
+    int32_t rc = render_preprocess(s->d.pool, s->chunks_d, max_chunks, ws, q);
     if (rc) return rc;
-    rc = launch_render(s, s->last_cam, s->last_image, s->last_parity, s->last_chunks, s->last_res,
-                       false, st);
-    if (rc) return rc;
-    if (s->last_host_image)
-      VMS_CUDA(cudaMemcpyAsync(s->last_host_image, s->last_image,
-                               sizeof(float) * 3 * (size_t)s->last_cam.width * s->last_cam.height,
-                               cudaMemcpyDeviceToHost, st));
-    VMS_CUDA(cudaEventSynchronize(s->ev_render));
-    VMS_CUDA(cudaStreamSynchronize(st));
+    if (timing)
+      VMS_CUDA(cudaEventRecordWithFlags(s->tev[4], q,
+                                        captured ? cudaEventRecordExternal : cudaEventRecordDefault));
+    return render_finish(w, h, ws, 0, s->d.exact, ev, captured, q);
+  };
+  return run_captured(s, s->render_graph[timing ? 1 : 0], w, h, s->m_cap, enqueue, st);
+}
+
+// The frame two back used this parity's pinned buffers: wait for its render,
+// and grow the tile-instance buffer if it overflowed (it was still blended
+// exactly, through the depth-sorted list).
+int32_t recycle(vms_session* s, int par) {
+  if (!s->pending[par]) return VMS_OK;
+  VMS_CUDA(cudaEventSynchronize(s->ev_done[par]));
+  s->pending[par] = false;
+  const uint32_t* c = s->counters_h[par];
+  if (c[2]) {
+    // frames past the limit (camera inside dense geometry: tens of millions
+    // of instances, blends that saturate in a few splats) keep the spill path
+    const uint32_t need = c[3];
+    uint64_t want = (uint64_t)need + need / 4 + (1u << 16);
+    if (want > s->m_limit) want = s->m_limit;
+    if (want > s->m_want) s->m_want = (uint32_t)want;
   }
   return VMS_OK;
 }
@@ -232,11 +287,25 @@ vms_session* vms_session_create(const vms_session_desc* desc) {
   const uint32_t P = desc->page_count;
   s->max_chunks = (int64_t)desc->capacity *
                   (ceil_div<uint32_t>(desc->page_size, kChunkRecords) + (1u << (desc->lod_levels - 1)));
-  s->m_cap = desc->m_cap ? desc->m_cap : 16u * desc->capacity * desc->page_size;
+  s->m_cap = 0;
+  s->m_want = desc->m_cap ? desc->m_cap : 16u * desc->capacity * desc->page_size;
+  const char* g = std::getenv("VMSPLAT_GRAPHS");
+  s->use_graphs = !(g && g[0] == '0');
+  const char* tr = std::getenv("VMSPLAT_TRACE");
+  s->trace = tr && tr[0] == '1';
+  if (const char* ml = std::getenv("VMSPLAT_MAX_INSTANCES")) {
+    const long long v = std::atoll(ml);
+    if (v > 0) s->m_limit = (uint32_t)(v < 0xFFFFFFF0ll ? v : 0xFFFFFFF0ll);
+  }
+  if (s->m_want > s->m_limit) s->m_limit = s->m_want;
+  int lo = 0, hi = 0;
+  cudaDeviceGetStreamPriorityRange(&lo, &hi);
   bool ok = s->pt != nullptr;
-  ok = ok && cudaStreamCreateWithFlags(&s->vis_stream, cudaStreamNonBlocking) == cudaSuccess;
+  // visibility gates the host's page-table work: let it overtake render kernels
+  ok = ok && cudaStreamCreateWithPriority(&s->vis_stream, cudaStreamNonBlocking, hi) == cudaSuccess;
   ok = ok && cudaStreamCreateWithFlags(&s->copy_stream, cudaStreamNonBlocking) == cudaSuccess;
-  for (cudaEvent_t* e : {&s->ev_vis, &s->ev_copy, &s->ev_render, &s->ev_staging})
+  ok = ok && cudaStreamCreateWithFlags(&s->cap_stream, cudaStreamNonBlocking) == cudaSuccess;
+  for (cudaEvent_t* e : {&s->ev_vis, &s->ev_copy, &s->ev_staging, &s->ev_done[0], &s->ev_done[1]})
     ok = ok && cudaEventCreateWithFlags(e, cudaEventDisableTiming) == cudaSuccess;
   for (cudaEvent_t& e : s->tev) ok = ok && cudaEventCreate(&e) == cudaSuccess;
   ok = ok && host_alloc(&s->req_pid, P + 1) == cudaSuccess;
@@ -244,22 +313,22 @@ vms_session* vms_session_create(const vms_session_desc* desc) {
   ok = ok && host_alloc(&s->req_direct, P + 1) == cudaSuccess;
   ok = ok && host_alloc(&s->req_level, P + 1) == cudaSuccess;
   ok = ok && host_alloc(&s->req_meta, 4) == cudaSuccess;
+  ok = ok && host_alloc(&s->vis_fd_h, 1) == cudaSuccess;
   for (int k = 0; k < 2; ++k) {
     ok = ok && host_alloc(&s->copies[k], P + 1) == cudaSuccess;
     ok = ok && host_alloc(&s->scatter_h[k], P + 1) == cudaSuccess;
+    ok = ok && host_alloc(&s->chunks_h[k], (size_t)s->max_chunks) == cudaSuccess;
+    ok = ok && host_alloc(&s->fd_h[k], 1) == cudaSuccess;
+    ok = ok && host_alloc(&s->counters_h[k], 4) == cudaSuccess;
   }
-  ok = ok && host_alloc(&s->chunks_h[0], (size_t)s->max_chunks) == cudaSuccess;
-  ok = ok && host_alloc(&s->chunks_h[1], (size_t)s->max_chunks) == cudaSuccess;
-  ok = ok && host_alloc(&s->counters, 4) == cudaSuccess;
   ok = ok && cudaMalloc(&s->scatter_d, sizeof(vms_copy) * (P + 1)) == cudaSuccess;
-  ok = ok && cudaMalloc(&s->chunks_d[0], sizeof(vms_chunk) * s->max_chunks) == cudaSuccess;
-  ok = ok && cudaMalloc(&s->chunks_d[1], sizeof(vms_chunk) * s->max_chunks) == cudaSuccess;
+  ok = ok && cudaMalloc(&s->chunks_d, sizeof(vms_chunk) * s->max_chunks) == cudaSuccess;
   if (!ok) {
     set_error("session_create: %s", cudaGetErrorString(cudaGetLastError()));
     free_session(s);
     return nullptr;
   }
-  std::memset(s->counters, 0, sizeof(uint32_t) * 4);
+  for (int k = 0; k < 2; ++k) std::memset(s->counters_h[k], 0, sizeof(uint32_t) * 4);
   s->level_start.assign(desc->lod_levels + 1, 0);
   for (uint32_t k = 0; k < desc->lod_levels; ++k)
     s->level_start[k + 1] =
@@ -288,13 +357,17 @@ int32_t vms_session_set_render_ws(vms_session* s, void* ws, uint64_t bytes, uint
   // the session owns its scratch; this only raises the instance capacity
   (void)ws;
   (void)bytes;
+  (void)width;
+  (void)height;
   if (!s) return VMS_ERR_INVALID;
-  return ensure_ws(s, width, height, m_cap);
+  if (m_cap > s->m_want) s->m_want = m_cap;
+  return VMS_OK;
 }
 
 int32_t vms_session_frame(vms_session* s, const vms_frame_args* a, vms_frame_stats* out,
                           void* stream) {
-  if (!s || !a || !out || !a->image) {
+  if (!s || !a || !out || !a->image || a->cam.width < 1 || a->cam.height < 1 ||
+      a->vis_cam.width < 1 || a->vis_cam.height < 1 || a->lod.count < 0 || a->lod.count > 8) {
     set_error("session_frame: invalid arguments");
     return VMS_ERR_INVALID;
   }
@@ -303,9 +376,16 @@ int32_t vms_session_frame(vms_session* s, const vms_frame_args* a, vms_frame_sta
   const bool timing = a->timing != 0;
   const uint32_t P = s->d.page_count;
   const int par = s->parity;
+  int32_t rc = recycle(s, par);
+  if (rc) return rc;
   s->parity ^= 1;
-  // [1]+[2] visibility on its own stream (overlaps the previous render)
+  // [1]+[2] visibility on its own high-priority stream (overlaps the renders
+  // in flight); the compacted required list lands in mapped pinned memory
   if (timing) VMS_CUDA(cudaEventRecord(s->tev[0], s->vis_stream));
+  s->vis_fd_h->cam = a->vis_cam;
+  s->vis_fd_h->lod = a->lod;
+  VMS_CUDA(cudaMemcpyAsync(vis_frame_dev(s->d.vis_ws, s->d.n_faces, P), s->vis_fd_h,
+                           sizeof(VisFrameDev), cudaMemcpyHostToDevice, s->vis_stream));
   vms_vis_args v{};
   v.cam = a->vis_cam;
   v.verts = s->d.verts;
@@ -322,7 +402,8 @@ int32_t vms_session_frame(vms_session* s, const vms_frame_args* a, vms_frame_sta
   v.out.level = s->req_level;
   v.out.meta = s->req_meta;
   v.workspace = s->d.vis_ws;
-  int32_t rc = vis_frame(v, s->vis_stream);
+  rc = run_captured(s, s->vis_graph, v.cam.width, v.cam.height, 0,
+                    [&](cudaStream_t q, bool) { return vis_launch(v, q); }, s->vis_stream);
   if (rc) return rc;
   if (timing) VMS_CUDA(cudaEventRecord(s->tev[1], s->vis_stream));
   VMS_CUDA(cudaEventRecord(s->ev_vis, s->vis_stream));
@@ -362,7 +443,7 @@ int32_t vms_session_frame(vms_session* s, const vms_frame_args* a, vms_frame_sta
   }
   out->host_update_s =
       std::chrono::duration<double>(std::chrono::steady_clock::now() - h0).count();
-  // uploads into staging on the copy stream (overlap the previous render)
+  // uploads into staging on the copy stream (overlap the renders in flight)
   if (n_plan) {
     rc = ensure_staging(s, bytes);
     if (rc) return rc;
@@ -372,13 +453,14 @@ int32_t vms_session_frame(vms_session* s, const vms_frame_args* a, vms_frame_sta
                           s->copy_stream);
     if (rc) return rc;
     if (timing) VMS_CUDA(cudaEventRecord(s->tev[3], s->copy_stream));
-    VMS_CUDA(cudaEventRecord(s->ev_copy, s->copy_stream));
     VMS_CUDA(cudaMemcpyAsync(s->scatter_d, s->scatter_h[par], sizeof(vms_copy) * n_plan,
                              cudaMemcpyHostToDevice, s->copy_stream));
     VMS_CUDA(cudaEventRecord(s->ev_copy, s->copy_stream));
   }
-  // the previous render must be final before pool slots are rewritten
-  rc = settle_last(s, st);
+  // [4]-[6] on the main stream: pool slots are rewritten only after the
+  // previous render (stream order), then the frame block, chunk table, graph
+  const int W = a->cam.width, H = a->cam.height;
+  rc = ensure_ws(s, W, H, s->m_cap > s->m_want ? s->m_cap : s->m_want);
   if (rc) return rc;
   if (timing) VMS_CUDA(cudaEventRecord(s->tev[8], st));
   if (n_plan) {
@@ -389,18 +471,26 @@ int32_t vms_session_frame(vms_session* s, const vms_frame_args* a, vms_frame_sta
     mark("scatter", st);
     VMS_CUDA(cudaEventRecord(s->ev_staging, st));
   }
+  RenderWs ws = render_carve(s->ws, s->d.capacity * s->d.page_size, s->m_cap, tile_count(W, H));
+  FrameDev* f = s->fd_h[par];
+  f->cam = a->cam;
+  f->image = a->image;
+  f->n_chunks = (uint32_t)n_chunks;
+  f->n_splats = (uint32_t)n_res;
+  VMS_CUDA(cudaMemcpyAsync(ws.fd, f, sizeof(FrameDev), cudaMemcpyHostToDevice, st));
   if (n_chunks)
-    VMS_CUDA(cudaMemcpyAsync(s->chunks_d[par], s->chunks_h[par], sizeof(vms_chunk) * n_chunks,
+    VMS_CUDA(cudaMemcpyAsync(s->chunks_d, s->chunks_h[par], sizeof(vms_chunk) * n_chunks,
                              cudaMemcpyHostToDevice, st));
-  // [4]-[6] render every resident record
-  rc = launch_render(s, a->cam, a->image, par, (uint32_t)n_chunks, (uint32_t)n_res, timing, st);
+  rc = launch_render(s, W, H, timing, st);
   if (rc) return rc;
-  s->last_host_image = a->host_image;
-  s->last_timing = timing;
+  VMS_CUDA(cudaMemcpyAsync(s->counters_h[par], ws.ctr, sizeof(uint32_t) * 4,
+                           cudaMemcpyDeviceToHost, st));
+  VMS_CUDA(cudaEventRecord(s->ev_done[par], st));
+  s->pending[par] = true;
+  s->last_par = par;
   if (timing) VMS_CUDA(cudaEventRecord(s->tev[9], st));
   if (a->host_image)
-    VMS_CUDA(cudaMemcpyAsync(a->host_image, a->image,
-                             sizeof(float) * 3 * (size_t)a->cam.width * a->cam.height,
+    VMS_CUDA(cudaMemcpyAsync(a->host_image, a->image, sizeof(float) * 3 * (size_t)W * H,
                              cudaMemcpyDeviceToHost, st));
   // stats (runtime.py:471-481)
   out->required = n_req;
@@ -415,12 +505,14 @@ int32_t vms_session_frame(vms_session* s, const vms_frame_args* a, vms_frame_sta
   rc = vms_pt_resident_counts(s->pt, out->resident_per_level, (int32_t)s->d.lod_levels);
   if (rc) return rc;
   if (timing || a->host_image) {
-    rc = settle_last(s, st);
-    if (rc) return rc;
     VMS_CUDA(cudaStreamSynchronize(st));
-    out->n_kept = s->counters[0];
-    out->n_inst = s->counters[1];
-    out->n_need = s->counters[3];
+    const uint32_t* c = s->counters_h[par];
+    out->n_kept = c[0];
+    out->n_inst = c[1];
+    out->overflow = c[2];
+    out->n_need = c[3];
+    rc = recycle(s, par);
+    if (rc) return rc;
     if (timing) {
       out->ms_vis = ms_between(s->tev[0], s->tev[1]);
       out->ms_copy = n_plan ? ms_between(s->tev[2], s->tev[3]) : 0.f;
@@ -434,36 +526,18 @@ int32_t vms_session_frame(vms_session* s, const vms_frame_args* a, vms_frame_sta
   return VMS_OK;
 }
 
-int32_t vms_session_rerender(vms_session* s, float* host_image, void* stream) {
-  if (!s || !s->have_last) {
-    set_error("session_rerender: nothing to re-render");
-    return VMS_ERR_INVALID;
-  }
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  int32_t rc = settle_last(s, st);
-  if (rc) return rc;
-  rc = launch_render(s, s->last_cam, s->last_image, s->last_parity, s->last_chunks, s->last_res,
-                     false, st);
-  if (rc) return rc;
-  if (host_image)
-    VMS_CUDA(cudaMemcpyAsync(host_image, s->last_image,
-                             sizeof(float) * 3 * (size_t)s->last_cam.width * s->last_cam.height,
-                             cudaMemcpyDeviceToHost, st));
-  s->last_host_image = host_image;
-  rc = settle_last(s, st);
-  if (rc) return rc;
-  VMS_CUDA(cudaStreamSynchronize(st));
-  return VMS_OK;
-}
-
 int32_t vms_session_counters(vms_session* s, uint32_t* out4, void* stream) {
   if (!s || !out4) return VMS_ERR_INVALID;
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  int32_t rc = settle_last(s, st);
-  if (rc) return rc;
-  VMS_CUDA(cudaStreamSynchronize(st));
-  std::memcpy(out4, s->counters, sizeof(uint32_t) * 4);
-  return VMS_OK;
+  (void)stream;
+  std::memset(out4, 0, sizeof(uint32_t) * 4);
+  if (s->last_par < 0) return VMS_OK;
+  const int par = s->last_par;
+  const bool was_pending = s->pending[par];
+  if (was_pending) {
+    VMS_CUDA(cudaEventSynchronize(s->ev_done[par]));
+  }
+  std::memcpy(out4, s->counters_h[par], sizeof(uint32_t) * 4);
+  return recycle(s, par);
 }
 
 }  // extern "C"

@@ -82,9 +82,12 @@ __device__ __forceinline__ void face_view(const VisCamera& c, const double* vert
   for (int j = 0; j < 3; ++j) v[j] = to_view(c, verts + 3 * (int64_t)faces[3 * f + j]);
 }
 
-__global__ void vis_count_k(VisCamera cam, const double* __restrict__ verts,
+__global__ void vis_count_k(const VisFrameDev* __restrict__ fd, const double* __restrict__ verts,
                             const int32_t* __restrict__ faces, uint32_t nf,
                             uint32_t* __restrict__ counts) {
+  __shared__ VisCamera cam;
+  if (threadIdx.x == 0) cam = fd->cam;
+  __syncthreads();
   uint32_t f = blockIdx.x * blockDim.x + threadIdx.x;
   if (f >= nf) return;
   View3 v[3], poly[4];
@@ -140,10 +143,13 @@ __device__ __forceinline__ void to_pixels(const VisCamera& c, const View3& v, do
   *iz = ddiv(1.0, v.z);
 }
 
-__global__ void vis_emit_k(VisCamera cam, const double* __restrict__ verts,
+__global__ void vis_emit_k(const VisFrameDev* __restrict__ fd, const double* __restrict__ verts,
                            const int32_t* __restrict__ faces,
                            const uint32_t* __restrict__ face_page, uint32_t nf,
                            const uint32_t* __restrict__ offsets, VisTri* __restrict__ tris) {
+  __shared__ VisCamera cam;
+  if (threadIdx.x == 0) cam = fd->cam;
+  __syncthreads();
   uint32_t f = blockIdx.x * blockDim.x + threadIdx.x;
   if (f >= nf) return;
   View3 v[3], poly[4];
@@ -307,9 +313,10 @@ __global__ void vis_flags_k(const uint32_t* __restrict__ depth, uint32_t page_co
 __global__ void vis_required_k(const uint32_t* __restrict__ depth,
                                const uint8_t* __restrict__ direct,
                                const uint32_t* __restrict__ pos, uint32_t page_count,
-                               VisLod lod, RequiredOut out) {
+                               const VisFrameDev* __restrict__ fd, RequiredOut out) {
   uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p == 0 || p > page_count) return;
+  const VisLod& lod = fd->lod;
   const uint32_t e = depth[p];
   if (!e) return;
   const uint32_t o = pos[p];
@@ -333,6 +340,7 @@ size_t vis_ws_bytes(uint32_t n_faces, uint32_t page_count) {
   b += sizeof(uint32_t) * (page_count + 1) * 3;      // base, depth, flags/pos
   b += sizeof(uint8_t) * (page_count + 1);           // direct
   b += scan_ws_bytes(n_faces > page_count + 1 ? n_faces : page_count + 1) + 1024;
+  b += sizeof(VisFrameDev);
   return b + 8 * 256;
 }
 
@@ -342,6 +350,7 @@ struct VisWs {
   VisTri* tris;
   uint8_t* direct;
   void* scan;
+  VisFrameDev* fd;
 };
 
 template <typename T>
@@ -366,11 +375,25 @@ VisWs carve_ws(void* ws, uint32_t nf, uint32_t P) {
   w.pos = carve<uint32_t>(p, P + 1);
   w.direct = carve<uint8_t>(p, P + 1);
   w.scan = carve<char>(p, scan_ws_bytes(nf > P + 1 ? nf : P + 1));
+  w.fd = carve<VisFrameDev>(p, 1);
   return w;
 }
 }  // namespace
 
+VisFrameDev* vis_frame_dev(void* ws, uint32_t n_faces, uint32_t page_count) {
+  return carve_ws(ws, n_faces, page_count).fd;
+}
+
 int32_t vis_frame(const VisArgs& a, cudaStream_t s) {
+  VisFrameDev f;
+  f.cam = a.cam;
+  f.lod = a.lod;
+  VMS_CUDA(cudaMemcpyAsync(vis_frame_dev(a.workspace, a.n_faces, a.page_count), &f,
+                           sizeof(VisFrameDev), cudaMemcpyHostToDevice, s));
+  return vis_launch(a, s);
+}
+
+int32_t vis_launch(const VisArgs& a, cudaStream_t s) {
   if (a.n_faces && (!a.verts || !a.faces || !a.face_page)) {
     set_error("vis_frame: null mesh pointer");
     return VMS_ERR_INVALID;
@@ -382,14 +405,14 @@ int32_t vis_frame(const VisArgs& a, cudaStream_t s) {
   VMS_CUDA(cudaMemsetAsync(w.base, 0, sizeof(uint32_t) * (a.page_count + 1), s));
   VMS_CUDA(cudaMemsetAsync(w.direct, 0, a.page_count + 1, s));
   if (a.n_faces) {
-    vis_count_k<<<ceil_div<uint32_t>(a.n_faces, T), T, 0, s>>>(a.cam, a.verts, a.faces,
+    vis_count_k<<<ceil_div<uint32_t>(a.n_faces, T), T, 0, s>>>(w.fd, a.verts, a.faces,
                                                                 a.n_faces, w.counts);
     mark("vis_count", s);
     int32_t st = scan_exclusive_u32(w.counts, w.offsets, nullptr, a.n_faces, a.n_faces, w.n_tris,
                                     w.scan, s);
     if (st) return st;
     vis_emit_k<<<ceil_div<uint32_t>(a.n_faces, T), T, 0, s>>>(
-        a.cam, a.verts, a.faces, a.face_page, a.n_faces, w.offsets, w.tris);
+        w.fd, a.verts, a.faces, a.face_page, a.n_faces, w.offsets, w.tris);
     mark("vis_emit", s);
   }
   dim3 grid(ceil_div(a.cam.width, kVisTile), ceil_div(a.cam.height, kVisTile));
@@ -411,7 +434,7 @@ int32_t vis_frame(const VisArgs& a, cudaStream_t s) {
                                   w.n_req, w.scan, s);
   if (st) return st;
   vis_required_k<<<ceil_div<uint32_t>(a.page_count + 1, T), T, 0, s>>>(
-      w.depth, w.direct, w.pos, a.page_count, a.lod, a.out);
+      w.depth, w.direct, w.pos, a.page_count, w.fd, a.out);
   mark("vis_required", s);
   if (a.out.meta) {
     VMS_CUDA(cudaMemcpyAsync(a.out.meta, w.n_tris, sizeof(uint32_t) * 4,

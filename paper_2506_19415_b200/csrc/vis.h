@@ -21,8 +21,20 @@ using VisLod = vms_lod;
 using RequiredOut = vms_required_out;
 using VisArgs = vms_vis_args;
 
+// Per-frame values the visibility kernels read from device memory (so the
+// launch sequence can be captured into a CUDA graph once per resolution).
+struct VisFrameDev {
+  VisCamera cam;
+  VisLod lod;
+};
+
 size_t vis_ws_bytes(uint32_t n_faces, uint32_t page_count);
+VisFrameDev* vis_frame_dev(void* ws, uint32_t n_faces, uint32_t page_count);
+// Upload a.cam / a.lod into the workspace, then vis_launch.
 int32_t vis_frame(const VisArgs& a, cudaStream_t s);
+// The kernel sequence only (camera and LOD from the workspace block; a.cam's
+// width/height fix the raster grid).
+int32_t vis_launch(const VisArgs& a, cudaStream_t s);
 int32_t reduce_images(const uint32_t* ids, const double* depth, uint64_t n_px,
                       uint32_t page_count, const uint32_t* link_off, const uint32_t* link_tgt,
                       uint32_t* depth_out, uint8_t* direct_out, uint32_t* err, void* ws,

@@ -195,28 +195,27 @@ class FlatRenderer:
         cam = camera.struct(dot_mode)
         lib = _lib.load()
         m_cap = max(self.m_cap, 16 * max(n, 1024))
-        while True:
-            nbytes = lib.vms_render_workspace_bytes(max(n, 1), m_cap, camera.width,
-                                                    camera.height)
-            ws = _device.workspace("flat_render", nbytes)
-            ctr = t.zeros(4, dtype=t.int32).pin_memory()
-            a = _lib.RenderArgs()
-            a.cam = cam
-            a.pool = rec.data_ptr()
-            a.chunks = dchunks.data_ptr()
-            a.n_chunks = len(starts)
-            a.n_splats = n
-            a.n_cap = max(n, 1)
-            a.m_cap = m_cap
-            a.image = image.data_ptr()
-            a.accumulate = 0
-            a.exact = int(exact)
-            a.counters_out = ctr.data_ptr()
-            a.workspace = ws.data_ptr()
-            _lib.check(lib.vms_render(ctypes.byref(a), _device.sptr()), "render")
-            t.cuda.current_stream().synchronize()
-            if int(ctr[2]) == 0:
-                break
+        nbytes = lib.vms_render_workspace_bytes(max(n, 1), m_cap, camera.width, camera.height)
+        ws = _device.workspace("flat_render", nbytes)
+        ctr = t.zeros(4, dtype=t.int32).pin_memory()
+        a = _lib.RenderArgs()
+        a.cam = cam
+        a.pool = rec.data_ptr()
+        a.chunks = dchunks.data_ptr()
+        a.n_chunks = len(starts)
+        a.n_splats = n
+        a.n_cap = max(n, 1)
+        a.m_cap = m_cap
+        a.image = image.data_ptr()
+        a.accumulate = 0
+        a.exact = int(exact)
+        a.counters_out = ctr.data_ptr()
+        a.workspace = ws.data_ptr()
+        _lib.check(lib.vms_render(ctypes.byref(a), _device.sptr()), "render")
+        t.cuda.current_stream().synchronize()
+        if int(ctr[2]):
+            # the frame was blended from the depth-sorted list (correct, slow);
+            # size the tile-instance buffer for the next call
             m_cap = int(ctr[3]) + int(ctr[3]) // 4 + 1024
         self.m_cap = m_cap
         return image

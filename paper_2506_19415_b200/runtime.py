@@ -531,6 +531,8 @@ class VmSession:
             "time_frame_wall": h1 - h0,
             "n_kept": int(st.n_kept),
             "n_instances": int(st.n_inst),
+            "n_need": int(st.n_need),
+            "overflow": int(st.overflow),
             "n_resident_records": int(st.n_res),
             "n_chunks": int(st.n_chunks),
             "n_tris": int(st.n_tris),
