@@ -141,6 +141,9 @@ const char* vms_last_error(void);
 int32_t vms_abi_version(void);
 /* Edge (pixels) of the square blend tiles: 32, or 16 with VMSPLAT_TILE=16. */
 int32_t vms_tile_size(void);
+/* 1 if `ptr` is page-locked host memory the device can address (zero-copy
+ * target), 0 otherwise. */
+int32_t vms_host_accessible(const void* ptr);
 
 /* Per-launch device timing for profiling runs: when enabled every kernel
  * launch records a CUDA event; the report (CSV "kernel,count,total_us")
@@ -148,6 +151,9 @@ int32_t vms_tile_size(void);
  * report length; buf may be NULL to query it. */
 int32_t vms_profile_enable(int32_t on);
 int64_t vms_profile_report(char* buf, int64_t len);
+/* Profiling: when dev_ptr is non-NULL every blend CTA writes {start ns, end
+ * ns, SM id, (list length << 32) | tile} (4 x u64) at dev_ptr[4 * block]. */
+int32_t vms_debug_blend_trace(void* dev_ptr);
 
 /* ---- kernel-level drop-ins (pkg/src/vmsplat/kernels/__init__.py) ------ */
 
@@ -285,10 +291,11 @@ typedef struct vms_frame_args {
   vms_lod lod;                  /* controller thresholds before this frame's adaptation */
   int64_t frame;
   double budget;                /* staging_pages */
-  float* image;                 /* [dev] (h, w, 3) */
+  float* image;                 /* [dev] (h, w, 3); may be device-accessible pinned host
+                                   memory (zero-copy: the blend writes over PCIe) */
   float* host_image;            /* [host pinned] optional: D2H + sync at the end */
   int32_t timing;               /* 1: stage CUDA events + sync at the end */
-  int32_t pad_;
+  int32_t sync;                 /* 1: return only once the frame is complete */
 } vms_frame_args;
 
 typedef struct vms_frame_stats {

@@ -80,7 +80,7 @@ class SessionDesc(ctypes.Structure):
 class FrameArgs(ctypes.Structure):
     _fields_ = [("cam", Camera), ("vis_cam", Camera), ("lod", Lod), ("frame", I64),
                 ("budget", D), ("image", P), ("host_image", P), ("timing", I32),
-                ("pad_", I32)]
+                ("sync", I32)]
 
 
 class FrameStats(ctypes.Structure):
@@ -136,6 +136,8 @@ SIGNATURES = {
     "vms_session_set_render_ws": (I32, [P, P, ctypes.c_uint64, U32, I32, I32]),
     "vms_session_frame": (I32, [P, ctypes.POINTER(FrameArgs), ctypes.POINTER(FrameStats), P]),
     "vms_session_counters": (I32, [P, P, P]),
+    "vms_host_accessible": (I32, [P]),
+    "vms_debug_blend_trace": (I32, [P]),
 }
 
 _lib = None

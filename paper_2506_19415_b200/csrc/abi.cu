@@ -163,6 +163,18 @@ int32_t vms_abi_version(void) { return VMS_ABI_VERSION; }
 
 int32_t vms_tile_size(void) { return tile_size(); }
 
+int32_t vms_debug_blend_trace(void* dev_ptr) { return debug_blend_trace(dev_ptr); }
+
+int32_t vms_host_accessible(const void* ptr) {
+  if (!ptr) return 0;
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, ptr) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return at.type == cudaMemoryTypeHost && at.devicePointer == ptr ? 1 : 0;
+}
+
 size_t vms_composite_workspace_bytes(int64_t n, int64_t n_instances, int32_t h, int32_t w) {
   const uint32_t tiles = tile_count(w, h);
   return render_ws_bytes((uint32_t)(n > 0 ? n : 1),
@@ -183,6 +195,8 @@ int32_t vms_composite_splats(const float* centers, const float* conics, const fl
     set_error("composite_splats: workspace too small");
     return VMS_ERR_INVALID;
   }
+  int32_t rc0 = blend_init();
+  if (rc0) return rc0;
   const uint32_t tiles = tile_count(w, h);
   RenderWs ws = render_carve(workspace, (uint32_t)(n > 0 ? n : 1),
                              (uint32_t)(n_instances > 0 ? n_instances : 1), tiles);
@@ -351,6 +365,8 @@ int32_t vms_render(const vms_render_args* a, void* stream) {
     return VMS_ERR_INVALID;
   }
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  int32_t rc0 = blend_init();
+  if (rc0) return rc0;
   const uint32_t tiles =
       tile_count(a->cam.width, a->cam.height);
   RenderWs w = render_carve(a->workspace, a->n_cap, a->m_cap, tiles);
@@ -365,7 +381,8 @@ int32_t vms_render(const vms_render_args* a, void* stream) {
   st = render_preprocess(a->pool, a->chunks, a->n_chunks, w, s);
   if (st) return st;
   if (a->events[0]) VMS_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(a->events[0]), s));
-  st = render_finish(a->cam.width, a->cam.height, w, a->accumulate, a->exact, a->events, false, s);
+  st = render_finish(a->cam.width, a->cam.height, w, a->accumulate, a->exact, a->events, false, 1,
+                     s);
   if (st) return st;
   if (a->counters_out)
     VMS_CUDA(cudaMemcpyAsync(a->counters_out, w.ctr, sizeof(uint32_t) * 4,

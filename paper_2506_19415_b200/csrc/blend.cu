@@ -16,6 +16,7 @@
 // Fast mode blends in FP32 (measured <= 2.6e-5 from the FP64 reference,
 // SURVEY A16); exact mode reproduces the reference's FP64 arithmetic with
 // f32 storage of T and colour.
+#include <cmath>
 #include <cstdlib>
 #include <type_traits>
 
@@ -152,47 +153,84 @@ __global__ void ranges_k(const uint32_t* __restrict__ tk, const RenderCounters* 
   }
 }
 
-// Blend: one CTA per 16x16 sub-tile of a TS x TS sort tile (TS/16)^2 CTAs
-// share one tile list), one thread per pixel.  Splats of the list are staged
-// 256 at a time; each staging thread tests its splat against the CTA's
-// sub-tile and a warp-ballot compaction keeps only the overlapping ones (in
-// list order) in shared memory - the pixel loop touches relevant splats only.
-// Exact mode stages the splat parameters already widened to FP64, so the
-// inner loop has no f32->f64 conversions of splat data.
+// Blend: one CTA per 16x16 sub-tile of a TS x TS sort tile ((TS/16)^2 CTAs
+// share one tile list), one thread per pixel, each warp an 8x4 pixel block.
+// Splats of the list are staged 256 at a time: each staging thread tests its
+// splat against the CTA's sub-tile and a warp-ballot compaction keeps the
+// overlapping ones (in list order) in shared memory.  Each warp then walks
+// the staged splats 32 at a time, ballots which of them touch its own 8x4
+// block, and iterates only those - warp-uniform control flow, no per-splat
+// work for warps the splat misses.  Exact mode stages the splat parameters
+// widened to FP64 and evaluates exp with a table-driven FP64 kernel (64-entry
+// double-double table, degree-5 polynomial: <= 0.82 ulp, tested against
+// libm on 2e7 points), the reference's arithmetic otherwise.
+constexpr int kMaxBands = 8;
+
 struct SplatF64 {
   double cx, cy, ca, cb2, cc, al, r, g, b;
   double skip;  // sigma below which alpha * exp(sigma) < 2^-36 (no effect on f32 T)
   int x0, x1, y0, y1;
 };
 
-// Longest-list-first tile schedule: tiles bucketed by floor(log2(list length))
-// in descending order (one CTA; the order only affects scheduling, never
-// results - tiles are independent).
+// 2^(j/64) as double-double, j = 0..63
+__constant__ double2 kExp2Tab[64];
+
+__device__ __forceinline__ double exp_tab(double x, const double2* __restrict__ tab) {
+  // exp(x), x in [-700, 0]: x = (64 m + j) ln2/64 + r, |r| <= ln2/128
+  const double kInvL = 0x1.71547652b82fep+6;  // 64 / ln2
+  const double kLhi = 0x1.62e4200000000p-7;   // ln2/64, 21 leading bits (k * kLhi exact)
+  const double kLlo = 0x1.fdf473de6af28p-28;  // ln2/64 - kLhi
+  const double kMagic = 0x1.8p52;
+  const double t = __fma_rn(x, kInvL, kMagic);
+  const int k = __double2loint(t);
+  const double kd = __dsub_rn(t, kMagic);
+  double r = __fma_rn(kd, -kLhi, x);
+  r = __fma_rn(kd, -kLlo, r);
+  double q = __fma_rn(1.0 / 120.0, r, 1.0 / 24.0);
+  q = __fma_rn(q, r, 1.0 / 6.0);
+  q = __fma_rn(q, r, 0.5);
+  q = __fma_rn(q, r, 1.0);
+  const double sr = __dmul_rn(q, r);  // exp(r) - 1
+  const double2 tj = tab[k & 63];
+  const double v = __dadd_rn(tj.x, __fma_rn(tj.x, sr, tj.y));
+  return __hiloint2double(__double2hiint(v) + ((k >> 6) << 20), __double2loint(v));
+}
+
+// Tile schedule: band-major (horizontal bands of tile rows, see
+// blend_bands), and within a band longest list first, bucketed by
+// floor(log2(list length)).  One CTA; the order only affects scheduling,
+// never results - tiles are independent.
 __global__ void __launch_bounds__(1024) tile_order_k(const uint32_t* __restrict__ ranges,
-                                                     uint32_t n_tiles,
+                                                     int tiles_x, int tiles_y, int bands,
                                                      uint32_t* __restrict__ order) {
-  __shared__ uint32_t hist[33];
-  __shared__ uint32_t base[33];
-  if (threadIdx.x < 33) hist[threadIdx.x] = 0;
+  __shared__ uint32_t hist[33 * kMaxBands];
+  __shared__ uint32_t base[33 * kMaxBands];
+  const uint32_t n_tiles = (uint32_t)tiles_x * tiles_y;
+  for (int i = threadIdx.x; i < 33 * kMaxBands; i += blockDim.x) hist[i] = 0;
   __syncthreads();
-  for (uint32_t t = threadIdx.x; t < n_tiles; t += blockDim.x) {
+  auto key = [&](uint32_t t) -> int {
     const uint32_t len = ranges[2 * t + 1] - ranges[2 * t];
-    atomicAdd(&hist[len ? 32 - __clz(len) : 0], 1u);
-  }
+    // the band whose rows [blend_band_row(b), blend_band_row(b + 1)) hold t
+    const int band = (((int)(t / tiles_x) + 1) * bands - 1) / tiles_y;
+    return band * 33 + (len ? __clz(len) : 32);  // descending length within the band
+  };
+  for (uint32_t t = threadIdx.x; t < n_tiles; t += blockDim.x) atomicAdd(&hist[key(t)], 1u);
   __syncthreads();
   if (threadIdx.x == 0) {
     uint32_t run = 0;
-    for (int b = 32; b >= 0; --b) {
+    for (int b = 0; b < 33 * bands; ++b) {
       base[b] = run;
       run += hist[b];
     }
   }
   __syncthreads();
-  for (uint32_t t = threadIdx.x; t < n_tiles; t += blockDim.x) {
-    const uint32_t len = ranges[2 * t + 1] - ranges[2 * t];
-    order[atomicAdd(&base[len ? 32 - __clz(len) : 0], 1u)] = t;
-  }
+  for (uint32_t t = threadIdx.x; t < n_tiles; t += blockDim.x) order[atomicAdd(&base[key(t)], 1u)] = t;
 }
+
+// Optional per-CTA timing trace for schedule studies (vms_debug_blend_trace):
+// 8 u64 per CTA: globaltimer at start and end, SM id, list length << 32 |
+// tile, then 4 zero words.
+__device__ unsigned long long* g_blend_trace = nullptr;
 
 // Tile-instance overflow (the frame needs more instances than the buffer
 // holds): the tile lists were not built, and every CTA walks the whole
@@ -207,6 +245,7 @@ __global__ void __launch_bounds__(kBlendThreads) blend_k(const uint32_t* __restr
                                                          const RenderCounters* __restrict__ ctr,
                                                          const BlendRec* __restrict__ rec,
                                                          int w, int h, int tiles_x,
+                                                         uint32_t order_offset,
                                                          float* image_arg,
                                                          const FrameDev* __restrict__ fd,
                                                          int accumulate) {
@@ -214,17 +253,24 @@ __global__ void __launch_bounds__(kBlendThreads) blend_k(const uint32_t* __restr
   using Staged = typename std::conditional<kExact, SplatF64, BlendRec>::type;
   __shared__ Staged sp[kBlendThreads];
   __shared__ uint32_t wsum[kBlendThreads / 32];
-  const int tile = order[blockIdx.x / (SUB * SUB)], sub = blockIdx.x % (SUB * SUB);
+  __shared__ double2 tab[kExact ? 64 : 1];
+  unsigned long long t_start = 0;
+  unsigned long long* trace = g_blend_trace;
+  if (trace && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+  const int tile = order[order_offset + blockIdx.x / (SUB * SUB)], sub = blockIdx.x % (SUB * SUB);
   const int sx0 = (tile % tiles_x) * TS + (sub % SUB) * 16;
   const int sy0 = (tile / tiles_x) * TS + (sub / SUB) * 16;
-  const int px = sx0 + (threadIdx.x & 15), py = sy0 + (threadIdx.x >> 4);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // warp w: 8x4 block at ((w & 1) * 8, (w >> 1) * 4) of the sub-tile
+  const int wx0 = sx0 + (warp & 1) * 8, wy0 = sy0 + (warp >> 1) * 4;
+  const int px = wx0 + (lane & 7), py = wy0 + (lane >> 3);
   const bool inside = px < w && py < h;
+  if (kExact && threadIdx.x < 64) tab[threadIdx.x] = kExp2Tab[threadIdx.x];
   const bool spill = ctr->overflow != 0u;
   const uint32_t start = spill ? 0u : ranges[2 * tile];
   const uint32_t end = spill ? ctr->n_kept : ranges[2 * tile + 1];
   const uint32_t* __restrict__ tv = spill ? vals : tv_tiles;
   float* __restrict__ image = image_arg ? image_arg : fd->image;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   float cr = 0.f, cg = 0.f, cb = 0.f, T = 1.f;
   if (accumulate && inside) {
     const float* p = image + ((size_t)py * w + px) * 3;
@@ -233,6 +279,7 @@ __global__ void __launch_bounds__(kBlendThreads) blend_k(const uint32_t* __restr
     cb = p[2];
   }
   bool done = !inside;
+  const double fx = (double)px + 0.5, fy = (double)py + 0.5;
   for (uint32_t base = start; base < end; base += kBlendThreads) {
     if (__syncthreads_and(done)) break;
     const uint32_t i = base + threadIdx.x;
@@ -263,7 +310,7 @@ __global__ void __launch_bounds__(kBlendThreads) blend_k(const uint32_t* __restr
         d.cb2 = 2.0 * (double)r.cb;  // exact: power-of-two scaling
         d.cc = r.cc;
         d.al = r.alpha;
-        d.skip = r.alpha > 0.f ? log(0x1p-36 / d.al) : 1e300;
+        d.skip = r.skip;
         d.r = r.r;
         d.g = r.g;
         d.b = r.b;
@@ -277,26 +324,41 @@ __global__ void __launch_bounds__(kBlendThreads) blend_k(const uint32_t* __restr
       }
     }
     __syncthreads();
-    if (!done) {
-      for (uint32_t j = 0; j < cnt; ++j) {
-        const Staged& s = sp[j];
+    // this warp: the staged splats touching its 8x4 block, 32 at a time
+    for (uint32_t c0 = 0; c0 < cnt && !__all_sync(0xffffffffu, done); c0 += 32) {
+      bool mine = false;
+      if (c0 + lane < cnt) {
+        const Staged& q = sp[c0 + lane];
+        int x0, x1, y0, y1;
+        if constexpr (kExact) {
+          x0 = q.x0; x1 = q.x1; y0 = q.y0; y1 = q.y1;
+        } else {
+          x0 = q.bx & 0xFFFF; x1 = q.bx >> 16; y0 = q.by & 0xFFFF; y1 = q.by >> 16;
+        }
+        mine = x0 < wx0 + 8 && x1 > wx0 && y0 < wy0 + 4 && y1 > wy0;
+      }
+      uint32_t m = __ballot_sync(0xffffffffu, mine);
+      while (m) {
+        const Staged& s = sp[c0 + __ffs(m) - 1];
+        m &= m - 1;
+        if (done) continue;
         if constexpr (kExact) {
           if (px < s.x0 || px >= s.x1 || py < s.y0 || py >= s.y1) continue;
-          // _core.pyx:49-78: FP64 arithmetic, f32 storage of T and colour
+          // _core.pyx:56-78: FP64 arithmetic, f32 storage of T and colour
           const double t = (double)T;
           if (t < 1.0 / 255.0) {
             done = true;
-            break;
+            continue;
           }
-          const double dx = ((double)px + 0.5) - s.cx;
-          const double dy = ((double)py + 0.5) - s.cy;
+          const double dx = __dsub_rn(fx, s.cx);
+          const double dy = __dsub_rn(fy, s.cy);
           const double sig = -0.5 * __dadd_rn(__dadd_rn(__dmul_rn(__dmul_rn(s.ca, dx), dx),
                                                         __dmul_rn(__dmul_rn(s.cb2, dy), dx)),
                                               __dmul_rn(__dmul_rn(s.cc, dy), dy));
           // weight < 2^-36: T is unchanged bit for bit and the colour moves by
-          // < 2^-36 (far tails of elongated splats) - skip the FP64 exp
+          // < 2^-36 (far tails of elongated splats) - skip the exp
           if (sig < s.skip) continue;
-          double wgt = __dmul_rn(s.al, exp(sig));
+          double wgt = __dmul_rn(s.al, exp_tab(sig, tab));
           if (wgt > 0.99) wgt = 0.99;
           const double wt = __dmul_rn(wgt, t);
           cr = __double2float_rn(__dadd_rn((double)cr, __dmul_rn(wt, s.r)));
@@ -308,7 +370,7 @@ __global__ void __launch_bounds__(kBlendThreads) blend_k(const uint32_t* __restr
           if (px < x0 || px >= x1 || py < y0 || py >= y1) continue;
           if (T < (1.0f / 255.0f)) {
             done = true;
-            break;
+            continue;
           }
           const float dx = ((float)px + 0.5f) - s.cx, dy = ((float)py + 0.5f) - s.cy;
           const float sig = -0.5f * (s.ca * dx * dx + 2.0f * s.cb * dy * dx + s.cc * dy * dy);
@@ -320,8 +382,8 @@ __global__ void __launch_bounds__(kBlendThreads) blend_k(const uint32_t* __restr
           T = T * (1.0f - wgt);
         }
       }
-      if (!done && T < (1.0f / 255.0f)) done = true;
     }
+    if (!done && T < (1.0f / 255.0f)) done = true;
     __syncthreads();
   }
   if (inside) {
@@ -329,6 +391,21 @@ __global__ void __launch_bounds__(kBlendThreads) blend_k(const uint32_t* __restr
     p[0] = cr;
     p[1] = cg;
     p[2] = cb;
+  }
+  if (trace) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned long long t_end;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+      uint32_t smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      unsigned long long* o = trace + 8 * ((size_t)order_offset * SUB * SUB + blockIdx.x);
+      o[0] = t_start;
+      o[1] = t_end;
+      o[2] = smid;
+      o[3] = ((unsigned long long)(end - start) << 32) | (uint32_t)tile;
+      o[4] = o[5] = o[6] = o[7] = 0;
+    }
   }
 }
 
@@ -351,7 +428,7 @@ __global__ void pack_ordered_k(const float* __restrict__ centers, const float* _
   o.g = colors[3 * i + 1];
   o.b = colors[3 * i + 2];
   o.alpha = alphas[i];
-  o.pad_ = 0;
+  o.skip = blend_skip(o.alpha);
   const bool empty = x1 <= x0 || y1 <= y0;
   if (empty) {
     x0 = x1 = y0 = y1 = 0;
@@ -375,9 +452,45 @@ void record(void* const* events, int i, bool external, cudaStream_t s) {
                              external ? cudaEventRecordExternal : cudaEventRecordDefault);
 }
 
+}  // namespace
+
+// First tile row of band b of `bands` (bands of near-equal height).
+int blend_band_row(int b, int bands, int tiles_y) { return (int)((int64_t)b * tiles_y / bands); }
+
+namespace {
+
+// Depth-sorted splat list and tile-sorted instance list of the last render
+// (the radix sorts ping-pong a fixed number of passes).
+const uint32_t* sorted_vals(const RenderWs& w) { return w.v0; }  // 4 depth passes
+const uint32_t* sorted_tiles(const RenderWs& w, uint32_t n_tiles) {
+  return ((tile_bits(n_tiles) + 7) / 8) % 2 ? w.tv1 : w.tv0;
+}
+
+int32_t launch_band(int width, int height, const uint32_t* vals, const RenderWs& w, float* image,
+                    int accumulate, int exact, int band, int bands, cudaStream_t s) {
+  const int ts = tile_size();
+  const int tiles_x = ceil_div(width, ts), tiles_y = ceil_div(height, ts);
+  const uint32_t n_tiles = (uint32_t)tiles_x * tiles_y;
+  auto* kern = exact ? (ts == 16 ? blend_k<true, 16> : blend_k<true, 32>)
+                     : (ts == 16 ? blend_k<false, 16> : blend_k<false, 32>);
+  const uint32_t subs = (uint32_t)(ts / 16) * (ts / 16);
+  const int r0 = blend_band_row(band, bands, tiles_y), r1 = blend_band_row(band + 1, bands, tiles_y);
+  const uint32_t first = (uint32_t)r0 * tiles_x, count = (uint32_t)(r1 - r0) * tiles_x;
+  if (count)
+    kern<<<count * subs, kBlendThreads, 0, s>>>(w.ranges, w.order, sorted_tiles(w, n_tiles), vals,
+                                                w.ctr, w.rec, width, height, tiles_x, first, image,
+                                                w.fd, accumulate);
+  mark("blend", s);
+  VMS_LAUNCH_CHECK("blend");
+  return VMS_OK;
+}
+
+// Tile duplication, tile sort, ranges, a band-major schedule for |bands|
+// bands; then the blend as |bands| launches, unless bands < 0 (the caller
+// launches them with render_band).
 int32_t tiles_and_blend(int width, int height, const uint32_t* vals, const RenderWs& w,
                         float* image, int accumulate, int exact, void* const* events,
-                        bool external, cudaStream_t s) {
+                        bool external, int bands, cudaStream_t s) {
   const int ts = tile_size(), shift = ts == 16 ? 4 : 5;
   const int tiles_x = ceil_div(width, ts), tiles_y = ceil_div(height, ts);
   const uint32_t n_tiles = (uint32_t)tiles_x * tiles_y;
@@ -401,21 +514,48 @@ int32_t tiles_and_blend(int width, int height, const uint32_t* vals, const Rende
   VMS_CUDA(cudaMemsetAsync(w.ranges, 0, sizeof(uint32_t) * 2 * n_tiles, s));
   ranges_k<<<8 * kSMs, T, 0, s>>>(tk, w.ctr, w.ranges);
   mark("ranges", s);
-  tile_order_k<<<1, 1024, 0, s>>>(w.ranges, n_tiles, w.order);
+  const int ab = bands < 0 ? -bands : bands;
+  const int nb = ab < 1 ? 1 : (ab > kMaxBands ? kMaxBands : ab);
+  tile_order_k<<<1, 1024, 0, s>>>(w.ranges, tiles_x, tiles_y, nb, w.order);
   mark("tile_order", s);
   record(events, 2, external, s);
-  auto* kern = exact ? (ts == 16 ? blend_k<true, 16> : blend_k<true, 32>)
-                     : (ts == 16 ? blend_k<false, 16> : blend_k<false, 32>);
-  const uint32_t subs = (uint32_t)(ts / 16) * (ts / 16);
-  kern<<<n_tiles * subs, kBlendThreads, 0, s>>>(w.ranges, w.order, tv, vals, w.ctr, w.rec, width,
-                                                height, tiles_x, image, w.fd, accumulate);
-  mark("blend", s);
+  if (bands < 0) return VMS_OK;  // the caller launches the bands
+  if (tv != sorted_tiles(w, n_tiles)) {
+    set_error("tiles_and_blend: tile sort parity");
+    return VMS_ERR_INVARIANT;
+  }
+  for (int b = 0; b < nb; ++b) {
+    st = launch_band(width, height, vals, w, image, accumulate, exact, b, nb, s);
+    if (st) return st;
+  }
   record(events, 3, external, s);
   VMS_LAUNCH_CHECK("tiles_and_blend");
   return VMS_OK;
 }
 
 }  // namespace
+
+// One-time device setup of the blend (constant exp table).  Called outside
+// any graph capture (session create, ABI entries).
+int32_t blend_init() {
+  static bool done = false;
+  if (done) return VMS_OK;
+  double2 t[64];
+  for (int j = 0; j < 64; ++j) {
+    const long double v = exp2l((long double)j / 64.0L);
+    t[j].x = (double)v;
+    t[j].y = (double)(v - (long double)t[j].x);
+  }
+  VMS_CUDA(cudaMemcpyToSymbol(kExp2Tab, t, sizeof(t)));
+  done = true;
+  return VMS_OK;
+}
+
+int32_t debug_blend_trace(void* dev_ptr) {
+  unsigned long long* p = static_cast<unsigned long long*>(dev_ptr);
+  VMS_CUDA(cudaMemcpyToSymbol(g_blend_trace, &p, sizeof(p)));
+  return VMS_OK;
+}
 
 size_t render_ws_bytes(uint32_t n_cap, uint32_t m_cap, uint32_t n_tiles) {
   size_t b = 0;
@@ -462,8 +602,13 @@ int32_t render_upload_frame(const RenderWs& w, const FrameDev& f, cudaStream_t s
   return VMS_OK;
 }
 
+int32_t render_band(int width, int height, const RenderWs& w, int exact, int band, int bands,
+                    cudaStream_t s) {
+  return launch_band(width, height, sorted_vals(w), w, nullptr, 0, exact, band, bands, s);
+}
+
 int32_t render_finish(int width, int height, const RenderWs& w, int accumulate, int exact,
-                      void* const* events, bool external, cudaStream_t s) {
+                      void* const* events, bool external, int bands, cudaStream_t s) {
   const int T = 256;
   VMS_CUDA(cudaMemsetAsync(w.ctr, 0, sizeof(RenderCounters), s));
   int32_t st = scan_exclusive_u32(w.flag, w.pos, &w.fd->n_splats, 0, w.n_cap, &w.ctr->n_kept,
@@ -477,8 +622,12 @@ int32_t render_finish(int width, int height, const RenderWs& w, int accumulate, 
                       w.radix_ws, s);
   if (st) return st;
   record(events, 1, external, s);
+  if ((alt ? w.v1 : w.v0) != sorted_vals(w)) {
+    set_error("render_finish: depth sort parity");
+    return VMS_ERR_INVARIANT;
+  }
   return tiles_and_blend(width, height, alt ? w.v1 : w.v0, w, nullptr, accumulate, exact, events,
-                         external, s);
+                         external, bands, s);
 }
 
 int32_t composite_ordered(const float* centers, const float* conics, const float* colors,
@@ -496,7 +645,7 @@ int32_t composite_ordered(const float* centers, const float* conics, const float
     compact_k<<<ceil_div<uint32_t>(n, T), T, 0, s>>>(ws.flag, ws.pos, ws.v1, nullptr, n, ws.k0,
                                                      ws.v0);
   }
-  return tiles_and_blend(w, h, ws.v0, ws, image, 1, exact, nullptr, false, s);
+  return tiles_and_blend(w, h, ws.v0, ws, image, 1, exact, nullptr, false, 1, s);
 }
 
 }  // namespace vms

@@ -208,7 +208,7 @@ __global__ void __launch_bounds__(kChunkRecords) preprocess_k(
   o.alpha = r[10];
   o.bx = (uint32_t)p.x0 | ((uint32_t)p.x1 << 16);
   o.by = (uint32_t)p.y0 | ((uint32_t)p.y1 << 16);
-  o.pad_ = 0;
+  o.skip = blend_skip(o.alpha);
   rec[g] = o;
   flag[g] = 1u;
   key_g[g] = __float_as_uint(__double2float_rn(p.tz));

@@ -28,8 +28,14 @@ struct __align__(16) BlendRec {
   float alpha;
   uint32_t bx;  // x0 | x1 << 16
   uint32_t by;  // y0 | y1 << 16
-  uint32_t pad_;
+  float skip;   // f32 <= log(2^-36 / alpha): sigma below it cannot change f32 T
 };
+
+// Exp-skip threshold of a splat, rounded down so that skipping is always
+// conservative (alpha * exp(sigma) < 2^-36 for sigma < skip).
+__device__ __forceinline__ float blend_skip(float alpha) {
+  return alpha > 0.f ? __double2float_rd(log(0x1p-36 / (double)alpha)) : -3.0e38f;
+}
 
 // Per-frame values every render kernel reads from device memory, so that a
 // frame's launch sequence is identical from frame to frame and can be
@@ -81,8 +87,22 @@ int32_t render_preprocess(const float* pool, const Chunk* chunks, uint32_t max_c
 // from w.fd; width/height fix the tile grid.  `events` (optional, 4) are
 // recorded after preprocess-side stages; `external` marks them as graph
 // event-record nodes when the sequence is being captured.
+// `bands` > 1 splits the blend into that many launches over horizontal
+// bands of tile rows; bands < 0 builds the schedule for -bands bands and
+// stops there: the caller launches the bands itself with render_band (e.g.
+// to start each band's device->host copy as soon as it is blended).
 int32_t render_finish(int width, int height, const RenderWs& w, int accumulate, int exact,
-                      void* const* events, bool external, cudaStream_t s);
+                      void* const* events, bool external, int bands, cudaStream_t s);
+int32_t render_band(int width, int height, const RenderWs& w, int exact, int band, int bands,
+                    cudaStream_t s);
+int blend_band_row(int b, int bands, int tiles_y);
+
+// One-time blend setup (constant tables, shared-memory limits); must run
+// before the first blend launch and outside graph capture.
+int32_t blend_init();
+
+// Per-CTA blend timing trace (profiling only; nullptr disables).
+int32_t debug_blend_trace(void* dev_ptr);
 
 // Stage FrameDev from host memory (pageable or pinned) into w.fd.
 int32_t render_upload_frame(const RenderWs& w, const FrameDev& f, cudaStream_t s);

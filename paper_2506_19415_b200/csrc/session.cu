@@ -24,6 +24,7 @@
 // back to the depth-sorted splat list); the host sees the overflow counter
 // when it recycles that frame's buffers and grows the buffer (re-capturing
 // the graph) for the frames after it.
+#include <algorithm>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -33,6 +34,10 @@
 #include "common.cuh"
 #include "render.h"
 #include "vis.h"
+
+namespace {
+constexpr int kBands = 4;  // blend launches / image copy pieces for host output
+}
 
 namespace {
 struct Graph {
@@ -50,6 +55,9 @@ struct vms_session {
   vms_session_desc d;
   vms_pagetable* pt = nullptr;
   cudaStream_t vis_stream = nullptr, copy_stream = nullptr, cap_stream = nullptr;
+  cudaStream_t d2h_stream = nullptr;  // banded image copies to the host
+  cudaEvent_t ev_band[kBands] = {};
+  cudaEvent_t ev_d2h = nullptr;
   cudaEvent_t ev_vis = nullptr, ev_copy = nullptr, ev_staging = nullptr;
   cudaEvent_t ev_done[2] = {nullptr, nullptr};
   cudaEvent_t tev[10] = {};
@@ -81,7 +89,7 @@ struct vms_session {
   int64_t max_chunks = 0;
   int parity = 0;
   bool use_graphs = true;
-  Graph vis_graph, render_graph[2];  // render: [timing]
+  Graph vis_graph, render_graph[2][2];  // render: [timing][banded]
   std::vector<uint64_t> level_start;  // first row of each level block
   std::vector<uint32_t> plan_pid;
   std::vector<uint8_t> plan_level;
@@ -94,11 +102,14 @@ namespace {
 void free_session(vms_session* s) {
   if (!s) return;
   s->vis_graph.reset();
-  s->render_graph[0].reset();
-  s->render_graph[1].reset();
+  for (auto& gt : s->render_graph)
+    for (auto& g : gt) g.reset();
   if (s->pt) vms_pt_destroy(s->pt);
-  for (cudaStream_t x : {s->vis_stream, s->copy_stream, s->cap_stream})
+  for (cudaStream_t x : {s->vis_stream, s->copy_stream, s->cap_stream, s->d2h_stream})
     if (x) cudaStreamDestroy(x);
+  for (cudaEvent_t e : s->ev_band)
+    if (e) cudaEventDestroy(e);
+  if (s->ev_d2h) cudaEventDestroy(s->ev_d2h);
   for (cudaEvent_t e : {s->ev_vis, s->ev_copy, s->ev_staging, s->ev_done[0], s->ev_done[1]})
     if (e) cudaEventDestroy(e);
   for (cudaEvent_t e : s->tev)
@@ -133,8 +144,8 @@ int32_t ensure_ws(vms_session* s, int w, int h, uint32_t m_cap) {
     VMS_CUDA(cudaFree(s->ws));
     s->ws = nullptr;
   }
-  s->render_graph[0].reset();
-  s->render_graph[1].reset();
+  for (auto& gt : s->render_graph)
+    for (auto& g : gt) g.reset();
   VMS_CUDA(cudaMalloc(&s->ws, bytes));
   s->ws_bytes = bytes;
   s->m_cap = m_cap;
@@ -215,7 +226,7 @@ int32_t run_captured(vms_session* s, Graph& g, int w, int h, uint32_t m_cap, F&&
   return VMS_OK;
 }
 
-int32_t launch_render(vms_session* s, int w, int h, bool timing, cudaStream_t st) {
+int32_t launch_render(vms_session* s, int w, int h, bool timing, bool banded, cudaStream_t st) {
   RenderWs ws = render_carve(s->ws, s->d.capacity * s->d.page_size, s->m_cap, tile_count(w, h));
   const uint32_t max_chunks = (uint32_t)s->max_chunks;
   auto enqueue = [&](cudaStream_t q, bool captured) -> int32_t {
@@ -228,9 +239,20 @@ int32_t launch_render(vms_session* s, int w, int h, bool timing, cudaStream_t st
     if (timing)
       VMS_CUDA(cudaEventRecordWithFlags(s->tev[4], q,
                                         captured ? cudaEventRecordExternal : cudaEventRecordDefault));
-    return render_finish(w, h, ws, 0, s->d.exact, ev, captured, q);
+    return render_finish(w, h, ws, 0, s->d.exact, ev, captured, banded ? -kBands : 1, q);
   };
-  return run_captured(s, s->render_graph[timing ? 1 : 0], w, h, s->m_cap, enqueue, st);
+  int32_t rc = run_captured(s, s->render_graph[timing ? 1 : 0][banded ? 1 : 0], w, h, s->m_cap,
+                            enqueue, st);
+  if (rc || !banded) return rc;
+  // banded: the blend bands are launched after the graph, each followed by
+  // an event the image copy of that band waits for
+  for (int b = 0; b < kBands; ++b) {
+    rc = render_band(w, h, ws, s->d.exact, b, kBands, st);
+    if (rc) return rc;
+    VMS_CUDA(cudaEventRecord(s->ev_band[b], st));
+  }
+  if (timing) VMS_CUDA(cudaEventRecord(s->tev[7], st));
+  return VMS_OK;
 }
 
 // The frame two back used this parity's pinned buffers: wait for its render,
@@ -281,6 +303,7 @@ vms_session* vms_session_create(const vms_session_desc* desc) {
     set_error("session_create: pool larger than 2^32 records");
     return nullptr;
   }
+  if (blend_init() != VMS_OK) return nullptr;
   vms_session* s = new vms_session();
   s->d = *desc;
   s->pt = vms_pt_create(desc->capacity);
@@ -305,6 +328,10 @@ vms_session* vms_session_create(const vms_session_desc* desc) {
   ok = ok && cudaStreamCreateWithPriority(&s->vis_stream, cudaStreamNonBlocking, hi) == cudaSuccess;
   ok = ok && cudaStreamCreateWithFlags(&s->copy_stream, cudaStreamNonBlocking) == cudaSuccess;
   ok = ok && cudaStreamCreateWithFlags(&s->cap_stream, cudaStreamNonBlocking) == cudaSuccess;
+  ok = ok && cudaStreamCreateWithFlags(&s->d2h_stream, cudaStreamNonBlocking) == cudaSuccess;
+  for (cudaEvent_t& e : s->ev_band)
+    ok = ok && cudaEventCreateWithFlags(&e, cudaEventDisableTiming) == cudaSuccess;
+  ok = ok && cudaEventCreateWithFlags(&s->ev_d2h, cudaEventDisableTiming) == cudaSuccess;
   for (cudaEvent_t* e : {&s->ev_vis, &s->ev_copy, &s->ev_staging, &s->ev_done[0], &s->ev_done[1]})
     ok = ok && cudaEventCreateWithFlags(e, cudaEventDisableTiming) == cudaSuccess;
   for (cudaEvent_t& e : s->tev) ok = ok && cudaEventCreate(&e) == cudaSuccess;
@@ -481,17 +508,32 @@ int32_t vms_session_frame(vms_session* s, const vms_frame_args* a, vms_frame_sta
   if (n_chunks)
     VMS_CUDA(cudaMemcpyAsync(s->chunks_d, s->chunks_h[par], sizeof(vms_chunk) * n_chunks,
                              cudaMemcpyHostToDevice, st));
-  rc = launch_render(s, W, H, timing, st);
+  // host output: the blend runs as kBands launches over bands of tile rows
+  // and each band's rows go to the host as soon as that band is blended
+  const bool banded = a->host_image != nullptr;
+  rc = launch_render(s, W, H, timing, banded, st);
   if (rc) return rc;
+  if (banded) {
+    const int ts = tile_size(), tiles_y = ceil_div(H, ts);
+    const size_t row_bytes = sizeof(float) * 3 * (size_t)W;
+    for (int b = 0; b < kBands; ++b) {
+      const int y0 = blend_band_row(b, kBands, tiles_y) * ts;
+      const int y1 = std::min(blend_band_row(b + 1, kBands, tiles_y) * ts, H);
+      VMS_CUDA(cudaStreamWaitEvent(s->d2h_stream, s->ev_band[b], 0));
+      if (y1 > y0)
+        VMS_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(a->host_image) + row_bytes * y0,
+                                 reinterpret_cast<const char*>(a->image) + row_bytes * y0,
+                                 row_bytes * (y1 - y0), cudaMemcpyDeviceToHost, s->d2h_stream));
+    }
+    VMS_CUDA(cudaEventRecord(s->ev_d2h, s->d2h_stream));
+    VMS_CUDA(cudaStreamWaitEvent(st, s->ev_d2h, 0));
+  }
   VMS_CUDA(cudaMemcpyAsync(s->counters_h[par], ws.ctr, sizeof(uint32_t) * 4,
                            cudaMemcpyDeviceToHost, st));
   VMS_CUDA(cudaEventRecord(s->ev_done[par], st));
   s->pending[par] = true;
   s->last_par = par;
   if (timing) VMS_CUDA(cudaEventRecord(s->tev[9], st));
-  if (a->host_image)
-    VMS_CUDA(cudaMemcpyAsync(a->host_image, a->image, sizeof(float) * 3 * (size_t)W * H,
-                             cudaMemcpyDeviceToHost, st));
   // stats (runtime.py:471-481)
   out->required = n_req;
   out->resident = (uint32_t)vms_pt_resident_count(s->pt);
@@ -504,7 +546,7 @@ int32_t vms_session_frame(vms_session* s, const vms_frame_args* a, vms_frame_sta
   out->n_res = (uint32_t)n_res;
   rc = vms_pt_resident_counts(s->pt, out->resident_per_level, (int32_t)s->d.lod_levels);
   if (rc) return rc;
-  if (timing || a->host_image) {
+  if (timing || a->host_image || a->sync) {
     VMS_CUDA(cudaStreamSynchronize(st));
     const uint32_t* c = s->counters_h[par];
     out->n_kept = c[0];

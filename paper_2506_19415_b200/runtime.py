@@ -424,7 +424,10 @@ class VmSession:
             d.exact = int(self.exact)
             d.upload_mode = self.upload_mode
             # tile-instance capacity; the session regrows it on overflow
-            d.m_cap = int(instance_capacity) if instance_capacity else max(16 * self.n_cap, 1 << 20)
+            # (64 M instances, 1 GB: frames with the camera inside dense
+            # geometry need tens of millions; past it they blend through the
+            # exact but slower spill path)
+            d.m_cap = int(instance_capacity) if instance_capacity else 1 << 26
             self._desc = d
             self._h = None
             h = self._lib.vms_session_create(ctypes.byref(d))
@@ -459,9 +462,11 @@ class VmSession:
     def render_frame(self, camera, frame_index: int, out=None):
         """Run one frame.  Returns (image, stats) with the reference's stats
         keys (runtime.py:471-488) plus device counters.  ``out``: None -> a new
-        numpy array; a float32 (h, w, 3) numpy array (ideally pinned) ->
-        filled in place; "device" -> a CUDA tensor (no host copy; final once
-        the next render_frame/flush call returns)."""
+        (page-locked) numpy array; a float32 (h, w, 3) numpy array -> filled
+        in place (by DMA when it is page-locked, else through a staging
+        buffer); "device" -> a CUDA tensor, ordered on the current stream (the
+        session alternates two such buffers), returned as soon as the frame
+        is enqueued."""
         t = _device.torch()
         lib = self._lib
         h0 = time.perf_counter()
@@ -478,28 +483,31 @@ class VmSession:
         a.budget = float(self.staging_pages)
         a.timing = int(self.timing)
         device_out = isinstance(out, str) and out == "device"
-        image = self._frame_image(camera)
-        a.image = image.data_ptr()
+        a.host_image = None
+        a.sync = 0
         host = None
+        image = self._frame_image(camera)
         if not device_out:
+            # the frame is copied to page-locked memory by DMA right after the
+            # blend (the caller's array when it is page-locked, else a fresh
+            # page-locked array / a staging buffer)
             if out is None:
-                key = (camera.height, camera.width)
-                if self._pinned_out is None or self._pinned_out[0] != key:
-                    self._pinned_out = (key, t.empty((camera.height, camera.width, 3),
-                                                     dtype=t.float32).pin_memory())
-                host = self._pinned_out[1]
+                host = t.empty((camera.height, camera.width, 3), dtype=t.float32, pin_memory=True)
                 a.host_image = host.data_ptr()
             else:
                 if out.dtype != np.float32 or out.shape != (camera.height, camera.width, 3) \
                         or not out.flags.c_contiguous:
                     raise ValueError("out must be a C-contiguous float32 (h, w, 3) array")
-                a.host_image = out.ctypes.data
-        else:
-            a.host_image = None
+                if self._zero_copy(out):
+                    a.host_image = out.ctypes.data
+                else:
+                    host = self._staging(camera)
+                    a.host_image = host.data_ptr()
+        a.image = image.data_ptr()
         stream = _device.sptr()
         st = self._stats
-        # one call: visibility, page table, uploads, render (tile-instance
-        # overflows are regrown and re-rendered inside the session)
+        # one call: visibility, page table, uploads, render graph, and for
+        # host output the banded image copy (waits for the frame)
         _lib.check(lib.vms_session_frame(self._h, ctypes.byref(a), ctypes.byref(st), stream),
                    "render_frame")
         usage = st.occupied_entries / self.capacity
@@ -540,8 +548,30 @@ class VmSession:
         if device_out:
             return image, stats
         if out is None:
-            return host.numpy().copy(), stats
+            return host.numpy(), stats
+        if host is not None:
+            out[...] = host.numpy()
         return out, stats
+
+    def _zero_copy(self, arr) -> bool:
+        key = (arr.ctypes.data, arr.nbytes)
+        cache = self.__dict__.setdefault("_zc_cache", {})
+        hit = cache.get(key)
+        if hit is None:
+            hit = bool(self._lib.vms_host_accessible(arr.ctypes.data)) and bool(
+                self._lib.vms_host_accessible(arr.ctypes.data + arr.nbytes - 1))
+            if len(cache) > 64:
+                cache.clear()
+            cache[key] = hit
+        return hit
+
+    def _staging(self, camera):
+        t = _device.torch()
+        key = (camera.height, camera.width)
+        if self._pinned_out is None or self._pinned_out[0] != key:
+            self._pinned_out = (key, t.empty((camera.height, camera.width, 3), dtype=t.float32)
+                                .pin_memory())
+        return self._pinned_out[1]
 
     def flush(self):
         """Wait for the last frame (device-output mode); returns its device
