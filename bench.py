@@ -143,16 +143,22 @@ def peaks():
         return 6650.0, "fallback"
 
 
-def launches_per_frame(stats, n_faces, upload_mode):
-    """Kernel launches of libvmsplat_b200.so per frame (static count of the
-    launch sequence in vis.cu / abi.cu / prims.cu / blend.cu)."""
-    vis = (5 if n_faces else 0) + 1 + 1 + 1 + 3 + 1
-    up = 1 if (stats["planned_copies"] and upload_mode == 1) else 0
-    render = 0
-    if stats["n_resident_records"]:
-        render = 1 + 4 + 12 + 14
-    else:
-        render = 12 + 14
+def launches_per_frame(stats, n_faces, upload_mode, host_output=False):
+    """Kernels of libvmsplat_b200.so launched per frame (static count of the
+    captured sequences in vis.cu / prims.cu / preprocess.cu / blend.cu and the
+    per-frame copies in session.cu):
+      visibility graph  vis_count, scan, vis_emit, vis_raster, vis_links,
+                        vis_flags, scan, vis_required                     8
+      page copies       upload_k (copy stream), scatter_k                 2
+      render graph      preprocess, scan, compact, radix hist + 4 passes,
+                        dup_count, scan, dup_emit, clamp, radix hist + 2
+                        passes, ranges, tile_order, blend                18
+    (host output without zero-copy runs the blend as 4 band launches)."""
+    vis = 8 if n_faces else 5
+    up = 2 if stats["planned_copies"] else 0
+    if up and upload_mode != 1:
+        up = 1  # per-page cudaMemcpyAsync + scatter
+    render = 18
     return vis + up + render
 
 

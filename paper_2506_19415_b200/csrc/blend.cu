@@ -386,7 +386,23 @@ __global__ void __launch_bounds__(kBlendThreads) blend_k(const uint32_t* __restr
     if (!done && T < (1.0f / 255.0f)) done = true;
     __syncthreads();
   }
-  if (inside) {
+  // output: the 16x16 block goes through shared memory and out as whole
+  // rows of 16-byte stores (coalesced; with a zero-copy host image these are
+  // full PCIe writes instead of scattered 4-byte ones)
+  __shared__ __align__(16) float obuf[16][48];
+  const int lx = px - sx0, ly = py - sy0;
+  obuf[ly][3 * lx + 0] = cr;
+  obuf[ly][3 * lx + 1] = cg;
+  obuf[ly][3 * lx + 2] = cb;
+  __syncthreads();
+  if ((w & 3) == 0 && sx0 + 16 <= w) {
+    for (int k = threadIdx.x; k < 16 * 12; k += kBlendThreads) {
+      const int row = k / 12, c4 = k - row * 12, y = sy0 + row;
+      if (y < h)
+        *reinterpret_cast<float4*>(image + ((size_t)y * w + sx0) * 3 + 4 * c4) =
+            *reinterpret_cast<const float4*>(&obuf[row][4 * c4]);
+    }
+  } else if (inside) {
     float* p = image + ((size_t)py * w + px) * 3;
     p[0] = cr;
     p[1] = cg;

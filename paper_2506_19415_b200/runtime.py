@@ -488,22 +488,29 @@ class VmSession:
         host = None
         image = self._frame_image(camera)
         if not device_out:
-            # the frame is copied to page-locked memory by DMA right after the
-            # blend (the caller's array when it is page-locked, else a fresh
-            # page-locked array / a staging buffer)
+            # host output: the blend writes the page-locked host array directly
+            # (zero-copy, whole-row PCIe writes overlapped with the blend) - the
+            # caller's array when it is page-locked, else a fresh page-locked
+            # array (out=None) or a staging buffer copied into `out`.  Memory
+            # the device cannot address takes a banded device->host copy.
             if out is None:
                 host = t.empty((camera.height, camera.width, 3), dtype=t.float32, pin_memory=True)
-                a.host_image = host.data_ptr()
+                target = host.numpy()
             else:
                 if out.dtype != np.float32 or out.shape != (camera.height, camera.width, 3) \
                         or not out.flags.c_contiguous:
                     raise ValueError("out must be a C-contiguous float32 (h, w, 3) array")
                 if self._zero_copy(out):
-                    a.host_image = out.ctypes.data
+                    target = out
                 else:
                     host = self._staging(camera)
-                    a.host_image = host.data_ptr()
-        a.image = image.data_ptr()
+                    target = host.numpy()
+            if self._zero_copy(target):
+                image = target
+                a.sync = 1
+            else:
+                a.host_image = target.ctypes.data
+        a.image = image.ctypes.data if isinstance(image, np.ndarray) else image.data_ptr()
         stream = _device.sptr()
         st = self._stats
         # one call: visibility, page table, uploads, render graph, and for

@@ -424,3 +424,33 @@ def test_tile_instance_overflow_recovers(cuda):
             small.flush()
             img = dev.cpu().numpy()
         assert np.array_equal(img, ref), f
+
+
+def test_output_modes_identical(cuda):
+    """Every output path gives the same image: device tensor, page-locked
+    array (zero-copy blend writes), pageable array (staging + copy) and a
+    fresh array - on two sessions stepping the same frames."""
+    import torch
+
+    from paper_2506_19415_b200.runtime import VmSession
+
+    sc = _city()
+    path = inputs.city_path(inputs.CITY_SMALL)
+    a = VmSession(sc, buffer_pages=16, staging_pages=6.0, vis_scale=0.5)
+    b = VmSession(sc, buffer_pages=16, staging_pages=6.0, vis_scale=0.5)
+    cam0 = path.frame_camera(0)
+    pinned = torch.empty((cam0.height, cam0.width, 3), dtype=torch.float32).pin_memory().numpy()
+    pageable = np.empty((cam0.height, cam0.width, 3), np.float32)
+    for f in range(path.frame_count):
+        cam = path.frame_camera(f)
+        ref, _ = a.render_frame(cam, f)
+        mode = f % 3
+        if mode == 0:
+            dev, _ = b.render_frame(cam, f, out="device")
+            b.flush()
+            img = dev.cpu().numpy()
+        elif mode == 1:
+            img, _ = b.render_frame(cam, f, out=pinned)
+        else:
+            img, _ = b.render_frame(cam, f, out=pageable)
+        assert np.array_equal(img, ref), (f, mode)
