@@ -2,12 +2,14 @@
 //
 //   compact_k     kept splats in gather order -> (depth key, gather idx)
 //   radix (32b)   stable depth sort: ties keep gather order (render.py:235-239)
-//   dup_count_k / dup_emit_k  one instance per overlapped 16x16 tile, emitted
-//                 in depth order
+//   dup_count_k   per sorted splat: tile rectangle, instance count, and the
+//                 per-tile counts as a 2D difference array
+//   tile_prep_k   per-tile counts -> list ranges, overflow, the tile sort's
+//                 digit histograms, the blend schedule (one CTA)
+//   dup_emit_k    one instance per overlapped tile, emitted in depth order
 //   radix (tile)  stable sort on the tile id only -> per tile the instances
 //                 are in (depth key, gather idx) order, i.e. the reference's
 //                 global order restricted to the tile (SURVEY §0 finding 1)
-//   ranges_k      [start, end) per tile
 //   blend_k       one CTA per tile, one thread per pixel; splats staged in
 //                 shared memory 256 at a time; per-pixel half-open bbox test,
 //                 stop test before blending, 0.99 clamp, early exit once every
@@ -72,26 +74,168 @@ __device__ __forceinline__ void tile_rect(const BlendRec& r, int shift, int* tx0
   *ty1 = (y1 - 1) >> shift;
 }
 
+// Tile rectangle of a splat's clamped pixel box, inclusive tile bounds
+// packed tx0 | tx1 << 8 | ty0 << 16 | ty1 << 24 (tile grids up to 256 x 256).
+__device__ __forceinline__ uint32_t rect_of(const BlendRec& r, int shift) {
+  int tx0, tx1, ty0, ty1;
+  tile_rect(r, shift, &tx0, &tx1, &ty0, &ty1);
+  return (uint32_t)tx0 | ((uint32_t)tx1 << 8) | ((uint32_t)ty0 << 16) | ((uint32_t)ty1 << 24);
+}
+
+constexpr int kDiffSmemWords = 12288;  // 48 KB
+constexpr int kMaxBands = 8;           // blend launches per frame (host-output banding)
+
+// Per depth-sorted splat: instance count and packed tile rectangle.  The
+// per-tile instance counts come for free as a 2D difference array over the
+// tile grid (4 updates per splat, gx = tiles_x + 1 columns) accumulated in
+// shared memory and flushed once per CTA; tile_prep_k integrates it.
 __global__ void dup_count_k(const uint32_t* __restrict__ vals, const BlendRec* __restrict__ rec,
-                            const RenderCounters* __restrict__ ctr, int shift,
-                            uint32_t* __restrict__ cnt) {
+                            const RenderCounters* __restrict__ ctr, int shift, int gx, int gy,
+                            uint32_t* __restrict__ cnt, uint32_t* __restrict__ rects,
+                            uint32_t* __restrict__ tdiff) {
+  extern __shared__ uint32_t sdiff[];
+  const int cells = gx * gy;
+  const bool local = cells <= kDiffSmemWords;
+  uint32_t* d = local ? sdiff : tdiff;
+  if (local) {
+    for (int i = threadIdx.x; i < cells; i += blockDim.x) sdiff[i] = 0u;
+    __syncthreads();
+  }
   const uint32_t n = ctr->n_kept;
   for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < n; s += gridDim.x * blockDim.x) {
-    int tx0, tx1, ty0, ty1;
-    tile_rect(rec[vals[s]], shift, &tx0, &tx1, &ty0, &ty1);
+    const uint32_t rc = rect_of(rec[vals[s]], shift);
+    const int tx0 = rc & 0xFF, tx1 = (rc >> 8) & 0xFF, ty0 = (rc >> 16) & 0xFF, ty1 = rc >> 24;
     cnt[s] = (uint32_t)((tx1 - tx0 + 1) * (ty1 - ty0 + 1));
+    rects[s] = rc;
+    atomicAdd(&d[ty0 * gx + tx0], 1u);
+    atomicAdd(&d[ty0 * gx + tx1 + 1], 0xFFFFFFFFu);
+    atomicAdd(&d[(ty1 + 1) * gx + tx0], 0xFFFFFFFFu);
+    atomicAdd(&d[(ty1 + 1) * gx + tx1 + 1], 1u);
+  }
+  if (local) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < cells; i += blockDim.x)
+      if (sdiff[i]) atomicAdd(&tdiff[i], sdiff[i]);
   }
 }
 
-// Load-balanced expansion: each CTA owns a contiguous run of kEmitChunk
-// output instances, finds the splats covering it by binary search over the
-// exclusive offsets, and every thread writes consecutive instances
-// (coalesced) regardless of how many tiles one splat touches.
-constexpr int kEmitChunk = 1024;
+// One CTA, once per frame: integrates the difference array into per-tile
+// instance counts, and from them derives everything the tile stage needs
+// without touching the instances: the [start, end) range of every tile's
+// list (exclusive scan), the overflow decision, the digit histograms of both
+// tile-sort radix passes (their "upsweep"), and the blend schedule
+// (band-major, longest list first, bucketed by floor(log2(length))).
+__global__ void __launch_bounds__(1024) tile_prep_k(
+    const uint32_t* __restrict__ tdiff, int tiles_x, int tiles_y, int bands, uint32_t m_cap,
+    RenderCounters* __restrict__ ctr, uint32_t* __restrict__ tcount,
+    uint32_t* __restrict__ ranges, uint32_t* __restrict__ order, uint32_t* __restrict__ rcounters,
+    uint32_t* __restrict__ ghist) {
+  __shared__ uint32_t h[2][256];
+  __shared__ uint32_t scratch[33];
+  __shared__ uint32_t hist[33 * kMaxBands];
+  __shared__ uint32_t base[33 * kMaxBands];
+  const int gx = tiles_x + 1;
+  const uint32_t n_tiles = (uint32_t)tiles_x * tiles_y;
+  for (int i = threadIdx.x; i < 512; i += blockDim.x) (&h[0][0])[i] = 0u;
+  for (int i = threadIdx.x; i < 33 * kMaxBands; i += blockDim.x) hist[i] = 0u;
+  if (threadIdx.x < 64) rcounters[threadIdx.x] = 0u;
+  // rows: running sums along x; then columns: running sums along y
+  for (int y = threadIdx.x; y < tiles_y; y += blockDim.x) {
+    uint32_t run = 0;
+    for (int x = 0; x < tiles_x; ++x) {
+      run += tdiff[y * gx + x];
+      tcount[y * tiles_x + x] = run;
+    }
+  }
+  __syncthreads();
+  for (int x = threadIdx.x; x < tiles_x; x += blockDim.x) {
+    uint32_t run = 0;
+    for (int y = 0; y < tiles_y; ++y) {
+      run += tcount[y * tiles_x + x];
+      tcount[y * tiles_x + x] = run;
+    }
+  }
+  __syncthreads();
+  // exclusive scan over tiles -> ranges; each thread a contiguous run
+  const uint32_t per = (n_tiles + blockDim.x - 1) / blockDim.x;
+  const uint32_t t0 = threadIdx.x * per, t1 = min(n_tiles, t0 + per);
+  uint32_t local = 0;
+  for (uint32_t t = t0; t < t1; ++t) local += tcount[t];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t inc = local;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t v = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += v;
+  }
+  if (lane == 31) scratch[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    const uint32_t v = lane < (int)(blockDim.x / 32) ? scratch[lane] : 0u;
+    uint32_t wi = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t u = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= o) wi += u;
+    }
+    scratch[lane] = wi - v;
+    if (lane == 31) scratch[32] = wi;
+  }
+  __syncthreads();
+  uint32_t run = scratch[warp] + inc - local;
+  const uint32_t total = scratch[32];
+  for (uint32_t t = t0; t < t1; ++t) {
+    const uint32_t c = tcount[t];
+    ranges[2 * t] = run;
+    ranges[2 * t + 1] = run + c;
+    run += c;
+    if (c) {
+      atomicAdd(&h[0][t & 255u], c);
+      atomicAdd(&h[1][(t >> 8) & 255u], c);
+    }
+  }
+  if (threadIdx.x == 0) {
+    // total == ctr->n_inst (the scan of per-splat counts)
+    ctr->n_need = total;
+    if (total > m_cap) {
+      ctr->overflow = 1;
+      ctr->n_inst = 0;  // no lists: blend_k takes the spill path
+    }
+  }
+  // schedule
+  auto key = [&](uint32_t t) -> int {
+    const uint32_t len = tcount[t];
+    // the band whose rows [blend_band_row(b), blend_band_row(b + 1)) hold t
+    const int band = (((int)(t / tiles_x) + 1) * bands - 1) / tiles_y;
+    return band * 33 + (len ? __clz(len) : 32);  // descending length within the band
+  };
+  for (uint32_t t = threadIdx.x; t < n_tiles; t += blockDim.x) atomicAdd(&hist[key(t)], 1u);
+  __syncthreads();
+  for (int i = threadIdx.x; i < 512; i += blockDim.x) ghist[i] = (&h[0][0])[i];
+  if (threadIdx.x == 0) {
+    uint32_t r = 0;
+    for (int b = 0; b < 33 * bands; ++b) {
+      base[b] = r;
+      r += hist[b];
+    }
+  }
+  __syncthreads();
+  for (uint32_t t = threadIdx.x; t < n_tiles; t += blockDim.x) order[atomicAdd(&base[key(t)], 1u)] = t;
+}
+
+// Load-balanced expansion: each CTA owns contiguous runs of kEmitChunk
+// output instances (depth-sorted splats emit their tile rectangles in order;
+// near splats can cover thousands of tiles, so the split is by instances,
+// not by splats).  The splats covering a run are found with a warp-parallel
+// 32-ary search over the exclusive offsets (a handful of L2 round trips),
+// staged in shared memory, and every thread writes consecutive instances
+// (coalesced).  Also clears the look-back status words of the tile-sort
+// passes (sized by the frame's instance count).
+constexpr int kEmitChunk = 2048;
 constexpr int kEmitThreads = 256;
 
 __device__ __forceinline__ uint32_t last_le(const uint32_t* a, uint32_t n, uint32_t x) {
-  // largest j < n with a[j] <= x (a ascending, a[0] == 0)
+  // largest j < n with a[j] <= x (a ascending, a[0] <= x)
   uint32_t lo = 0, hi = n;
   while (hi - lo > 1) {
     const uint32_t mid = (lo + hi) >> 1;
@@ -100,56 +244,64 @@ __device__ __forceinline__ uint32_t last_le(const uint32_t* a, uint32_t n, uint3
   return lo;
 }
 
+// The same search by one warp over global memory, 32 pivots per round.
+__device__ __forceinline__ uint32_t warp_last_le(const uint32_t* __restrict__ a, uint32_t n,
+                                                 uint32_t x) {
+  const int lane = threadIdx.x & 31;
+  uint32_t lo = 0, hi = n;
+  while (hi - lo > 1) {
+    const uint32_t step = (hi - lo + 31) / 32;
+    const uint32_t piv = lo + (uint32_t)lane * step;
+    const bool le = piv < hi && a[piv] <= x;
+    const uint32_t b = __ballot_sync(0xffffffffu, le);  // a prefix of lanes (a ascending)
+    const uint32_t last = 31 - __clz(b);                  // lane 0 always holds (a[lo] <= x)
+    lo = lo + last * step;
+    hi = min(hi, lo + step);
+  }
+  return lo;
+}
+
 __global__ void __launch_bounds__(kEmitThreads) dup_emit_k(
-    const uint32_t* __restrict__ vals, const BlendRec* __restrict__ rec,
-    const uint32_t* __restrict__ off, RenderCounters* __restrict__ ctr, uint32_t m_cap,
-    int tiles_x, int shift, uint32_t* __restrict__ tk, uint32_t* __restrict__ tv) {
+    const uint32_t* __restrict__ vals, const uint32_t* __restrict__ rects,
+    const uint32_t* __restrict__ off, const RenderCounters* __restrict__ ctr, int tiles_x,
+    uint32_t* __restrict__ tk, uint32_t* __restrict__ tv, uint32_t* __restrict__ status,
+    size_t pass_stride, uint32_t tile_items) {
   __shared__ uint32_t soff[kEmitChunk + 1];
-  __shared__ uint4 sinfo[kEmitChunk];  // g, tx0, ty0, tiles across
+  __shared__ uint2 sinfo[kEmitChunk];  // g, tx0 | ty0 << 8 | tiles across << 16
   __shared__ uint32_t span[2];
   const uint32_t n = ctr->n_kept, m = ctr->n_inst;
-  if (m > m_cap || n == 0) return;
+  const size_t used = (size_t)((m + tile_items - 1) / tile_items) * 256;
+  for (size_t i = blockIdx.x * (size_t)kEmitThreads + threadIdx.x; i < used;
+       i += (size_t)gridDim.x * kEmitThreads) {
+    status[i] = 0u;
+    status[pass_stride + i] = 0u;
+  }
+  if (m == 0 || n == 0) return;  // no instances, or overflow (spill blend)
+  const int warp = threadIdx.x >> 5;
   for (uint32_t i0 = blockIdx.x * kEmitChunk; i0 < m; i0 += gridDim.x * kEmitChunk) {
     const uint32_t i1 = min(m, i0 + kEmitChunk);
-    if (threadIdx.x == 0) span[0] = last_le(off, n, i0);
-    if (threadIdx.x == 1) span[1] = last_le(off, n, i1 - 1);
+    if (warp < 2) {
+      const uint32_t r = warp_last_le(off, n, warp == 0 ? i0 : i1 - 1);
+      if ((threadIdx.x & 31) == 0) span[warp] = r;
+    }
     __syncthreads();
-    const uint32_t s0 = span[0], ns = span[1] - s0 + 1;
+    const uint32_t s0 = span[0], ns = span[1] - s0 + 1;  // <= kEmitChunk: each has >= 1
     for (uint32_t j = threadIdx.x; j < ns; j += kEmitThreads) {
-      const uint32_t g = vals[s0 + j];
-      int tx0, tx1, ty0, ty1;
-      tile_rect(rec[g], shift, &tx0, &tx1, &ty0, &ty1);
+      const uint32_t rc = rects[s0 + j];
+      const uint32_t tx0 = rc & 0xFF, tx1 = (rc >> 8) & 0xFF, ty0 = (rc >> 16) & 0xFF;
       soff[j] = off[s0 + j];
-      sinfo[j] = make_uint4(g, (uint32_t)tx0, (uint32_t)ty0, (uint32_t)(tx1 - tx0 + 1));
+      sinfo[j] = make_uint2(vals[s0 + j], tx0 | (ty0 << 8) | ((tx1 - tx0 + 1) << 16));
     }
     __syncthreads();
     for (uint32_t i = i0 + threadIdx.x; i < i1; i += kEmitThreads) {
       const uint32_t j = last_le(soff, ns, i);
-      const uint4 inf = sinfo[j];
-      const uint32_t k = i - soff[j];
-      const uint32_t ty = inf.z + k / inf.w, tx = inf.y + k % inf.w;
+      const uint2 inf = sinfo[j];
+      const uint32_t k = i - soff[j], wd = inf.y >> 16;
+      const uint32_t ty = ((inf.y >> 8) & 0xFF) + k / wd, tx = (inf.y & 0xFF) + k % wd;
       tk[i] = ty * (uint32_t)tiles_x + tx;
       tv[i] = inf.x;
     }
     __syncthreads();
-  }
-}
-
-__global__ void clamp_inst_k(RenderCounters* ctr, uint32_t m_cap) {
-  ctr->n_need = ctr->n_inst;
-  if (ctr->n_inst > m_cap) {
-    ctr->overflow = 1;
-    ctr->n_inst = 0;  // downstream stages see an empty frame; host re-runs
-  }
-}
-
-__global__ void ranges_k(const uint32_t* __restrict__ tk, const RenderCounters* __restrict__ ctr,
-                         uint32_t* __restrict__ ranges) {
-  const uint32_t m = ctr->n_inst;
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
-    const uint32_t t = tk[i];
-    if (i == 0 || tk[i - 1] != t) ranges[2 * t] = i;
-    if (i + 1 == m || tk[i + 1] != t) ranges[2 * t + 1] = i + 1;
   }
 }
 
@@ -164,8 +316,6 @@ __global__ void ranges_k(const uint32_t* __restrict__ tk, const RenderCounters* 
 // widened to FP64 and evaluates exp with a table-driven FP64 kernel (64-entry
 // double-double table, degree-5 polynomial: <= 0.82 ulp, tested against
 // libm on 2e7 points), the reference's arithmetic otherwise.
-constexpr int kMaxBands = 8;
-
 struct SplatF64 {
   double cx, cy, ca, cb2, cc, al, r, g, b;
   double skip;  // sigma below which alpha * exp(sigma) < 2^-36 (no effect on f32 T)
@@ -194,37 +344,6 @@ __device__ __forceinline__ double exp_tab(double x, const double2* __restrict__ 
   const double2 tj = tab[k & 63];
   const double v = __dadd_rn(tj.x, __fma_rn(tj.x, sr, tj.y));
   return __hiloint2double(__double2hiint(v) + ((k >> 6) << 20), __double2loint(v));
-}
-
-// Tile schedule: band-major (horizontal bands of tile rows, see
-// blend_bands), and within a band longest list first, bucketed by
-// floor(log2(list length)).  One CTA; the order only affects scheduling,
-// never results - tiles are independent.
-__global__ void __launch_bounds__(1024) tile_order_k(const uint32_t* __restrict__ ranges,
-                                                     int tiles_x, int tiles_y, int bands,
-                                                     uint32_t* __restrict__ order) {
-  __shared__ uint32_t hist[33 * kMaxBands];
-  __shared__ uint32_t base[33 * kMaxBands];
-  const uint32_t n_tiles = (uint32_t)tiles_x * tiles_y;
-  for (int i = threadIdx.x; i < 33 * kMaxBands; i += blockDim.x) hist[i] = 0;
-  __syncthreads();
-  auto key = [&](uint32_t t) -> int {
-    const uint32_t len = ranges[2 * t + 1] - ranges[2 * t];
-    // the band whose rows [blend_band_row(b), blend_band_row(b + 1)) hold t
-    const int band = (((int)(t / tiles_x) + 1) * bands - 1) / tiles_y;
-    return band * 33 + (len ? __clz(len) : 32);  // descending length within the band
-  };
-  for (uint32_t t = threadIdx.x; t < n_tiles; t += blockDim.x) atomicAdd(&hist[key(t)], 1u);
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    uint32_t run = 0;
-    for (int b = 0; b < 33 * bands; ++b) {
-      base[b] = run;
-      run += hist[b];
-    }
-  }
-  __syncthreads();
-  for (uint32_t t = threadIdx.x; t < n_tiles; t += blockDim.x) order[atomicAdd(&base[key(t)], 1u)] = t;
 }
 
 // Optional per-CTA timing trace for schedule studies (vms_debug_blend_trace):
@@ -511,29 +630,33 @@ int32_t tiles_and_blend(int width, int height, const uint32_t* vals, const Rende
   const int tiles_x = ceil_div(width, ts), tiles_y = ceil_div(height, ts);
   const uint32_t n_tiles = (uint32_t)tiles_x * tiles_y;
   const int T = 256;
-  dup_count_k<<<4 * kSMs, T, 0, s>>>(vals, w.rec, w.ctr, shift, w.cnt);
+  const int ab = bands < 0 ? -bands : bands;
+  const int nb = ab < 1 ? 1 : (ab > kMaxBands ? kMaxBands : ab);
+  if (tiles_x > 256 || tiles_y > 256) {
+    set_error("tiles_and_blend: more than 256 x 256 blend tiles");
+    return VMS_ERR_INVALID;
+  }
+  const int gx = tiles_x + 1, gy = tiles_y + 1;
+  VMS_CUDA(cudaMemsetAsync(w.tdiff, 0, sizeof(uint32_t) * gx * gy, s));
+  const size_t dsm = gx * gy <= kDiffSmemWords ? sizeof(uint32_t) * gx * gy : 0;
+  dup_count_k<<<2 * kSMs, T, dsm, s>>>(vals, w.rec, w.ctr, shift, gx, gy, w.cnt, w.rects, w.tdiff);
   mark("dup_count", s);
   int32_t st = scan_exclusive_u32(w.cnt, w.off, &w.ctr->n_kept, 0, w.n_cap, &w.ctr->n_inst,
                                   w.scan_ws, s);
   if (st) return st;
-  dup_emit_k<<<4 * kSMs, T, 0, s>>>(vals, w.rec, w.off, w.ctr, w.m_cap, tiles_x, shift, w.tk0,
-                                    w.tv0);
+  const RadixLayout rl = radix_layout(w.radix_ws, w.n_cap > w.m_cap ? w.n_cap : w.m_cap);
+  tile_prep_k<<<1, 1024, 0, s>>>(w.tdiff, tiles_x, tiles_y, nb, w.m_cap, w.ctr, w.tcount, w.ranges,
+                                  w.order, rl.counters, rl.ghist);
+  mark("tile_prep", s);
+  dup_emit_k<<<4 * kSMs, T, 0, s>>>(vals, w.rects, w.off, w.ctr, tiles_x, w.tk0, w.tv0, rl.status,
+                                    rl.pass_stride, rl.tile_items);
   mark("dup_emit", s);
-  clamp_inst_k<<<1, 1, 0, s>>>(w.ctr, w.m_cap);
-  mark("clamp", s);
   int alt = 0;
-  st = radix_sort_u32(w.tk0, w.tv0, w.tk1, w.tv1, &w.ctr->n_inst, 0, w.m_cap, 0, tile_bits(n_tiles), &alt,
-                      w.radix_ws, s);
+  st = radix_passes_u32(w.tk0, w.tv0, w.tk1, w.tv1, &w.ctr->n_inst,
+                        w.n_cap > w.m_cap ? w.n_cap : w.m_cap, 0, tile_bits(n_tiles), &alt,
+                        w.radix_ws, s);
   if (st) return st;
-  const uint32_t* tk = alt ? w.tk1 : w.tk0;
   const uint32_t* tv = alt ? w.tv1 : w.tv0;
-  VMS_CUDA(cudaMemsetAsync(w.ranges, 0, sizeof(uint32_t) * 2 * n_tiles, s));
-  ranges_k<<<8 * kSMs, T, 0, s>>>(tk, w.ctr, w.ranges);
-  mark("ranges", s);
-  const int ab = bands < 0 ? -bands : bands;
-  const int nb = ab < 1 ? 1 : (ab > kMaxBands ? kMaxBands : ab);
-  tile_order_k<<<1, 1024, 0, s>>>(w.ranges, tiles_x, tiles_y, nb, w.order);
-  mark("tile_order", s);
   record(events, 2, external, s);
   if (bands < 0) return VMS_OK;  // the caller launches the bands
   if (tv != sorted_tiles(w, n_tiles)) {
@@ -579,10 +702,12 @@ size_t render_ws_bytes(uint32_t n_cap, uint32_t m_cap, uint32_t n_tiles) {
   b += sizeof(BlendRec) * (size_t)n_cap;       // rec
   b += sizeof(uint32_t) * (size_t)n_cap * 6;   // k0 v0 k1 v1 cnt off
   b += sizeof(uint32_t) * (size_t)m_cap * 4;   // tk0 tv0 tk1 tv1
+  b += sizeof(uint32_t) * (size_t)n_cap;      // rects
+  b += sizeof(uint32_t) * (4 * (size_t)n_tiles + 2);  // tcount + tdiff
   b += sizeof(uint32_t) * 3 * (size_t)n_tiles; // ranges + order
   b += sizeof(RenderCounters) + sizeof(FrameDev);
   b += scan_ws_bytes(n_cap) + radix_ws_bytes(n_cap > m_cap ? n_cap : m_cap);
-  return b + 256 * 20;
+  return b + 256 * 24;
 }
 
 RenderWs render_carve(void* ws, uint32_t n_cap, uint32_t m_cap, uint32_t n_tiles) {
@@ -604,6 +729,9 @@ RenderWs render_carve(void* ws, uint32_t n_cap, uint32_t m_cap, uint32_t n_tiles
   w.tv0 = carve<uint32_t>(p, m_cap);
   w.tk1 = carve<uint32_t>(p, m_cap);
   w.tv1 = carve<uint32_t>(p, m_cap);
+  w.rects = carve<uint32_t>(p, n_cap);
+  w.tcount = carve<uint32_t>(p, n_tiles);
+  w.tdiff = carve<uint32_t>(p, 2 * (size_t)n_tiles + 2);  // >= (tx + 1)(ty + 1)
   w.ranges = carve<uint32_t>(p, 2 * (size_t)n_tiles);
   w.order = carve<uint32_t>(p, (size_t)n_tiles);
   w.ctr = carve<RenderCounters>(p, 1);

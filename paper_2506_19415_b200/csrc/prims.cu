@@ -11,6 +11,8 @@
 // Warps cover consecutive sub-tiles, so (warp, item, lane) order equals
 // input order.  Each tile is re-ordered in shared memory by digit before the
 // scatter so the global writes of one digit run are coalesced.
+#include <algorithm>
+
 #include "common.cuh"
 #include "prims.h"
 
@@ -78,16 +80,33 @@ __device__ __forceinline__ void st_status(uint32_t* p, uint32_t v) {
   *reinterpret_cast<volatile uint32_t*>(p) = v;
 }
 
-// exclusive prefix of tile t from the statuses of tiles t-1, t-2, ...
+// Exclusive prefix of tile t from the statuses of tiles t-1, t-2, ...,
+// read kWindow predecessors at a time (independent loads in flight instead
+// of one L2 round trip per predecessor); a window is consumed up to the first
+// inclusive prefix, or up to the first predecessor that has not published
+// yet, which is then re-read.
+constexpr int kWindow = 8;
+
 __device__ __forceinline__ uint32_t look_back(const uint32_t* status, uint32_t t, uint32_t stride) {
   uint32_t excl = 0;
-  for (int64_t j = (int64_t)t - 1; j >= 0; --j) {
-    uint32_t v;
-    do {
-      v = ld_status(status + (size_t)j * stride);
-    } while ((v & ~kValMask) == 0u);
-    excl += v & kValMask;
-    if (v & kFlagP) break;
+  int64_t j = (int64_t)t - 1;
+  while (j >= 0) {
+    uint32_t v[kWindow];
+#pragma unroll
+    for (int k = 0; k < kWindow; ++k)
+      v[k] = j - k >= 0 ? ld_status(status + (size_t)(j - k) * stride) : kFlagP;
+    int used = 0;
+    bool found = false;
+#pragma unroll
+    for (int k = 0; k < kWindow; ++k) {
+      if (found || used < k) continue;  // stop at the first gap or prefix
+      if ((v[k] & ~kValMask) == 0u) continue;
+      excl += v[k] & kValMask;
+      ++used;
+      if (v[k] & kFlagP) found = true;
+    }
+    if (found) break;
+    j -= used;
   }
   return excl;
 }
@@ -341,6 +360,45 @@ size_t radix_ws_bytes(uint32_t n_max) {
   return sizeof(uint32_t) * (64 + 4 * 256 + 4 * 256 * tiles) + 256;
 }
 
+RadixLayout radix_layout(void* ws, uint32_t n_max) {
+  RadixLayout l;
+  l.counters = static_cast<uint32_t*>(ws);
+  l.ghist = l.counters + 64;
+  l.status = l.ghist + 4 * 256;
+  l.pass_stride = 256 * (((size_t)n_max + kRTile - 1) / kRTile);
+  l.tile_items = kRTile;
+  return l;
+}
+
+int32_t radix_passes_u32(uint32_t* k0, uint32_t* v0, uint32_t* k1, uint32_t* v1,
+                         const uint32_t* n_dev, uint32_t n_max, int begin_bit, int end_bit,
+                         int* in_alt, void* ws, cudaStream_t s) {
+  const int passes = (end_bit - begin_bit + 7) / 8;
+  if (passes > 4) {
+    set_error("radix_passes_u32: at most 32 key bits");
+    return VMS_ERR_INVALID;
+  }
+  const RadixLayout l = radix_layout(ws, n_max);
+  const size_t tiles = l.pass_stride / 256;
+  const int grid = persistent_grid((const void*)radix_onesweep_k, kRBlock, tiles ? (int)tiles : 1);
+  int alt = 0;
+  for (int p = 0; p < passes; ++p) {
+    const int b = begin_bit + 8 * p;
+    const int bits = end_bit - b < 8 ? end_bit - b : 8;
+    const uint32_t mask = (1u << bits) - 1u;
+    uint32_t *ki = alt ? k1 : k0, *vi = alt ? v1 : v0;
+    uint32_t *ko = alt ? k0 : k1, *vo = alt ? v0 : v1;
+    radix_onesweep_k<<<grid, kRBlock, 0, s>>>(ki, vi, ko, vo, n_dev, 0, b, mask,
+                                              l.ghist + p * 256, l.status + p * l.pass_stride,
+                                              l.counters + p);
+    mark("radix_pass", s);
+    alt ^= 1;
+  }
+  VMS_LAUNCH_CHECK("radix_passes_u32");
+  *in_alt = alt;
+  return VMS_OK;
+}
+
 int32_t radix_sort_u32(uint32_t* k0, uint32_t* v0, uint32_t* k1, uint32_t* v1,
                        const uint32_t* n_dev, uint32_t n_host, uint32_t n_max, int begin_bit,
                        int end_bit, int* in_alt, void* ws, cudaStream_t s) {
@@ -354,7 +412,9 @@ int32_t radix_sort_u32(uint32_t* k0, uint32_t* v0, uint32_t* k1, uint32_t* v1,
   uint32_t* ghist = counters + 64;                  // [passes][256]
   uint32_t* status = ghist + 4 * 256;               // [passes][tiles][256]
   VMS_CUDA(cudaMemsetAsync(ws, 0, sizeof(uint32_t) * (64 + 4 * 256), s));
-  const int hgrid = persistent_grid((const void*)radix_hist_k, kRBlock, 0);
+  // a few CTAs per SM: each flushes 4 x 256 bins with global atomics
+  const int hgrid = persistent_grid((const void*)radix_hist_k, kRBlock,
+                                    (int)std::min<size_t>(2 * 148, (n_max + 4095) / 4096 + 1));
   radix_hist_k<<<hgrid, kRBlock, 0, s>>>(k0, n_dev, n_host, begin_bit, end_bit, ghist, status,
                                          256 * tiles);
   mark("radix_hist", s);

@@ -25,4 +25,20 @@ int32_t radix_sort_u32(uint32_t* k0, uint32_t* v0, uint32_t* k1, uint32_t* v1,
                        const uint32_t* n_dev, uint32_t n_host, uint32_t n_max, int begin_bit,
                        int end_bit, int* in_alt, void* ws, cudaStream_t s);
 
+// The same sort for callers that produce the digit histograms themselves
+// (e.g. from per-bin counts they already have).  Before the call: counters
+// zero, ghist[p][d] = count of digit d in pass p, and for every pass the
+// first ceil(n / tile_items) * 256 status words zero.  n comes from n_dev.
+struct RadixLayout {
+  uint32_t* counters;  // [64]
+  uint32_t* ghist;     // [4][256]
+  uint32_t* status;    // [pass][pass_stride]
+  size_t pass_stride;
+  uint32_t tile_items;
+};
+RadixLayout radix_layout(void* ws, uint32_t n_max);
+int32_t radix_passes_u32(uint32_t* k0, uint32_t* v0, uint32_t* k1, uint32_t* v1,
+                         const uint32_t* n_dev, uint32_t n_max, int begin_bit, int end_bit,
+                         int* in_alt, void* ws, cudaStream_t s);
+
 }  // namespace vms

@@ -65,6 +65,9 @@ struct RenderWs {
   uint32_t *k0, *v0, *k1, *v1;
   uint32_t *cnt, *off;
   uint32_t *tk0, *tv0, *tk1, *tv1;
+  uint32_t* rects;   // packed tile rectangle per sorted splat
+  uint32_t* tcount;  // instances per tile
+  uint32_t* tdiff;   // 2D difference array of tcount ((tiles_x + 1) x (tiles_y + 1))
   uint32_t* ranges;  // 2 per tile
   uint32_t* order;   // blend schedule: tiles, longest list first
   RenderCounters* ctr;
