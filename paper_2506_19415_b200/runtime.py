@@ -471,8 +471,7 @@ class VmSession:
         lib = self._lib
         h0 = time.perf_counter()
         a = self._args
-        a.cam = camera.struct(self.dot_mode)
-        a.vis_cam = camera.scaled(self.vis_scale).struct(self.dot_mode)
+        fill_frame_cameras(a, camera, self.vis_scale, self.dot_mode)
         thr = self.controller.thresholds
         if thr.size > 8:
             raise InvariantViolation("at most 9 LOD levels are supported")
@@ -598,6 +597,32 @@ class VmSession:
         self._images = (key, bufs, i ^ 1)
         return bufs[i]
 
+
+
+def fill_frame_cameras(args, camera, vis_scale: float, dot_mode: int) -> None:
+    """args.cam / args.vis_cam = camera.struct(), camera.scaled(vis_scale)
+    .struct() - the same numbers (quat_to_matrix's elementwise FP64
+    arithmetic in the same order, the same focal and rounding), without
+    building NumPy arrays and a second validated Camera each frame."""
+    w, x, y, z = (float(v) for v in camera.orientation)
+    rot = (1 - 2 * (y * y + z * z), 2 * (x * y - w * z), 2 * (x * z + w * y),
+           2 * (x * y + w * z), 1 - 2 * (x * x + z * z), 2 * (y * z - w * x),
+           2 * (x * z - w * y), 2 * (y * z + w * x), 1 - 2 * (x * x + y * y))
+    pos = [float(v) for v in camera.position]
+    t = float(np.tan(camera.fov_y / 2.0))
+    vw = max(1, int(round(camera.width * vis_scale)))
+    vh = max(1, int(round(camera.height * vis_scale)))
+    for c, wd, ht in ((args.cam, camera.width, camera.height), (args.vis_cam, vw, vh)):
+        c.pos[0], c.pos[1], c.pos[2] = pos
+        for i in range(9):
+            c.rot[i] = rot[i]
+        c.focal = (ht / 2.0) / t
+        c.half_w = wd / 2.0
+        c.half_h = ht / 2.0
+        c.near = float(camera.near)
+        c.width = int(wd)
+        c.height = int(ht)
+        c.dot_mode = int(dot_mode)
 
 
 def _pinned_records(scene):

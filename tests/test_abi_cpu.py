@@ -156,3 +156,25 @@ def test_same_level_packing_and_transition():
 def test_table_capacity_validated():
     with pytest.raises(InvariantViolation):
         PageTable(0)
+
+
+def test_frame_camera_fill_matches_struct():
+    """The per-frame fast camera fill equals Camera.struct() and
+    Camera.scaled(s).struct() field for field (bit-exact doubles)."""
+    import numpy as np
+
+    from paper_2506_19415_b200 import _lib, scenegen
+    from paper_2506_19415_b200.runtime import fill_frame_cameras
+
+    traj = scenegen.street_path(scenegen.C2, frames=120)
+    fields = ("focal", "half_w", "half_h", "near", "width", "height", "dot_mode")
+    for f in range(0, 120, 7):
+        cam = traj.frame_camera(f)
+        for scale in (0.25, 0.5, 1.0 / 3.0):
+            a = _lib.FrameArgs()
+            fill_frame_cameras(a, cam, scale, 1)
+            for got, ref in ((a.cam, cam.struct(1)), (a.vis_cam, cam.scaled(scale).struct(1))):
+                assert np.array_equal(np.array(got.pos[:]), np.array(ref.pos[:]))
+                assert np.array(got.rot[:]).tobytes() == np.array(ref.rot[:]).tobytes()
+                for k in fields:
+                    assert getattr(got, k) == getattr(ref, k), (f, scale, k)
