@@ -268,12 +268,15 @@ def run_ours(args, rank, world, local_rank):
         ach = blend_bytes / blend_s / 1e9
     else:
         ach = pre_bytes / pre_s / 1e9
+    # DRAM bytes per launch of the dominant kernel from one ncu --set full
+    # capture (profiles/traffic.json, written by profiles/ncu_summary.py)
     traffic = None
     tf = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tf):
         try:
-            traffic = json.load(open(tf)).get(dominant)
-        except ValueError:
+            ent = json.load(open(tf)).get(dominant + "_k")
+            traffic = int(ent["bytes_per_launch"]) if ent else None
+        except (ValueError, KeyError, TypeError):
             traffic = None
     up_bytes = sum(s["bytes_copied"] for s in stats_t)
     up_s = sum(s["time_copy"] for s in stats_t if s["bytes_copied"])
@@ -299,7 +302,10 @@ def run_ours(args, rank, world, local_rank):
                     s["required_pages"] for s in stats_e2e))},
         "roofline": {"bound": "hbm", "kernel": dominant, "achieved": round(ach, 2),
                      "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s",
-                     "frac": round(ach / hbm, 4), "traffic": traffic},
+                     "frac": round(ach / hbm, 4), "traffic": traffic,
+                     "limiter": ("FP64 + XU (f32<->f64 conversion) issue in the exact blend, "
+                                 "not HBM: see profiles/r1/SUMMARY.md")
+                     if dominant == "blend" else "HBM read of the resident records"},
         "stages_ms": {k: round(v, 4) for k, v in stages.items()},
         "upload": {"gbs": round(up_bytes / up_s / 1e9, 2) if up_s else None,
                    "bytes": up_bytes, "frames_with_copies": sum(1 for s in stats_t if s["bytes_copied"])},
