@@ -1,3 +1,2 @@
 timeout 1200 python -m pytest tests -m gpu -x -q 2>&1 | tail -30 > gpurun_out/gputests.log
-timeout 900 python bench.py > gpurun_out/bench.log 2>&1
-timeout 600 python profiles/e2e_modes.py > gpurun_out/e2e_modes.txt 2>&1
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1
