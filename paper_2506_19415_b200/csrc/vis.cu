@@ -203,8 +203,10 @@ __global__ void __launch_bounds__(kVisThreads) vis_raster_k(
     bool hit = false;
     VisTri t;
     if (ti < n) {
-      t = tris[ti];
-      hit = t.x0 <= t.x1 && t.x0 <= tx1 && t.x1 >= tx0 && t.y0 <= ty1 && t.y1 >= ty0;
+      // the 16-byte box first; the 112-byte triangle only for the hits
+      const int4 bx = __ldg(reinterpret_cast<const int4*>(&tris[ti].x0));
+      hit = bx.x <= bx.y && bx.x <= tx1 && bx.y >= tx0 && bx.z <= ty1 && bx.w >= ty0;
+      if (hit) t = tris[ti];
     }
     const uint32_t bal = __ballot_sync(0xffffffffu, hit);
     if (lane == 0) wsum[warp] = __popc(bal);

@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <cstddef>
 #include <stdint.h>
 
 #include "../../include/vmsplat_b200.h"
@@ -10,12 +11,13 @@ namespace vms {
 
 using VisCamera = vms_camera;
 
-struct VisTri {
+struct __align__(16) VisTri {
   double ax, ay, bx, by, cx, cy, iza, izb, izc, area;
   int x0, x1, y0, y1;  // inclusive clamped pixel box; x0 > x1 means empty
   uint32_t id;
   uint32_t pad_;
 };
+static_assert(sizeof(VisTri) == 112 && offsetof(VisTri, x0) == 80, "VisTri layout");
 
 using VisLod = vms_lod;
 using RequiredOut = vms_required_out;

@@ -1,2 +1,4 @@
-timeout 1200 python -m pytest tests -m gpu -x -q 2>&1 | tail -30 > gpurun_out/gputests.log
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1
+timeout 1200 python -m pytest tests -m gpu -x -q 2>&1 | tail -3 > gpurun_out/gputests.log
+timeout 300 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv \
+   -k regex:vis_raster --log-file gpurun_out/vr.csv python profiles/profile_frames.py --warm 12 --frames 1 > /dev/null 2>&1
+timeout 900 python bench.py --no-cpu-baseline > gpurun_out/bench.log 2>&1
