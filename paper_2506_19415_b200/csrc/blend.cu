@@ -134,27 +134,38 @@ __global__ void __launch_bounds__(1024) tile_prep_k(
   __shared__ uint32_t scratch[33];
   __shared__ uint32_t hist[33 * kMaxBands];
   __shared__ uint32_t base[33 * kMaxBands];
-  const int gx = tiles_x + 1;
+  extern __shared__ uint32_t sgrid[];  // the difference array, when it fits
+  const int gx = tiles_x + 1, gy = tiles_y + 1;
   const uint32_t n_tiles = (uint32_t)tiles_x * tiles_y;
+  const bool in_smem = gx * gy <= kDiffSmemWords;
   for (int i = threadIdx.x; i < 512; i += blockDim.x) (&h[0][0])[i] = 0u;
   for (int i = threadIdx.x; i < 33 * kMaxBands; i += blockDim.x) hist[i] = 0u;
   if (threadIdx.x < 64) rcounters[threadIdx.x] = 0u;
-  // rows: running sums along x; then columns: running sums along y
+  // integrate the difference array (rows, then columns) in shared memory
+  // (global memory for tile grids too large for it), then publish tcount
+  uint32_t* g = in_smem ? sgrid : const_cast<uint32_t*>(tdiff);
+  if (in_smem) {
+    for (int i = threadIdx.x; i < gx * gy; i += blockDim.x) sgrid[i] = tdiff[i];
+    __syncthreads();
+  }
   for (int y = threadIdx.x; y < tiles_y; y += blockDim.x) {
     uint32_t run = 0;
     for (int x = 0; x < tiles_x; ++x) {
-      run += tdiff[y * gx + x];
-      tcount[y * tiles_x + x] = run;
+      run += g[y * gx + x];
+      g[y * gx + x] = run;
     }
   }
   __syncthreads();
   for (int x = threadIdx.x; x < tiles_x; x += blockDim.x) {
     uint32_t run = 0;
     for (int y = 0; y < tiles_y; ++y) {
-      run += tcount[y * tiles_x + x];
-      tcount[y * tiles_x + x] = run;
+      run += g[y * gx + x];
+      g[y * gx + x] = run;
     }
   }
+  __syncthreads();
+  for (uint32_t t = threadIdx.x; t < n_tiles; t += blockDim.x)
+    tcount[t] = g[(t / tiles_x) * gx + t % tiles_x];
   __syncthreads();
   // exclusive scan over tiles -> ranges; each thread a contiguous run
   const uint32_t per = (n_tiles + blockDim.x - 1) / blockDim.x;
@@ -645,8 +656,8 @@ int32_t tiles_and_blend(int width, int height, const uint32_t* vals, const Rende
                                   w.scan_ws, s);
   if (st) return st;
   const RadixLayout rl = radix_layout(w.radix_ws, w.n_cap > w.m_cap ? w.n_cap : w.m_cap);
-  tile_prep_k<<<1, 1024, 0, s>>>(w.tdiff, tiles_x, tiles_y, nb, w.m_cap, w.ctr, w.tcount, w.ranges,
-                                  w.order, rl.counters, rl.ghist);
+  tile_prep_k<<<1, 1024, dsm, s>>>(w.tdiff, tiles_x, tiles_y, nb, w.m_cap, w.ctr, w.tcount,
+                                    w.ranges, w.order, rl.counters, rl.ghist);
   mark("tile_prep", s);
   dup_emit_k<<<4 * kSMs, T, 0, s>>>(vals, w.rects, w.off, w.ctr, tiles_x, w.tk0, w.tv0, rl.status,
                                     rl.pass_stride, rl.tile_items);
@@ -686,6 +697,9 @@ int32_t blend_init() {
     t[j].y = (double)(v - (long double)t[j].x);
   }
   VMS_CUDA(cudaMemcpyToSymbol(kExp2Tab, t, sizeof(t)));
+  VMS_CUDA(cudaFuncSetAttribute((const void*)tile_prep_k,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)(sizeof(uint32_t) * kDiffSmemWords)));
   done = true;
   return VMS_OK;
 }
