@@ -454,3 +454,27 @@ def test_output_modes_identical(cuda):
         else:
             img, _ = b.render_frame(cam, f, out=pageable)
         assert np.array_equal(img, ref), (f, mode)
+
+
+def test_4k_frames_match_oracle(cuda):
+    """BASELINE config 5's resolution (3840x2160, 120x68 blend tiles, vis
+    960x540) with every SH coefficient non-zero: stats identical to the
+    oracle, images within the exact-blend tolerance."""
+    from paper_2506_19415_b200 import scenegen
+    from paper_2506_19415_b200.runtime import VmSession
+
+    lay = scenegen.CityLayout(n_pages=40, page_size=256, levels=3, seed=5, scale=0.12)
+    sc = scenegen.city_scene(lay)
+    assert np.count_nonzero(np.asarray(sc.gaussians)[:, 11:]) == np.asarray(sc.gaussians)[:, 11:].size
+    path = scenegen.street_path(lay, frames=16, width=3840, height=2160)
+    s = VmSession(sc, buffer_pages=16, staging_pages=6.0, vis_scale=0.25)
+    o = core.OSession(sc, buffer_pages=16, staging_pages=6.0, vis_scale=0.25)
+    for f in range(3):
+        cam = path.frame_camera(f)
+        img, st = s.render_frame(cam, f)
+        ref, rst = o.render_frame(cam, f)
+        for k in ("required_pages", "resident_pages", "missing_pages", "bytes_copied",
+                  "resident_per_level", "thresholds"):
+            assert st[k] == rst[k], (f, k)
+        assert float(ref.max()) > 0.0
+        assert _maxabs(img, ref) <= EXACT_TOL, f
