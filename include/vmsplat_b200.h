@@ -261,7 +261,9 @@ int64_t vms_pt_chunks(const vms_pagetable* pt, int64_t page_size, vms_chunk* out
 typedef struct vms_session vms_session;
 
 typedef struct vms_session_desc {
-  const float* host_records;    /* [dev-mapped pinned] the GAUS section, all levels */
+  const float* host_records;    /* the GAUS section, all levels: [dev-mapped pinned] for
+                                   upload_mode 0/1; any host memory (e.g. the mmap of the
+                                   .vms file) for upload_mode 2 */
   uint64_t host_rows;
   uint32_t page_size;
   uint32_t lod_levels;          /* levels stored in the scene */
@@ -282,7 +284,9 @@ typedef struct vms_session_desc {
   int32_t width;                /* render resolution render_ws is sized for */
   int32_t height;
   int32_t exact;                /* 1: FP64 blend */
-  int32_t upload_mode;          /* see vms_upload_pages */
+  int32_t upload_mode;          /* 0/1: see vms_upload_pages; 2: streaming - planned rows are
+                                   gathered by host threads into a page-locked bounce buffer,
+                                   one cudaMemcpyAsync per frame */
 } vms_session_desc;
 
 typedef struct vms_frame_args {

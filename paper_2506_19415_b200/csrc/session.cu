@@ -25,7 +25,12 @@
 // when it recycles that frame's buffers and grows the buffer (re-capturing
 // the graph) for the frames after it.
 #include <algorithm>
+#include <atomic>
 #include <chrono>
+#include <condition_variable>
+#include <mutex>
+#include <thread>
+#include <tuple>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -37,6 +42,72 @@
 
 namespace {
 constexpr int kBands = 4;  // blend launches / image copy pieces for host output
+
+// Streaming source (upload_mode 2): planned page rows are gathered from
+// ordinary host memory (e.g. the memory-mapped .vms file, which need not fit
+// in page-locked memory) into a page-locked bounce buffer by a few host
+// threads, then cross PCIe as one copy.
+class CopyPool {
+ public:
+  explicit CopyPool(int n) {
+    for (int i = 0; i < n; ++i) workers_.emplace_back([this, i] { run(i); });
+  }
+  ~CopyPool() {
+    {
+      std::lock_guard<std::mutex> g(m_);
+      stop_ = true;
+      ++gen_;
+    }
+    cv_.notify_all();
+    for (auto& t : workers_) t.join();
+  }
+  // Copy every piece (dst, src, bytes) and return when all are done.
+  void copy(const std::vector<std::tuple<char*, const char*, size_t>>& pieces) {
+    if (pieces.empty()) return;
+    {
+      std::lock_guard<std::mutex> g(m_);
+      job_ = &pieces;
+      next_ = 0;
+      pending_ = (int)workers_.size();
+      ++gen_;
+    }
+    cv_.notify_all();
+    std::unique_lock<std::mutex> lk(m_);
+    done_cv_.wait(lk, [this] { return pending_ == 0; });
+    job_ = nullptr;
+  }
+
+ private:
+  void run(int) {
+    uint64_t seen = 0;
+    for (;;) {
+      const std::vector<std::tuple<char*, const char*, size_t>>* job;
+      {
+        std::unique_lock<std::mutex> lk(m_);
+        cv_.wait(lk, [&] { return gen_ != seen; });
+        seen = gen_;
+        if (stop_) return;
+        job = job_;
+      }
+      for (;;) {
+        const size_t i = next_.fetch_add(1);
+        if (i >= job->size()) break;
+        const auto& pc = (*job)[i];
+        std::memcpy(std::get<0>(pc), std::get<1>(pc), std::get<2>(pc));
+      }
+      std::lock_guard<std::mutex> g(m_);
+      if (--pending_ == 0) done_cv_.notify_one();
+    }
+  }
+  std::vector<std::thread> workers_;
+  std::mutex m_;
+  std::condition_variable cv_, done_cv_;
+  const std::vector<std::tuple<char*, const char*, size_t>>* job_ = nullptr;
+  std::atomic<size_t> next_{0};
+  int pending_ = 0;
+  uint64_t gen_ = 0;
+  bool stop_ = false;
+};
 }
 
 namespace {
@@ -86,6 +157,11 @@ struct vms_session {
   int ws_w = 0, ws_h = 0;
   char* staging = nullptr;
   size_t staging_bytes = 0;
+  // upload_mode 2 (streaming source): page-locked bounce buffers per parity
+  char* bounce[2] = {nullptr, nullptr};
+  size_t bounce_bytes[2] = {0, 0};
+  CopyPool* pool = nullptr;
+  std::vector<std::tuple<char*, const char*, size_t>> pieces;
   int64_t max_chunks = 0;
   int parity = 0;
   bool use_graphs = true;
@@ -123,6 +199,9 @@ void free_session(vms_session* s) {
     if (p) cudaFreeHost(p);
   for (void* p : {(void*)s->scatter_d, (void*)s->chunks_d, s->ws, (void*)s->staging})
     if (p) cudaFree(p);
+  for (char* p : s->bounce)
+    if (p) cudaFreeHost(p);
+  delete s->pool;
   delete s;
 }
 
@@ -365,6 +444,10 @@ vms_session* vms_session_create(const vms_session_desc* desc) {
     free_session(s);
     return nullptr;
   }
+  if (desc->upload_mode == 2) {
+    const unsigned hw = std::thread::hardware_concurrency();
+    s->pool = new CopyPool((int)std::max(1u, std::min(8u, hw ? hw / 2 : 4u)));
+  }
   s->plan_pid.resize(P + 1);
   s->plan_level.resize(P + 1);
   s->plan_entry.resize(P + 1);
@@ -476,9 +559,35 @@ int32_t vms_session_frame(vms_session* s, const vms_frame_args* a, vms_frame_sta
     if (rc) return rc;
     VMS_CUDA(cudaStreamWaitEvent(s->copy_stream, s->ev_staging, 0));  // staging reuse
     if (timing) VMS_CUDA(cudaEventRecord(s->tev[2], s->copy_stream));
-    rc = vms_upload_pages(s->copies[par], n_plan, s->d.host_records, s->staging, s->d.upload_mode,
-                          s->copy_stream);
-    if (rc) return rc;
+    if (s->d.upload_mode == 2) {
+      // gather the planned rows into page-locked memory on host threads, then
+      // one PCIe copy (the bounce buffer of this parity was released when the
+      // frame two back was recycled)
+      if (s->bounce_bytes[par] < bytes) {
+        if (s->bounce[par]) VMS_CUDA(cudaFreeHost(s->bounce[par]));
+        s->bounce[par] = nullptr;
+        const size_t want = bytes + bytes / 4;
+        VMS_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&s->bounce[par]), want,
+                               cudaHostAllocPortable));
+        s->bounce_bytes[par] = want;
+      }
+      s->pieces.clear();
+      const char* src = reinterpret_cast<const char*>(s->d.host_records);
+      constexpr size_t kPiece = 1u << 20;
+      for (int64_t i = 0; i < n_plan; ++i) {
+        const vms_copy& c = s->copies[par][i];
+        for (size_t o = 0; o < c.nbytes; o += kPiece)
+          s->pieces.emplace_back(s->bounce[par] + c.dst_offset + o, src + c.src_offset + o,
+                                 std::min<size_t>(kPiece, c.nbytes - o));
+      }
+      s->pool->copy(s->pieces);
+      VMS_CUDA(cudaMemcpyAsync(s->staging, s->bounce[par], bytes, cudaMemcpyHostToDevice,
+                               s->copy_stream));
+    } else {
+      rc = vms_upload_pages(s->copies[par], n_plan, s->d.host_records, s->staging,
+                            s->d.upload_mode, s->copy_stream);
+      if (rc) return rc;
+    }
     if (timing) VMS_CUDA(cudaEventRecord(s->tev[3], s->copy_stream));
     VMS_CUDA(cudaMemcpyAsync(s->scatter_d, s->scatter_h[par], sizeof(vms_copy) * n_plan,
                              cudaMemcpyHostToDevice, s->copy_stream));

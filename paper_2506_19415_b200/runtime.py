@@ -351,7 +351,10 @@ class VmSession:
     Extra (non-reference) knobs: ``exact`` (default) blends with the
     reference's FP64 arithmetic, False selects the FP32 blend;
     ``upload_mode`` 1 uploads a frame's pages with one gather kernel over
-    mapped pinned memory, 0 with one cudaMemcpyAsync per page; ``timing``
+    mapped pinned memory, 0 with one cudaMemcpyAsync per page, 2 streams them
+    from the scene's memory-mapped rows (host threads gather each frame's
+    pages into a page-locked bounce buffer; for scenes larger than the
+    page-locked memory one wants to commit - out-of-core); ``timing``
     records per-stage CUDA events (the stats' time_* keys; costs one sync per
     frame); ``device`` selects the GPU.
     """
@@ -403,9 +406,17 @@ class VmSession:
                                          scene.page_count, off, tgt)
             self.n_cap = self.capacity * self.page_size
             self.pool = t.empty((self.n_cap, RECORD_SIZE), dtype=t.float32, device=self.device)
-            self.host = _pinned_records(scene)  # the streaming source (pinned, mapped)
+            if self.upload_mode == 2:
+                # streaming source: the scene's own (memory-mapped) rows; the
+                # session gathers each frame's pages through a page-locked
+                # bounce buffer, so the scene need not fit in pinned memory
+                self.host = np.ascontiguousarray(scene.gaussians, dtype=np.float32)
+                host_ptr = self.host.ctypes.data
+            else:
+                self.host = _pinned_records(scene)  # pinned, mapped into the device
+                host_ptr = self.host.data_ptr()
             d = _lib.SessionDesc()
-            d.host_records = self.host.data_ptr()
+            d.host_records = host_ptr
             d.host_rows = int(len(scene.gaussians))
             d.page_size = self.page_size
             d.lod_levels = int(scene.lod_levels)

@@ -281,7 +281,7 @@ def test_session_matches_reference(cuda, golden, variant, exact):
     assert core.stats_csv(stats).encode() == g[f"{variant}_stats"].tobytes()
 
 
-@pytest.mark.parametrize("upload_mode", [0, 1])
+@pytest.mark.parametrize("upload_mode", [0, 1, 2])
 def test_c1_session_matches_reference(cuda, golden, upload_mode):
     """BASELINE config 1 (reference-preprocessed box scene, 8 frames, 256^2,
     default knobs): stats.csv identical, images within tolerance of the
@@ -478,3 +478,25 @@ def test_4k_frames_match_oracle(cuda):
             assert st[k] == rst[k], (f, k)
         assert float(ref.max()) > 0.0
         assert _maxabs(img, ref) <= EXACT_TOL, f
+
+
+def test_c2_streamed_pages_render_identically(cuda, c2_scene):
+    """Out-of-core source (upload_mode 2: pages gathered from the memory-mapped
+    scene through a page-locked bounce buffer) gives the same frames and
+    stats as the pinned, device-mapped source - over the first 24 frames of
+    the benchmark path, which stream ~20 MB of pages per frame early on."""
+    from paper_2506_19415_b200 import scenegen
+    from paper_2506_19415_b200.runtime import VmSession
+
+    traj = scenegen.street_path(scenegen.C2, frames=120)
+    a = VmSession(c2_scene, upload_mode=1, timing=False)
+    b = VmSession(c2_scene, upload_mode=2, timing=False)
+    copied = 0
+    for f in range(24):
+        cam = traj.frame_camera(f)
+        ia, sa = a.render_frame(cam, f)
+        ib, sb = b.render_frame(cam, f)
+        assert sa["bytes_copied"] == sb["bytes_copied"] and sa["resident_pages"] == sb["resident_pages"]
+        copied += sb["bytes_copied"]
+        assert np.array_equal(ia, ib), f
+    assert copied > 100 << 20
