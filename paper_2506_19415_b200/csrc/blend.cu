@@ -690,6 +690,10 @@ int32_t tiles_and_blend(int width, int height, const uint32_t* vals, const Rende
 int32_t blend_init() {
   static bool done = false;
   if (done) return VMS_OK;
+  {
+    const int32_t rc = preprocess_init();
+    if (rc) return rc;
+  }
   double2 t[64];
   for (int j = 0; j < 64; ++j) {
     const long double v = exp2l((long double)j / 64.0L);

@@ -8,6 +8,8 @@
 // rows (59 f32 = 236 B each) are staged into shared memory with coalesced
 // 16-byte loads; record stride 59 words is odd, so the per-thread column
 // reads that follow are bank-conflict free.
+#include <algorithm>
+
 #include "common.cuh"
 #include "render.h"
 
@@ -166,52 +168,123 @@ __device__ __forceinline__ void project_one(const float* r, const RenderCamera& 
   sh_rgb(r + 11, d0 / dv, d1 / dv, d2 / dv, o.col);
 }
 
+// Bulk async copy (TMA engine, 1D) + mbarrier helpers.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+constexpr int kPreStages = 2;
+constexpr uint32_t kChunkFloats = kChunkRecords * kRecordFloats;
+
+// Persistent CTAs walk the chunk table (chunk c, c + grid, ...).  Each
+// chunk's rows (<= 128 x 236 B, contiguous in the pool) are brought into
+// shared memory by one bulk async copy (TMA) while the previous chunk is
+// projected, double-buffered on two mbarriers; the per-thread column reads
+// of the 59-word records (odd stride) are bank-conflict free.  Chunks whose
+// bytes are not 16-byte aligned fall back to plain loads (not the case for
+// power-of-two page sizes).
 __global__ void __launch_bounds__(kChunkRecords) preprocess_k(
     const float* __restrict__ pool, const Chunk* __restrict__ chunks,
     const FrameDev* __restrict__ fd, uint32_t* __restrict__ key_g, uint32_t* __restrict__ flag,
     BlendRec* __restrict__ rec) {
-  __shared__ __align__(16) float srec[kChunkRecords * kRecordFloats];
+  extern __shared__ __align__(128) float sbuf[];  // kPreStages x kChunkFloats
+  __shared__ __align__(8) uint64_t bar[kPreStages];
+  __shared__ Chunk s_chunk[kPreStages];
+  __shared__ int s_tma[kPreStages];
   __shared__ RenderCamera cam;
-  if (blockIdx.x >= fd->n_chunks) return;  // grid sized for the largest table
-  if (threadIdx.x == 0) cam = fd->cam;
-  const Chunk ch = chunks[blockIdx.x];
-  const float* src = pool + (size_t)ch.row * kRecordFloats;
-  const uint32_t nf = ch.count * kRecordFloats;
-  if ((ch.row & 3u) == 0 && (ch.count & 3u) == 0) {
-    const float4* s4 = reinterpret_cast<const float4*>(src);
-    float4* d4 = reinterpret_cast<float4*>(srec);
-    for (uint32_t i = threadIdx.x; i < nf / 4; i += blockDim.x) d4[i] = __ldg(s4 + i);
-  } else {
-    for (uint32_t i = threadIdx.x; i < nf; i += blockDim.x) srec[i] = __ldg(src + i);
+  const uint32_t n = fd->n_chunks;
+  if (blockIdx.x >= n) return;
+  const uint32_t t = threadIdx.x;
+  if (t == 0) {
+    cam = fd->cam;
+    for (int k = 0; k < kPreStages; ++k) mbar_init(&bar[k], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  const uint32_t t = threadIdx.x;
-  if (t >= ch.count) return;
-  const uint32_t g = ch.gather + t;
-  const float* r = srec + t * kRecordFloats;
-  Proj p;
-  project_one(r, cam, p, true);
-  if (!p.kept) {
-    flag[g] = 0u;
-    key_g[g] = 0xFFFFFFFFu;
-    return;
+  // thread 0: start chunk c into stage st
+  auto issue = [&](uint32_t c, int st) {
+    const Chunk ch = chunks[c];
+    s_chunk[st] = ch;
+    const uint32_t bytes = ch.count * kRecordFloats * 4u;
+    const bool tma = (ch.row & 3u) == 0 && (ch.count & 3u) == 0 && ch.count > 0;
+    s_tma[st] = tma;
+    if (tma) {
+      mbar_arrive_tx(&bar[st], bytes);
+      bulk_g2s(sbuf + st * kChunkFloats, pool + (size_t)ch.row * kRecordFloats, bytes, &bar[st]);
+    } else {
+      mbar_arrive_tx(&bar[st], 0u);
+    }
+  };
+  uint32_t phase = 0;  // bit k: parity of stage k's next completion
+  int st = 0;
+  if (t == 0) issue(blockIdx.x, 0);
+  for (uint32_t c = blockIdx.x; c < n; c += gridDim.x, st ^= 1) {
+    const uint32_t cn = c + gridDim.x;
+    if (t == 0 && cn < n) issue(cn, st ^ 1);  // freed by the barrier ending the last iteration
+    mbar_wait(&bar[st], (phase >> st) & 1u);
+    phase ^= 1u << st;
+    const Chunk ch = s_chunk[st];
+    float* stage = sbuf + st * kChunkFloats;
+    if (!s_tma[st]) {
+      const float* src = pool + (size_t)ch.row * kRecordFloats;
+      for (uint32_t i = t; i < ch.count * kRecordFloats; i += blockDim.x) stage[i] = __ldg(src + i);
+      __syncthreads();
+    }
+    if (t < ch.count) {
+      const uint32_t g = ch.gather + t;
+      const float* r = stage + t * kRecordFloats;
+      Proj p;
+      project_one(r, cam, p, true);
+      if (!p.kept) {
+        flag[g] = 0u;
+        key_g[g] = 0xFFFFFFFFu;
+      } else {
+        BlendRec o;
+        o.cx = __double2float_rn(p.cx);
+        o.cy = __double2float_rn(p.cy);
+        o.ca = __double2float_rn(p.ca);
+        o.cb = __double2float_rn(p.cb);
+        o.cc = __double2float_rn(p.cc);
+        o.r = __double2float_rn(p.col[0]);
+        o.g = __double2float_rn(p.col[1]);
+        o.b = __double2float_rn(p.col[2]);
+        o.alpha = r[10];
+        o.bx = (uint32_t)p.x0 | ((uint32_t)p.x1 << 16);
+        o.by = (uint32_t)p.y0 | ((uint32_t)p.y1 << 16);
+        o.skip = blend_skip(o.alpha);
+        rec[g] = o;
+        flag[g] = 1u;
+        key_g[g] = __float_as_uint(__double2float_rn(p.tz));
+      }
+    }
+    __syncthreads();  // this stage is refilled next iteration
   }
-  BlendRec o;
-  o.cx = __double2float_rn(p.cx);
-  o.cy = __double2float_rn(p.cy);
-  o.ca = __double2float_rn(p.ca);
-  o.cb = __double2float_rn(p.cb);
-  o.cc = __double2float_rn(p.cc);
-  o.r = __double2float_rn(p.col[0]);
-  o.g = __double2float_rn(p.col[1]);
-  o.b = __double2float_rn(p.col[2]);
-  o.alpha = r[10];
-  o.bx = (uint32_t)p.x0 | ((uint32_t)p.x1 << 16);
-  o.by = (uint32_t)p.y0 | ((uint32_t)p.y1 << 16);
-  o.skip = blend_skip(o.alpha);
-  rec[g] = o;
-  flag[g] = 1u;
-  key_g[g] = __float_as_uint(__double2float_rn(p.tz));
 }
 
 // project_records / compute_keys drop-ins over a contiguous (n, 59) array.
@@ -251,10 +324,33 @@ __global__ void sh_k(const double* __restrict__ coeffs, const double* __restrict
 
 }  // namespace
 
+namespace {
+constexpr size_t kPreSmem = sizeof(float) * kPreStages * kChunkFloats;
+int g_pre_grid = 0;  // persistent grid: SMs x resident CTAs
+}  // namespace
+
+int32_t preprocess_init() {
+  if (g_pre_grid) return VMS_OK;
+  VMS_CUDA(cudaFuncSetAttribute((const void*)preprocess_k,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPreSmem));
+  int per = 0, dev = 0, sms = 0;
+  VMS_CUDA(cudaGetDevice(&dev));
+  VMS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  VMS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, preprocess_k, kChunkRecords,
+                                                         kPreSmem));
+  g_pre_grid = std::max(1, sms) * std::max(1, per);
+  return VMS_OK;
+}
+
 int32_t render_preprocess(const float* pool, const Chunk* chunks, uint32_t max_chunks,
                           const RenderWs& w, cudaStream_t s) {
   if (max_chunks == 0) return VMS_OK;
-  preprocess_k<<<max_chunks, kChunkRecords, 0, s>>>(pool, chunks, w.fd, w.key_g, w.flag, w.rec);
+  if (!g_pre_grid) {
+    set_error("render_preprocess: preprocess_init() not called");
+    return VMS_ERR_INVALID;
+  }
+  const uint32_t g = std::min<uint32_t>(max_chunks, (uint32_t)g_pre_grid);
+  preprocess_k<<<g, kChunkRecords, kPreSmem, s>>>(pool, chunks, w.fd, w.key_g, w.flag, w.rec);
   mark("preprocess", s);
   VMS_LAUNCH_CHECK("render_preprocess");
   return VMS_OK;

@@ -100,9 +100,11 @@ int32_t render_band(int width, int height, const RenderWs& w, int exact, int ban
                     cudaStream_t s);
 int blend_band_row(int b, int bands, int tiles_y);
 
-// One-time blend setup (constant tables, shared-memory limits); must run
-// before the first blend launch and outside graph capture.
+// One-time setup (constant tables, shared-memory limits, persistent grid
+// sizes); must run before the first render launch and outside graph capture.
+// blend_init() also runs preprocess_init().
 int32_t blend_init();
+int32_t preprocess_init();
 
 // Per-CTA blend timing trace (profiling only; nullptr disables).
 int32_t debug_blend_trace(void* dev_ptr);
