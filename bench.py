@@ -56,15 +56,18 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-frames", type=int, default=1)
     p.add_argument("--scene-dir", default=os.environ.get("VMSPLAT_SCENE_DIR", "/tmp/vmsplat_bench"))
+    p.add_argument("--config", choices=("c2", "c3"), default="c2",
+                   help="c2 (BASELINE configs[1], the default bench line) or c3 (20M records, "
+                        "10k pages, 4 LOD levels; the scene is generated on first use, ~3 min)")
     return p.parse_args()
 
 
 def scene_path(args):
     from paper_2506_19415_b200 import scenegen
 
-    lay = scenegen.C2
+    lay = scenegen.C3 if getattr(args, "config", "c2") == "c3" else scenegen.C2
     os.makedirs(args.scene_dir, exist_ok=True)
-    path = os.path.join(args.scene_dir, f"c2_p{lay.n_pages}_s{lay.page_size}_l{lay.levels}"
+    path = os.path.join(args.scene_dir, f"city_p{lay.n_pages}_s{lay.page_size}_l{lay.levels}"
                                         f"_seed{lay.seed}.vms")
     return lay, path
 
@@ -143,23 +146,31 @@ def peaks():
         return 6650.0, "fallback"
 
 
-def launches_per_frame(stats, n_faces, upload_mode, host_output=False):
+def launches_per_frame(stats, n_faces, upload_mode, n_pages=1000):
     """Kernels of libvmsplat_b200.so launched per frame (static count of the
     captured sequences in vis.cu / prims.cu / preprocess.cu / blend.cu and the
     per-frame copies in session.cu):
-      visibility graph  vis_count, scan, vis_emit, vis_raster, vis_links,
-                        vis_flags, scan, vis_required                     8
+      visibility graph  vis_front (clip + scan + emit), vis_raster, vis_back
+                        (links + flags + compaction + LOD)                3
+                        (8 separate kernels past 16384 faces / 8191 pages)
       page copies       upload_k (copy stream), scatter_k                 2
       render graph      preprocess, scan, compact, radix hist + 4 passes,
                         dup_count, scan, dup_emit, clamp, radix hist + 2
                         passes, ranges, tile_order, blend                18
     (host output without zero-copy runs the blend as 4 band launches)."""
-    vis = 8 if n_faces else 5
+    vis = 3 if (n_faces <= 16384 and n_pages <= 8191) else 8
     up = 2 if stats["planned_copies"] else 0
     if up and upload_mode != 1:
         up = 1  # per-page cudaMemcpyAsync + scatter
     render = 18
     return vis + up + render
+
+
+def workload_name(args, lay):
+    n = lay.n_pages * lay.page_size
+    return (f"{args.config.upper()}: {n / 1e6:.2f}M-Gaussian paged city ({lay.n_pages} pages x "
+            f"{lay.page_size}, {lay.levels} LOD), {args.height}p {args.frames}-frame street "
+            f"fly-through, buffer 500, staging 40, vis 0.25, LOD+links on")
 
 
 def run_ours(args, rank, world, local_rank):
@@ -282,15 +293,14 @@ def run_ours(args, rank, world, local_rank):
     up_s = sum(s["time_copy"] for s in stats_t if s["bytes_copied"])
     value = world * args.steps / (ms_dev / 1e3)
     e2e = world * args.steps / (ms_e2e / 1e3)
-    launches = sum(launches_per_frame(s, len(scene.faces), args.upload_mode) for s in stats)
+    launches = sum(launches_per_frame(s, len(scene.faces), args.upload_mode, scene.page_count)
+                   for s in stats)
     out = {
         "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_dev / args.steps, 4),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64+f32",
         "data": "synthetic (scenegen city, seed 0)",
-        "config": {"workload": "C2: 2M-Gaussian paged city (1000 pages x 2048, 3 LOD), "
-                               "1080p 120-frame street fly-through, buffer 500, staging 40, "
-                               "vis 0.25, LOD+links on",
+        "config": {"workload": workload_name(args, lay),
                    "width": W, "height": H, "frames": F, "parallelism": f"view-shard x{world}",
                    "blend": "fp32" if args.fast else "fp64-exact",
                    "l2": "inputs larger than L2 (resident pool up to 241 MB > 126 MB L2)",
@@ -378,8 +388,7 @@ def run_reference(args, rank, world):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * dt / args.steps, 2),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (scenegen city, seed 0)", "impl": "reference",
-            "config": {"workload": "C2: 2M-Gaussian paged city, 1080p 120-frame street "
-                                   "fly-through, buffer 500, staging 40", "width": args.width,
+            "config": {"workload": workload_name(args, lay), "width": args.width,
                        "height": args.height},
             "cpu_baseline": {"value": round(v, 5), "unit": UNIT, "cores": 1, "kind": kind,
                              "sample": f"{n} full 1080p frames (step count capped at 12) after {args.warmup} "

@@ -166,6 +166,129 @@ __global__ void vis_emit_k(const VisFrameDev* __restrict__ fd, const double* __r
   }
 }
 
+// Single-CTA fused front end for meshes of up to kFrontMaxFaces faces (the
+// proxy meshes of the benchmark scenes): clears the per-frame counters, and
+// per round of 1024 faces clips them, scans their triangle counts across the
+// block and emits the screen triangles in (face, fan) order - replacing 3
+// memsets, vis_count_k, the scan and vis_emit_k.
+constexpr int kFrontThreads = 1024;
+constexpr uint32_t kFrontMaxFaces = 16384;
+constexpr uint32_t kBackMaxPages = 8191;
+
+__device__ __forceinline__ uint32_t block_scan_1024(uint32_t v, uint32_t* scratch,
+                                                    uint32_t* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t inc = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t u = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += u;
+  }
+  if (lane == 31) scratch[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    const uint32_t wv = scratch[lane];
+    uint32_t wi = wv;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t u = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= o) wi += u;
+    }
+    scratch[lane] = wi - wv;
+    if (lane == 31) scratch[32] = wi;
+  }
+  __syncthreads();
+  const uint32_t ex = scratch[warp] + inc - v;
+  *total = scratch[32];
+  __syncthreads();
+  return ex;
+}
+
+__global__ void __launch_bounds__(kFrontThreads) vis_front_k(
+    const VisFrameDev* __restrict__ fd, const double* __restrict__ verts,
+    const int32_t* __restrict__ faces, const uint32_t* __restrict__ face_page, uint32_t nf,
+    uint32_t page_count, VisTri* __restrict__ tris, uint32_t* __restrict__ meta,
+    uint32_t* __restrict__ base, uint8_t* __restrict__ direct) {
+  __shared__ VisCamera cam;
+  __shared__ uint32_t scratch[33];
+  if (threadIdx.x == 0) cam = fd->cam;
+  for (uint32_t p = threadIdx.x; p <= page_count; p += kFrontThreads) {
+    base[p] = 0u;
+    direct[p] = 0;
+  }
+  if (threadIdx.x < 4) meta[threadIdx.x] = 0u;
+  __syncthreads();
+  uint32_t run = 0;
+  for (uint32_t f0 = 0; f0 < nf; f0 += kFrontThreads) {
+    const uint32_t f = f0 + threadIdx.x;
+    View3 v[3], poly[4];
+    int k = 0;
+    if (f < nf) {
+      face_view(cam, verts, faces, f, v);
+      k = clip_poly(v, cam.near, poly);
+    }
+    const uint32_t cnt = k >= 3 ? (uint32_t)(k - 2) : 0u;
+    uint32_t tot;
+    const uint32_t o = run + block_scan_1024(cnt, scratch, &tot);
+    for (int i = 1; i + 1 < k; ++i) {
+      double x[3], y[3], z[3];
+      to_pixels(cam, poly[0], &x[0], &y[0], &z[0]);
+      to_pixels(cam, poly[i], &x[1], &y[1], &z[1]);
+      to_pixels(cam, poly[i + 1], &x[2], &y[2], &z[2]);
+      setup_tri(x[0], y[0], z[0], x[1], y[1], z[1], x[2], y[2], z[2], face_page[f], cam.width,
+                cam.height, &tris[o + i - 1]);
+    }
+    run += tot;
+  }
+  if (threadIdx.x == 0) meta[0] = run;  // clipped triangles
+}
+
+// Single-CTA fused back end for up to kBackMaxPages pages: one-hop link
+// expansion from the pre-propagation snapshot (shared-memory atomics),
+// required flags, the ordered compaction and the LOD level per page -
+// replacing a copy, vis_links_k, vis_flags_k, the scan and vis_required_k.
+__global__ void __launch_bounds__(kFrontThreads) vis_back_k(
+    const uint32_t* __restrict__ base, const uint8_t* __restrict__ direct,
+    const uint32_t* __restrict__ link_off, const uint32_t* __restrict__ link_tgt,
+    uint32_t page_count, const VisFrameDev* __restrict__ fd, uint32_t* __restrict__ depth_g,
+    uint32_t* __restrict__ meta, RequiredOut out) {
+  __shared__ uint32_t dep[kBackMaxPages + 1];
+  __shared__ uint32_t scratch[33];
+  for (uint32_t p = threadIdx.x; p <= page_count; p += kFrontThreads) dep[p] = base[p];
+  __syncthreads();
+  // links (runtime.py:89-96): targets pull the source's snapshot depth
+  for (uint32_t p = 1 + threadIdx.x; p <= page_count; p += kFrontThreads) {
+    if (!direct[p]) continue;
+    const uint32_t src = base[p];
+    for (uint32_t i = link_off[p - 1]; i < link_off[p]; ++i) {
+      const uint32_t q = link_tgt[i];
+      if (q != p && q >= 1 && q <= page_count) atomicMax(&dep[q], src);
+    }
+  }
+  __syncthreads();
+  const VisLod& lod = fd->lod;
+  uint32_t run = 0;
+  for (uint32_t p0 = 0; p0 <= page_count; p0 += kFrontThreads) {
+    const uint32_t p = p0 + threadIdx.x;
+    const uint32_t e = (p >= 1 && p <= page_count) ? dep[p] : 0u;
+    if (p <= page_count) depth_g[p] = e;
+    uint32_t tot;
+    const uint32_t o = run + block_scan_1024(e ? 1u : 0u, scratch, &tot);
+    if (e) {
+      // select_lod: level = #thresholds strictly below the decoded depth
+      const double d = (double)__uint_as_float(0xFFFFFFFFu - e);
+      uint8_t level = 0;
+      for (int k = 0; k < lod.count; ++k) level += lod.thresholds[k] < d ? 1 : 0;
+      out.pid[o] = p;
+      out.enc[o] = e;
+      out.direct[o] = direct[p];
+      out.level[o] = level;
+    }
+    run += tot;
+  }
+  if (threadIdx.x == 0) meta[1] = run;  // required pages
+}
+
 __global__ void vis_setup_raw_k(const double* __restrict__ raw, const uint32_t* __restrict__ ids,
                                 uint32_t n, int w, int h, VisTri* __restrict__ tris) {
   uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -403,10 +526,26 @@ int32_t vis_launch(const VisArgs& a, cudaStream_t s) {
   VisWs w = carve_ws(a.workspace, a.n_faces, a.page_count);
   const int T = 256;
   mark("begin", s);
-  VMS_CUDA(cudaMemsetAsync(w.n_tris, 0, sizeof(uint32_t) * 4, s));
-  VMS_CUDA(cudaMemsetAsync(w.base, 0, sizeof(uint32_t) * (a.page_count + 1), s));
-  VMS_CUDA(cudaMemsetAsync(w.direct, 0, a.page_count + 1, s));
-  if (a.n_faces) {
+  const bool fused = a.n_faces <= kFrontMaxFaces && a.page_count <= kBackMaxPages;
+  if (fused) {
+    // 3 kernels: fused front (clip/scan/emit), raster, fused back
+    vis_front_k<<<1, kFrontThreads, 0, s>>>(w.fd, a.verts, a.faces, a.face_page, a.n_faces,
+                                            a.page_count, w.tris, w.n_tris, w.base, w.direct);
+    mark("vis_front", s);
+    dim3 grid(ceil_div(a.cam.width, kVisTile), ceil_div(a.cam.height, kVisTile));
+    vis_raster_k<<<grid, kVisThreads, 0, s>>>(w.tris, w.n_tris, 0, a.cam.width, a.cam.height,
+                                              a.id_image, a.invz_image, 0, a.page_count,
+                                              w.base, w.direct, w.err);
+    mark("vis_raster", s);
+    vis_back_k<<<1, kFrontThreads, 0, s>>>(w.base, w.direct, a.link_off, a.link_tgt, a.page_count,
+                                           w.fd, w.depth, w.n_tris, a.out);
+    mark("vis_back", s);
+  } else {
+    VMS_CUDA(cudaMemsetAsync(w.n_tris, 0, sizeof(uint32_t) * 4, s));
+    VMS_CUDA(cudaMemsetAsync(w.base, 0, sizeof(uint32_t) * (a.page_count + 1), s));
+    VMS_CUDA(cudaMemsetAsync(w.direct, 0, a.page_count + 1, s));
+  }
+  if (!fused && a.n_faces) {
     vis_count_k<<<ceil_div<uint32_t>(a.n_faces, T), T, 0, s>>>(w.fd, a.verts, a.faces,
                                                                 a.n_faces, w.counts);
     mark("vis_count", s);
@@ -417,6 +556,7 @@ int32_t vis_launch(const VisArgs& a, cudaStream_t s) {
         w.fd, a.verts, a.faces, a.face_page, a.n_faces, w.offsets, w.tris);
     mark("vis_emit", s);
   }
+  if (!fused) {
   dim3 grid(ceil_div(a.cam.width, kVisTile), ceil_div(a.cam.height, kVisTile));
   vis_raster_k<<<grid, kVisThreads, 0, s>>>(w.tris, w.n_tris, 0, a.cam.width, a.cam.height,
                                             a.id_image, a.invz_image, 0, a.page_count,
@@ -438,6 +578,7 @@ int32_t vis_launch(const VisArgs& a, cudaStream_t s) {
   vis_required_k<<<ceil_div<uint32_t>(a.page_count + 1, T), T, 0, s>>>(
       w.depth, w.direct, w.pos, a.page_count, w.fd, a.out);
   mark("vis_required", s);
+  }
   if (a.out.meta) {
     VMS_CUDA(cudaMemcpyAsync(a.out.meta, w.n_tris, sizeof(uint32_t) * 4,
                              cudaMemcpyDeviceToHost, s));
