@@ -150,15 +150,15 @@ def launches_per_frame(stats, n_faces, upload_mode, n_pages=1000):
     """Kernels of libvmsplat_b200.so launched per frame (static count of the
     captured sequences in vis.cu / prims.cu / preprocess.cu / blend.cu and the
     per-frame copies in session.cu):
-      visibility graph  vis_front (clip + scan + emit), vis_raster, vis_back
-                        (links + flags + compaction + LOD)                3
-                        (8 separate kernels past 16384 faces / 8191 pages)
+      visibility graph  vis_count, scan, vis_emit, vis_raster, vis_back
+                        (links + flags + compaction + LOD)                5
+                        (4 separate back-end kernels past 32767 pages)
       page copies       upload_k (copy stream), scatter_k                 2
       render graph      preprocess, scan, compact, radix hist + 4 passes,
                         dup_count, scan, dup_emit, clamp, radix hist + 2
                         passes, ranges, tile_order, blend                18
     (host output without zero-copy runs the blend as 4 band launches)."""
-    vis = 3 if (n_faces <= 16384 and n_pages <= 8191) else 8
+    vis = 5 if n_pages <= 32767 else 8
     up = 2 if stats["planned_copies"] else 0
     if up and upload_mode != 1:
         up = 1  # per-page cudaMemcpyAsync + scatter

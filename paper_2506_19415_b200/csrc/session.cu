@@ -382,7 +382,7 @@ vms_session* vms_session_create(const vms_session_desc* desc) {
     set_error("session_create: pool larger than 2^32 records");
     return nullptr;
   }
-  if (blend_init() != VMS_OK) return nullptr;
+  if (blend_init() != VMS_OK || vis_init() != VMS_OK) return nullptr;
   vms_session* s = new vms_session();
   s->d = *desc;
   s->pt = vms_pt_create(desc->capacity);

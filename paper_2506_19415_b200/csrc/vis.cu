@@ -166,14 +166,8 @@ __global__ void vis_emit_k(const VisFrameDev* __restrict__ fd, const double* __r
   }
 }
 
-// Single-CTA fused front end for meshes of up to kFrontMaxFaces faces (the
-// proxy meshes of the benchmark scenes): clears the per-frame counters, and
-// per round of 1024 faces clips them, scans their triangle counts across the
-// block and emits the screen triangles in (face, fan) order - replacing 3
-// memsets, vis_count_k, the scan and vis_emit_k.
 constexpr int kFrontThreads = 1024;
-constexpr uint32_t kFrontMaxFaces = 16384;
-constexpr uint32_t kBackMaxPages = 8191;
+constexpr uint32_t kBackMaxPages = 32767;   // page depths in <= 128 KB of shared memory
 
 __device__ __forceinline__ uint32_t block_scan_1024(uint32_t v, uint32_t* scratch,
                                                     uint32_t* total) {
@@ -204,45 +198,6 @@ __device__ __forceinline__ uint32_t block_scan_1024(uint32_t v, uint32_t* scratc
   return ex;
 }
 
-__global__ void __launch_bounds__(kFrontThreads) vis_front_k(
-    const VisFrameDev* __restrict__ fd, const double* __restrict__ verts,
-    const int32_t* __restrict__ faces, const uint32_t* __restrict__ face_page, uint32_t nf,
-    uint32_t page_count, VisTri* __restrict__ tris, uint32_t* __restrict__ meta,
-    uint32_t* __restrict__ base, uint8_t* __restrict__ direct) {
-  __shared__ VisCamera cam;
-  __shared__ uint32_t scratch[33];
-  if (threadIdx.x == 0) cam = fd->cam;
-  for (uint32_t p = threadIdx.x; p <= page_count; p += kFrontThreads) {
-    base[p] = 0u;
-    direct[p] = 0;
-  }
-  if (threadIdx.x < 4) meta[threadIdx.x] = 0u;
-  __syncthreads();
-  uint32_t run = 0;
-  for (uint32_t f0 = 0; f0 < nf; f0 += kFrontThreads) {
-    const uint32_t f = f0 + threadIdx.x;
-    View3 v[3], poly[4];
-    int k = 0;
-    if (f < nf) {
-      face_view(cam, verts, faces, f, v);
-      k = clip_poly(v, cam.near, poly);
-    }
-    const uint32_t cnt = k >= 3 ? (uint32_t)(k - 2) : 0u;
-    uint32_t tot;
-    const uint32_t o = run + block_scan_1024(cnt, scratch, &tot);
-    for (int i = 1; i + 1 < k; ++i) {
-      double x[3], y[3], z[3];
-      to_pixels(cam, poly[0], &x[0], &y[0], &z[0]);
-      to_pixels(cam, poly[i], &x[1], &y[1], &z[1]);
-      to_pixels(cam, poly[i + 1], &x[2], &y[2], &z[2]);
-      setup_tri(x[0], y[0], z[0], x[1], y[1], z[1], x[2], y[2], z[2], face_page[f], cam.width,
-                cam.height, &tris[o + i - 1]);
-    }
-    run += tot;
-  }
-  if (threadIdx.x == 0) meta[0] = run;  // clipped triangles
-}
-
 // Single-CTA fused back end for up to kBackMaxPages pages: one-hop link
 // expansion from the pre-propagation snapshot (shared-memory atomics),
 // required flags, the ordered compaction and the LOD level per page -
@@ -252,7 +207,7 @@ __global__ void __launch_bounds__(kFrontThreads) vis_back_k(
     const uint32_t* __restrict__ link_off, const uint32_t* __restrict__ link_tgt,
     uint32_t page_count, const VisFrameDev* __restrict__ fd, uint32_t* __restrict__ depth_g,
     uint32_t* __restrict__ meta, RequiredOut out) {
-  __shared__ uint32_t dep[kBackMaxPages + 1];
+  extern __shared__ uint32_t dep[];  // page_count + 1 words
   __shared__ uint32_t scratch[33];
   for (uint32_t p = threadIdx.x; p <= page_count; p += kFrontThreads) dep[p] = base[p];
   __syncthreads();
@@ -302,9 +257,10 @@ __global__ void __launch_bounds__(kVisThreads) vis_raster_k(
     int w, int h, uint32_t* __restrict__ id_image, double* __restrict__ invz_image,
     int init_from_images, uint32_t page_count, uint32_t* __restrict__ page_depth,
     uint8_t* __restrict__ page_direct, uint32_t* __restrict__ err) {
+  constexpr int kBoxes = 4;  // triangle boxes tested per thread per round
   __shared__ VisTri stri[kVisThreads];
+  __shared__ uint32_t sidx[kBoxes * kVisThreads];
   __shared__ uint32_t wsum[kVisThreads / 32];
-  __shared__ uint32_t nlist;
 
   const int tx0 = blockIdx.x * kVisTile, ty0 = blockIdx.y * kVisTile;
   const int tx1 = min(tx0 + kVisTile, w) - 1, ty1 = min(ty0 + kVisTile, h) - 1;
@@ -321,52 +277,65 @@ __global__ void __launch_bounds__(kVisThreads) vis_raster_k(
     best_z = invz_image[(int64_t)py * w + px];
   }
   const uint32_t n = n_tris_dev ? *n_tris_dev : n_host;
-  for (uint32_t base = 0; base < n; base += kVisThreads) {
-    const uint32_t ti = base + threadIdx.x;
-    bool hit = false;
-    VisTri t;
-    if (ti < n) {
-      // the 16-byte box first; the 112-byte triangle only for the hits
-      const int4 bx = __ldg(reinterpret_cast<const int4*>(&tris[ti].x0));
-      hit = bx.x <= bx.y && bx.x <= tx1 && bx.y >= tx0 && bx.z <= ty1 && bx.w >= ty0;
-      if (hit) t = tris[ti];
-    }
-    const uint32_t bal = __ballot_sync(0xffffffffu, hit);
-    if (lane == 0) wsum[warp] = __popc(bal);
-    __syncthreads();
-    uint32_t pre = 0, tot = 0;
+  for (uint32_t base = 0; base < n; base += kBoxes * kVisThreads) {
+    // test kBoxes 16-byte boxes per thread (loads in flight together) and
+    // compact the indices of the triangles touching this tile, in order
+    bool hit[kBoxes];
 #pragma unroll
-    for (int k = 0; k < kVisThreads / 32; ++k) {
-      uint32_t c = wsum[k];
-      pre += k < warp ? c : 0u;
-      tot += c;
-    }
-    if (hit) stri[pre + __popc(bal & lanemask_lt())] = t;
-    if (threadIdx.x == 0) nlist = tot;
-    __syncthreads();
-    if (inside_img) {
-      const uint32_t m = nlist;
-      for (uint32_t j = 0; j < m; ++j) {
-        const VisTri& q = stri[j];
-        if (px < q.x0 || px > q.x1 || py < q.y0 || py > q.y1) continue;
-        const double e0 = dsub(dmul(dsub(q.cx, q.bx), dsub(fy, q.by)),
-                               dmul(dsub(q.cy, q.by), dsub(fx, q.bx)));
-        if (e0 < 0.0) continue;
-        const double e1 = dsub(dmul(dsub(q.ax, q.cx), dsub(fy, q.cy)),
-                               dmul(dsub(q.ay, q.cy), dsub(fx, q.cx)));
-        if (e1 < 0.0) continue;
-        const double e2 = dsub(dmul(dsub(q.bx, q.ax), dsub(fy, q.ay)),
-                               dmul(dsub(q.by, q.ay), dsub(fx, q.ax)));
-        if (e2 < 0.0) continue;
-        const double iz =
-            ddiv(dadd(dadd(dmul(e0, q.iza), dmul(e1, q.izb)), dmul(e2, q.izc)), q.area);
-        if (iz > best_z) {
-          best_z = iz;
-          best_id = q.id;
-        }
+    for (int k = 0; k < kBoxes; ++k) {
+      const uint32_t ti = base + k * kVisThreads + threadIdx.x;
+      hit[k] = false;
+      if (ti < n) {
+        const int4 bx = __ldg(reinterpret_cast<const int4*>(&tris[ti].x0));
+        hit[k] = bx.x <= bx.y && bx.x <= tx1 && bx.y >= tx0 && bx.z <= ty1 && bx.w >= ty0;
       }
     }
-    __syncthreads();
+    uint32_t cnt = 0;
+#pragma unroll
+    for (int k = 0; k < kBoxes; ++k) {
+      const uint32_t bal = __ballot_sync(0xffffffffu, hit[k]);
+      if (lane == 0) wsum[warp] = __popc(bal);
+      __syncthreads();
+      uint32_t pre = 0, tot = 0;
+#pragma unroll
+      for (int q = 0; q < kVisThreads / 32; ++q) {
+        const uint32_t c = wsum[q];
+        pre += q < warp ? c : 0u;
+        tot += c;
+      }
+      if (hit[k]) sidx[cnt + pre + __popc(bal & lanemask_lt())] = base + k * kVisThreads + threadIdx.x;
+      cnt += tot;
+      __syncthreads();
+    }
+    // the hits, kVisThreads at a time: stage the triangles, then every pixel
+    // walks them in index order (strict > keeps the first triangle on ties)
+    for (uint32_t h0 = 0; h0 < cnt; h0 += kVisThreads) {
+      const uint32_t m = min(cnt - h0, (uint32_t)kVisThreads);
+      if (threadIdx.x < m) stri[threadIdx.x] = tris[sidx[h0 + threadIdx.x]];
+      __syncthreads();
+      if (inside_img) {
+        for (uint32_t j = 0; j < m; ++j) {
+          const VisTri& q = stri[j];
+          if (px < q.x0 || px > q.x1 || py < q.y0 || py > q.y1) continue;
+          const double e0 = dsub(dmul(dsub(q.cx, q.bx), dsub(fy, q.by)),
+                                 dmul(dsub(q.cy, q.by), dsub(fx, q.bx)));
+          if (e0 < 0.0) continue;
+          const double e1 = dsub(dmul(dsub(q.ax, q.cx), dsub(fy, q.cy)),
+                                 dmul(dsub(q.ay, q.cy), dsub(fx, q.cx)));
+          if (e1 < 0.0) continue;
+          const double e2 = dsub(dmul(dsub(q.bx, q.ax), dsub(fy, q.ay)),
+                                 dmul(dsub(q.by, q.ay), dsub(fx, q.ax)));
+          if (e2 < 0.0) continue;
+          const double iz =
+              ddiv(dadd(dadd(dmul(e0, q.iza), dmul(e1, q.izb)), dmul(e2, q.izc)), q.area);
+          if (iz > best_z) {
+            best_z = iz;
+            best_id = q.id;
+          }
+        }
+      }
+      __syncthreads();
+    }
   }
   if (inside_img) {
     if (id_image) id_image[(int64_t)py * w + px] = best_id;
@@ -505,6 +474,16 @@ VisWs carve_ws(void* ws, uint32_t nf, uint32_t P) {
 }
 }  // namespace
 
+int32_t vis_init() {
+  static bool done = false;
+  if (done) return VMS_OK;
+  VMS_CUDA(cudaFuncSetAttribute((const void*)vis_back_k,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)(sizeof(uint32_t) * (kBackMaxPages + 1))));
+  done = true;
+  return VMS_OK;
+}
+
 VisFrameDev* vis_frame_dev(void* ws, uint32_t n_faces, uint32_t page_count) {
   return carve_ws(ws, n_faces, page_count).fd;
 }
@@ -519,6 +498,7 @@ int32_t vis_frame(const VisArgs& a, cudaStream_t s) {
 }
 
 int32_t vis_launch(const VisArgs& a, cudaStream_t s) {
+  if (const int32_t rc = vis_init()) return rc;
   if (a.n_faces && (!a.verts || !a.faces || !a.face_page)) {
     set_error("vis_frame: null mesh pointer");
     return VMS_ERR_INVALID;
@@ -526,26 +506,13 @@ int32_t vis_launch(const VisArgs& a, cudaStream_t s) {
   VisWs w = carve_ws(a.workspace, a.n_faces, a.page_count);
   const int T = 256;
   mark("begin", s);
-  const bool fused = a.n_faces <= kFrontMaxFaces && a.page_count <= kBackMaxPages;
-  if (fused) {
-    // 3 kernels: fused front (clip/scan/emit), raster, fused back
-    vis_front_k<<<1, kFrontThreads, 0, s>>>(w.fd, a.verts, a.faces, a.face_page, a.n_faces,
-                                            a.page_count, w.tris, w.n_tris, w.base, w.direct);
-    mark("vis_front", s);
-    dim3 grid(ceil_div(a.cam.width, kVisTile), ceil_div(a.cam.height, kVisTile));
-    vis_raster_k<<<grid, kVisThreads, 0, s>>>(w.tris, w.n_tris, 0, a.cam.width, a.cam.height,
-                                              a.id_image, a.invz_image, 0, a.page_count,
-                                              w.base, w.direct, w.err);
-    mark("vis_raster", s);
-    vis_back_k<<<1, kFrontThreads, 0, s>>>(w.base, w.direct, a.link_off, a.link_tgt, a.page_count,
-                                           w.fd, w.depth, w.n_tris, a.out);
-    mark("vis_back", s);
-  } else {
-    VMS_CUDA(cudaMemsetAsync(w.n_tris, 0, sizeof(uint32_t) * 4, s));
-    VMS_CUDA(cudaMemsetAsync(w.base, 0, sizeof(uint32_t) * (a.page_count + 1), s));
-    VMS_CUDA(cudaMemsetAsync(w.direct, 0, a.page_count + 1, s));
-  }
-  if (!fused && a.n_faces) {
+  // page sets up to kBackMaxPages: a single-CTA fused back end (links,
+  // flags, compaction, LOD) after the raster
+  const bool back = a.page_count <= kBackMaxPages;
+  VMS_CUDA(cudaMemsetAsync(w.n_tris, 0, sizeof(uint32_t) * 4, s));
+  VMS_CUDA(cudaMemsetAsync(w.base, 0, sizeof(uint32_t) * (a.page_count + 1), s));
+  VMS_CUDA(cudaMemsetAsync(w.direct, 0, a.page_count + 1, s));
+  if (a.n_faces) {
     vis_count_k<<<ceil_div<uint32_t>(a.n_faces, T), T, 0, s>>>(w.fd, a.verts, a.faces,
                                                                 a.n_faces, w.counts);
     mark("vis_count", s);
@@ -556,12 +523,16 @@ int32_t vis_launch(const VisArgs& a, cudaStream_t s) {
         w.fd, a.verts, a.faces, a.face_page, a.n_faces, w.offsets, w.tris);
     mark("vis_emit", s);
   }
-  if (!fused) {
   dim3 grid(ceil_div(a.cam.width, kVisTile), ceil_div(a.cam.height, kVisTile));
   vis_raster_k<<<grid, kVisThreads, 0, s>>>(w.tris, w.n_tris, 0, a.cam.width, a.cam.height,
                                             a.id_image, a.invz_image, 0, a.page_count,
                                             w.base, w.direct, w.err);
   mark("vis_raster", s);
+  if (back) {
+    vis_back_k<<<1, kFrontThreads, sizeof(uint32_t) * (a.page_count + 1), s>>>(
+        w.base, w.direct, a.link_off, a.link_tgt, a.page_count, w.fd, w.depth, w.n_tris, a.out);
+    mark("vis_back", s);
+  } else {
   VMS_CUDA(cudaMemcpyAsync(w.depth, w.base, sizeof(uint32_t) * (a.page_count + 1),
                            cudaMemcpyDeviceToDevice, s));
   if (a.page_count) {

@@ -31,6 +31,8 @@ struct VisFrameDev {
 };
 
 size_t vis_ws_bytes(uint32_t n_faces, uint32_t page_count);
+// One-time setup (shared-memory limits); outside graph capture.
+int32_t vis_init();
 VisFrameDev* vis_frame_dev(void* ws, uint32_t n_faces, uint32_t page_count);
 // Upload a.cam / a.lod into the workspace, then vis_launch.
 int32_t vis_frame(const VisArgs& a, cudaStream_t s);
