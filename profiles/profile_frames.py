@@ -21,6 +21,7 @@ def main():
     p.add_argument("--warm", type=int, default=10)
     p.add_argument("--frames", type=int, default=2)
     p.add_argument("--fast", action="store_true")
+    p.add_argument("--config", choices=("c2", "c3"), default="c2")
     a = p.parse_args()
     import torch
 
@@ -31,6 +32,7 @@ def main():
 
     class A:
         scene_dir = os.environ.get("VMSPLAT_SCENE_DIR", "/tmp/vmsplat_bench")
+        config = a.config
 
     lay, path = bench.ensure_scene(A, 0)
     scene = read_scene(path, mmap_gaussians=True)
