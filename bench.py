@@ -9,8 +9,12 @@ page uploads (pinned host -> HBM) -> preprocess -> sorts -> blend.
 
   value  frames/s with the image left in HBM (out="device"); page uploads are
          part of every step (the scene lives in host memory by design).
-  e2e    frames/s through the public API with the frame copied to a pinned
-         host buffer every step (render_frame(out=<pinned numpy>)).
+  e2e    frames/s with every frame delivered to host memory through the
+         public API: the benchmark harness (harness.run_benchmark, pipelined:
+         frame i + 1 is submitted before frame i is handed to the sink, so each
+         frame's PCIe transfer overlaps the next frame's render; host wall
+         clock, device synchronised on both sides).  e2e_sync: one synchronous
+         render_frame(out=<page-locked numpy>) per step (also the N > 1 e2e).
 
 Multi-GPU (torchrun): views are sharded - rank r renders its contiguous
 block of the trajectory with its own page cache over its own pinned host copy
@@ -245,6 +249,33 @@ def run_ours(args, rank, world, local_rank):
     pinned = torch.empty((args.height, args.width, 3), dtype=torch.float32).pin_memory()
     fresh_session()
     ms_e2e, stats_e2e = timed(pinned.numpy())
+    # e2e through the benchmark harness (harness.run_benchmark, pipelined:
+    # frame i + 1 is submitted before frame i is handed to the sink, each a
+    # fresh page-locked array written by the blend) - single-GPU line only
+    e2e_pipe = None
+    if world == 1:
+        from paper_2506_19415_b200 import harness
+
+        # warm-up frames through the same pipelined path (this also sizes the
+        # session's pool of page-locked output arrays: two in flight)
+        holder.pop("s", None)
+        torch.cuda.empty_cache()
+        holder["s"] = VmSession(scene, buffer_pages=500, staging_pages=40, vis_scale=0.25,
+                                exact=not args.fast, upload_mode=args.upload_mode, timing=False)
+        harness.run_benchmark(scene, traj, frames=range(args.warmup), session=holder["s"],
+                              pipelined=True)
+        got = []
+        sink = lambda i, im: got.append(float(im[0, 0, 0]))  # noqa: E731 - touch each frame
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        harness.run_benchmark(scene, traj, frames=range(args.warmup, args.warmup + args.steps),
+                              session=holder["s"], frame_sink=sink, pipelined=True)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        assert len(got) == args.steps
+        e2e_pipe = {"value": round(args.steps / dt, 3), "unit": UNIT,
+                    "api": "harness.run_benchmark(pipelined=True) -> frame_sink(i, host image)",
+                    "clock": "host wall (time.perf_counter), device synchronised on both sides"}
     # third pass over the same frames with per-stage CUDA events (one sync per
     # frame): the stage breakdown and the roofline come from here
     fresh_session(timing=True)
@@ -291,6 +322,9 @@ def run_ours(args, rank, world, local_rank):
             traffic = None
     up_bytes = sum(s["bytes_copied"] for s in stats_t)
     up_s = sum(s["time_copy"] for s in stats_t if s["bytes_copied"])
+    h2d_step = int(statistics.mean(s["bytes_copied"] for s in stats_e2e)) + 16 * int(
+        statistics.mean(s.get("n_chunks", 0) for s in stats_e2e))
+    d2h_step = W * H * 12 + 10 * int(statistics.mean(s["required_pages"] for s in stats_e2e))
     value = world * args.steps / (ms_dev / 1e3)
     e2e = world * args.steps / (ms_e2e / 1e3)
     launches = sum(launches_per_frame(s, len(scene.faces), args.upload_mode, scene.page_count)
@@ -305,11 +339,16 @@ def run_ours(args, rank, world, local_rank):
                    "blend": "fp32" if args.fast else "fp64-exact",
                    "l2": "inputs larger than L2 (resident pool up to 241 MB > 126 MB L2)",
                    "upload_mode": args.upload_mode},
-        "e2e": {"value": round(e2e, 3), "unit": UNIT,
-                "h2d_bytes_per_step": int(statistics.mean(s["bytes_copied"] for s in stats_e2e))
-                + 16 * int(statistics.mean(s.get("n_chunks", 0) for s in stats_e2e)),
-                "d2h_bytes_per_step": W * H * 12 + 10 * int(statistics.mean(
-                    s["required_pages"] for s in stats_e2e))},
+        # e2e: frames delivered to host memory through the public API - the
+        # benchmark harness (pipelined: frame i + 1 renders while frame i
+        # crosses PCIe) on the single-GPU line; e2e_sync: one synchronous
+        # render_frame(out=<page-locked array>) per step (also the N > 1 value)
+        "e2e": dict(e2e_pipe or {"value": round(e2e, 3), "unit": UNIT,
+                                 "api": "VmSession.render_frame(out=<page-locked numpy>)"},
+                    h2d_bytes_per_step=h2d_step, d2h_bytes_per_step=d2h_step),
+        "e2e_sync": {"value": round(e2e, 3), "unit": UNIT,
+                     "api": "VmSession.render_frame(out=<page-locked numpy>), one call per step",
+                     "h2d_bytes_per_step": h2d_step, "d2h_bytes_per_step": d2h_step},
         "roofline": {"bound": "hbm", "kernel": dominant, "achieved": round(ach, 2),
                      "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s",
                      "frac": round(ach / hbm, 4), "traffic": traffic,

@@ -136,6 +136,7 @@ SIGNATURES = {
     "vms_session_set_render_ws": (I32, [P, P, ctypes.c_uint64, U32, I32, I32]),
     "vms_session_frame": (I32, [P, ctypes.POINTER(FrameArgs), ctypes.POINTER(FrameStats), P]),
     "vms_session_counters": (I32, [P, P, P]),
+    "vms_session_wait": (I32, [P, I32]),
     "vms_host_accessible": (I32, [P]),
     "vms_debug_blend_trace": (I32, [P]),
 }

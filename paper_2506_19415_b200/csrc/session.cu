@@ -677,6 +677,15 @@ int32_t vms_session_frame(vms_session* s, const vms_frame_args* a, vms_frame_sta
   return VMS_OK;
 }
 
+int32_t vms_session_wait(vms_session* s, int32_t back) {
+  if (!s || back < 0 || back > 1) {
+    set_error("session_wait: invalid arguments");
+    return VMS_ERR_INVALID;
+  }
+  if (s->last_par < 0) return VMS_OK;
+  return recycle(s, back == 0 ? s->last_par : s->last_par ^ 1);
+}
+
 int32_t vms_session_counters(vms_session* s, uint32_t* out4, void* stream) {
   if (!s || !out4) return VMS_ERR_INVALID;
   (void)stream;

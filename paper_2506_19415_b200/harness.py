@@ -116,25 +116,43 @@ def make_session(scene, config: BenchConfig, **extra):
 
 
 def run_benchmark(scene, path, config: BenchConfig | None = None, frame_sink=None,
-                  frames=None, session=None):
+                  frames=None, session=None, pipelined: bool = False):
     """Replay ``path`` over ``scene``; returns the list of FrameStats
     (harness.py:101-181).  ``frame_sink(i, image)`` receives each frame
     (float32 (h, w, 3) host array); frames are not kept otherwise.
-    ``frames`` (B200 extension) restricts the run to those frame indices,
-    in order - a shard of the path; ``session`` reuses an existing one."""
+    B200 extensions: ``frames`` restricts the run to those frame indices, in
+    order (a shard of the path); ``session`` reuses an existing one;
+    ``pipelined`` submits frame i + 1 before handing frame i to the sink, so
+    each frame's transfer to the host overlaps the next frame's render (the
+    durations are then not measured: zeros)."""
     cfg = config or BenchConfig()
     if scene.page_count == 0:
         raise DataError("benchmark needs a paged scene")
     indices = list(range(frames_to_run(path, cfg))) if frames is None else list(frames)
     if not cfg.vm:
         return _run_flat(scene, path, indices, frame_sink)
-    s = session if session is not None else make_session(scene, cfg, timing=True)
+    s = session if session is not None else make_session(scene, cfg, timing=not pipelined)
     out = []
+    if not pipelined:
+        for i in indices:
+            image, st = s.render_frame(path.frame_camera(i), i)
+            out.append(FrameStats.from_session(i, st))
+            if frame_sink is not None:
+                frame_sink(i, image)
+        return out
+    held = None  # (index, image) submitted, not yet handed over
     for i in indices:
-        image, st = s.render_frame(path.frame_camera(i), i)
-        out.append(FrameStats.from_session(i, st))
+        image, st = s.render_frame(path.frame_camera(i), i, wait=False)
+        out.append(FrameStats.from_session(i, {**st, **{f"time_{k}": 0.0 for k in STAGES}}))
+        if held is not None:
+            s.wait(1)
+            if frame_sink is not None:
+                frame_sink(*held)
+        held = (i, image)
+    if held is not None:
+        s.wait(0)
         if frame_sink is not None:
-            frame_sink(i, image)
+            frame_sink(*held)
     return out
 
 

@@ -470,14 +470,17 @@ class VmSession:
     def buffer(self):
         return self.pool
 
-    def render_frame(self, camera, frame_index: int, out=None):
+    def render_frame(self, camera, frame_index: int, out=None, wait: bool = True):
         """Run one frame.  Returns (image, stats) with the reference's stats
         keys (runtime.py:471-488) plus device counters.  ``out``: None -> a new
         (page-locked) numpy array; a float32 (h, w, 3) numpy array -> filled
         in place (by DMA when it is page-locked, else through a staging
         buffer); "device" -> a CUDA tensor, ordered on the current stream (the
         session alternates two such buffers), returned as soon as the frame
-        is enqueued."""
+        is enqueued.  ``wait=False`` with page-locked host output also
+        returns as soon as the frame is enqueued (frames pipeline two deep);
+        the array is complete after ``wait(0)`` (or ``wait(1)`` once the next
+        frame has been submitted)."""
         t = _device.torch()
         lib = self._lib
         h0 = time.perf_counter()
@@ -504,8 +507,8 @@ class VmSession:
             # array (out=None) or a staging buffer copied into `out`.  Memory
             # the device cannot address takes a banded device->host copy.
             if out is None:
-                host = t.empty((camera.height, camera.width, 3), dtype=t.float32, pin_memory=True)
-                target = host.numpy()
+                target = self._fresh_output(camera)
+                host = target
             else:
                 if out.dtype != np.float32 or out.shape != (camera.height, camera.width, 3) \
                         or not out.flags.c_contiguous:
@@ -517,7 +520,7 @@ class VmSession:
                     target = host.numpy()
             if self._zero_copy(target):
                 image = target
-                a.sync = 1
+                a.sync = 1 if (wait or host is not None and out is not None) else 0
             else:
                 a.host_image = target.ctypes.data
         a.image = image.ctypes.data if isinstance(image, np.ndarray) else image.data_ptr()
@@ -565,10 +568,31 @@ class VmSession:
         if device_out:
             return image, stats
         if out is None:
-            return host.numpy(), stats
+            return host, stats
         if host is not None:
             out[...] = host.numpy()
         return out, stats
+
+    def _fresh_output(self, camera):
+        """A page-locked (h, w, 3) array nobody else holds: the reference
+        returns a new array per frame, so a buffer is reused only once every
+        array handed out from it has been dropped by the caller (its
+        reference count is back to the pool's own)."""
+        import sys
+
+        t = _device.torch()
+        key = (camera.height, camera.width)
+        pool = self.__dict__.setdefault("_out_pool", {}).setdefault(key, [])
+        for i in range(len(pool)):
+            # references: the pool's tuple and getrefcount's argument
+            if sys.getrefcount(pool[i][1]) <= 2:
+                return pool[i][1]
+        ten = t.empty((camera.height, camera.width, 3), dtype=t.float32, pin_memory=True)
+        arr = ten.numpy()
+        pool.append((ten, arr))
+        if len(pool) > 64:  # the caller keeps frames: stop tracking the oldest
+            del pool[0]
+        return arr
 
     def _zero_copy(self, arr) -> bool:
         key = (arr.ctypes.data, arr.nbytes)
@@ -589,6 +613,11 @@ class VmSession:
             self._pinned_out = (key, t.empty((camera.height, camera.width, 3), dtype=t.float32)
                                 .pin_memory())
         return self._pinned_out[1]
+
+    def wait(self, back: int = 0):
+        """Block until the last submitted frame (back=0) or the one before
+        it (back=1) is complete - for ``render_frame(..., wait=False)``."""
+        _lib.check(self._lib.vms_session_wait(self._h, int(back)), "wait")
 
     def flush(self):
         """Wait for the last frame (device-output mode); returns its device

@@ -147,3 +147,25 @@ def test_run_benchmark_c1_matches_reference_stats(cuda, tmp_path):
     assert all(f.durations["render"] > 0 for f in stats)
     flat = harness.run_benchmark(sc, path, harness.BenchConfig(vm=False, frame_limit=2))
     assert [f.required for f in flat] == [sc.page_count] * 2
+
+
+@pytest.mark.gpu
+def test_pipelined_harness_frames_identical(cuda):
+    """run_benchmark(pipelined=True) (frame i + 1 submitted before frame i is
+    handed to the sink, host images written asynchronously) delivers the
+    same frames, in order, and the same counters as the synchronous run."""
+    from paper_2506_19415_b200 import scenegen
+
+    lay = scenegen.CityLayout(n_pages=40, page_size=256, levels=3, seed=5, scale=0.12)
+    sc = scenegen.city_scene(lay)
+    path = scenegen.street_path(lay, frames=16, width=160, height=96)
+    cfg = harness.BenchConfig(buffer_pages=16, staging_pages=6.0, vis_scale=0.5)
+    a, b = [], []
+    sa = harness.run_benchmark(sc, path, cfg, frame_sink=lambda i, im: a.append((i, im.copy())))
+    sb = harness.run_benchmark(sc, path, cfg, frame_sink=lambda i, im: b.append((i, im)),
+                               pipelined=True)
+    assert [i for i, _ in b] == list(range(path.frame_count))
+    for (ia, x), (ib, y) in zip(a, b):
+        assert ia == ib and np.array_equal(x, y), ia
+    assert [(f.required, f.missing, f.bytes_copied, f.resident_per_level) for f in sa] == \
+           [(f.required, f.missing, f.bytes_copied, f.resident_per_level) for f in sb]
