@@ -129,6 +129,8 @@ struct vms_session {
   cudaStream_t d2h_stream = nullptr;  // banded image copies to the host
   cudaEvent_t ev_band[kBands] = {};
   cudaEvent_t ev_d2h = nullptr;
+  cudaEvent_t ev_out[2] = {nullptr, nullptr};  // asynchronous host copy of a frame done
+  bool pending_out[2] = {false, false};
   cudaEvent_t ev_vis = nullptr, ev_copy = nullptr, ev_staging = nullptr;
   cudaEvent_t ev_done[2] = {nullptr, nullptr};
   cudaEvent_t tev[10] = {};
@@ -184,6 +186,8 @@ void free_session(vms_session* s) {
   for (cudaStream_t x : {s->vis_stream, s->copy_stream, s->cap_stream, s->d2h_stream})
     if (x) cudaStreamDestroy(x);
   for (cudaEvent_t e : s->ev_band)
+    if (e) cudaEventDestroy(e);
+  for (cudaEvent_t e : s->ev_out)
     if (e) cudaEventDestroy(e);
   if (s->ev_d2h) cudaEventDestroy(s->ev_d2h);
   for (cudaEvent_t e : {s->ev_vis, s->ev_copy, s->ev_staging, s->ev_done[0], s->ev_done[1]})
@@ -338,6 +342,10 @@ int32_t launch_render(vms_session* s, int w, int h, bool timing, bool banded, cu
 // and grow the tile-instance buffer if it overflowed (it was still blended
 // exactly, through the depth-sorted list).
 int32_t recycle(vms_session* s, int par) {
+  if (s->pending_out[par]) {
+    VMS_CUDA(cudaEventSynchronize(s->ev_out[par]));
+    s->pending_out[par] = false;
+  }
   if (!s->pending[par]) return VMS_OK;
   VMS_CUDA(cudaEventSynchronize(s->ev_done[par]));
   s->pending[par] = false;
@@ -411,6 +419,8 @@ vms_session* vms_session_create(const vms_session_desc* desc) {
   for (cudaEvent_t& e : s->ev_band)
     ok = ok && cudaEventCreateWithFlags(&e, cudaEventDisableTiming) == cudaSuccess;
   ok = ok && cudaEventCreateWithFlags(&s->ev_d2h, cudaEventDisableTiming) == cudaSuccess;
+  for (cudaEvent_t& e : s->ev_out)
+    ok = ok && cudaEventCreateWithFlags(&e, cudaEventDisableTiming) == cudaSuccess;
   for (cudaEvent_t* e : {&s->ev_vis, &s->ev_copy, &s->ev_staging, &s->ev_done[0], &s->ev_done[1]})
     ok = ok && cudaEventCreateWithFlags(e, cudaEventDisableTiming) == cudaSuccess;
   for (cudaEvent_t& e : s->tev) ok = ok && cudaEventCreate(&e) == cudaSuccess;
@@ -619,9 +629,22 @@ int32_t vms_session_frame(vms_session* s, const vms_frame_args* a, vms_frame_sta
                              cudaMemcpyHostToDevice, st));
   // host output: the blend runs as kBands launches over bands of tile rows
   // and each band's rows go to the host as soon as that band is blended
-  const bool banded = a->host_image != nullptr;
+  // host output, synchronous call: the blend runs as kBands launches and each
+  // band's rows are copied while the next band blends.  Asynchronous call
+  // (sync = 0): one blend, then one copy on the d2h stream that overlaps the
+  // NEXT frame's render (the image buffer is recycled only after the copy).
+  const bool async_out = a->host_image != nullptr && !a->sync && !timing;
+  const bool banded = a->host_image != nullptr && !async_out;
   rc = launch_render(s, W, H, timing, banded, st);
   if (rc) return rc;
+  if (async_out) {
+    VMS_CUDA(cudaEventRecord(s->ev_band[0], st));
+    VMS_CUDA(cudaStreamWaitEvent(s->d2h_stream, s->ev_band[0], 0));
+    VMS_CUDA(cudaMemcpyAsync(a->host_image, a->image, sizeof(float) * 3 * (size_t)W * H,
+                             cudaMemcpyDeviceToHost, s->d2h_stream));
+    VMS_CUDA(cudaEventRecord(s->ev_out[par], s->d2h_stream));
+    s->pending_out[par] = true;
+  }
   if (banded) {
     const int ts = tile_size(), tiles_y = ceil_div(H, ts);
     const size_t row_bytes = sizeof(float) * 3 * (size_t)W;
@@ -655,7 +678,7 @@ int32_t vms_session_frame(vms_session* s, const vms_frame_args* a, vms_frame_sta
   out->n_res = (uint32_t)n_res;
   rc = vms_pt_resident_counts(s->pt, out->resident_per_level, (int32_t)s->d.lod_levels);
   if (rc) return rc;
-  if (timing || a->host_image || a->sync) {
+  if (timing || a->sync || (a->host_image && !async_out)) {
     VMS_CUDA(cudaStreamSynchronize(st));
     const uint32_t* c = s->counters_h[par];
     out->n_kept = c[0];

@@ -518,11 +518,15 @@ class VmSession:
                 else:
                     host = self._staging(camera)
                     target = host.numpy()
-            if self._zero_copy(target):
-                image = target
-                a.sync = 1 if (wait or host is not None and out is not None) else 0
+            staged = host is not None and out is not None  # copied into `out` below
+            if (wait or staged) and self._zero_copy(target):
+                image = target  # the blend writes the host array over PCIe
+                a.sync = 1
             else:
+                # device image + DMA copy; with wait=False the copy overlaps the
+                # next frame's render and completes before wait()/recycling
                 a.host_image = target.ctypes.data
+                a.sync = 1 if (wait or staged) else 0
         a.image = image.ctypes.data if isinstance(image, np.ndarray) else image.data_ptr()
         stream = _device.sptr()
         st = self._stats
