@@ -7,6 +7,8 @@
 #include <vector>
 #include <algorithm>
 
+#include <cstdlib>
+
 #include "common.cuh"
 #include "prims.h"
 #include "render.h"
@@ -29,6 +31,14 @@ int32_t cuda_status(cudaError_t e, const char* where) {
 }
 
 bool g_profile = false;
+
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("VMSPLAT_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
 namespace {
 struct Mark {
   const char* name;
@@ -377,6 +387,8 @@ int32_t vms_render(const vms_render_args* a, void* stream) {
   f.n_chunks = a->n_chunks;
   f.n_splats = a->n_splats;
   int32_t st = render_upload_frame(w, f, s);
+  if (st) return st;
+  st = render_clear(a->cam.width, a->cam.height, w, s);
   if (st) return st;
   st = render_preprocess(a->pool, a->chunks, a->n_chunks, w, s);
   if (st) return st;

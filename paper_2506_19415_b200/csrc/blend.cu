@@ -56,6 +56,7 @@ T* carve(char*& p, size_t n) {
 __global__ void compact_k(const uint32_t* __restrict__ flag, const uint32_t* __restrict__ pos,
                           const uint32_t* __restrict__ key_g, const uint32_t* n_dev, uint32_t n_host,
                           uint32_t* __restrict__ k0, uint32_t* __restrict__ v0) {
+  pdl_wait();
   const uint32_t n = n_dev ? *n_dev : n_host;
   for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < n; g += gridDim.x * blockDim.x) {
     if (!flag[g]) continue;
@@ -93,6 +94,7 @@ __global__ void dup_count_k(const uint32_t* __restrict__ vals, const BlendRec* _
                             const RenderCounters* __restrict__ ctr, int shift, int gx, int gy,
                             uint32_t* __restrict__ cnt, uint32_t* __restrict__ rects,
                             uint32_t* __restrict__ tdiff) {
+  pdl_wait();
   extern __shared__ uint32_t sdiff[];
   const int cells = gx * gy;
   const bool local = cells <= kDiffSmemWords;
@@ -130,6 +132,7 @@ __global__ void __launch_bounds__(1024) tile_prep_k(
     RenderCounters* __restrict__ ctr, uint32_t* __restrict__ tcount,
     uint32_t* __restrict__ ranges, uint32_t* __restrict__ order, uint32_t* __restrict__ rcounters,
     uint32_t* __restrict__ ghist) {
+  pdl_wait();
   __shared__ uint32_t h[2][256];
   __shared__ uint32_t scratch[33];
   __shared__ uint32_t hist[33 * kMaxBands];
@@ -277,6 +280,7 @@ __global__ void __launch_bounds__(kEmitThreads) dup_emit_k(
     const uint32_t* __restrict__ off, const RenderCounters* __restrict__ ctr, int tiles_x,
     uint32_t* __restrict__ tk, uint32_t* __restrict__ tv, uint32_t* __restrict__ status,
     size_t pass_stride, uint32_t tile_items) {
+  pdl_wait();
   __shared__ uint32_t soff[kEmitChunk + 1];
   __shared__ uint2 sinfo[kEmitChunk];  // g, tx0 | ty0 << 8 | tiles across << 16
   __shared__ uint32_t span[2];
@@ -379,6 +383,7 @@ __global__ void __launch_bounds__(kBlendThreads) blend_k(const uint32_t* __restr
                                                          float* image_arg,
                                                          const FrameDev* __restrict__ fd,
                                                          int accumulate) {
+  pdl_wait();
   constexpr int SUB = TS / 16;  // sub-tiles per tile edge
   using Staged = typename std::conditional<kExact, SplatF64, BlendRec>::type;
   __shared__ Staged sp[kBlendThreads];
@@ -623,9 +628,10 @@ int32_t launch_band(int width, int height, const uint32_t* vals, const RenderWs&
   const int r0 = blend_band_row(band, bands, tiles_y), r1 = blend_band_row(band + 1, bands, tiles_y);
   const uint32_t first = (uint32_t)r0 * tiles_x, count = (uint32_t)(r1 - r0) * tiles_x;
   if (count)
-    kern<<<count * subs, kBlendThreads, 0, s>>>(w.ranges, w.order, sorted_tiles(w, n_tiles), vals,
-                                                w.ctr, w.rec, width, height, tiles_x, first, image,
-                                                w.fd, accumulate);
+    VMS_CUDA(launch(kern, count * subs, kBlendThreads, 0, s, (const uint32_t*)w.ranges,
+                    (const uint32_t*)w.order, sorted_tiles(w, n_tiles), vals,
+                    (const RenderCounters*)w.ctr, (const BlendRec*)w.rec, width, height, tiles_x,
+                    first, image, (const FrameDev*)w.fd, accumulate));
   mark("blend", s);
   VMS_LAUNCH_CHECK("blend");
   return VMS_OK;
@@ -636,7 +642,7 @@ int32_t launch_band(int width, int height, const uint32_t* vals, const RenderWs&
 // launches them with render_band).
 int32_t tiles_and_blend(int width, int height, const uint32_t* vals, const RenderWs& w,
                         float* image, int accumulate, int exact, void* const* events,
-                        bool external, int bands, cudaStream_t s) {
+                        bool external, int bands, bool cleared, cudaStream_t s) {
   const int ts = tile_size(), shift = ts == 16 ? 4 : 5;
   const int tiles_x = ceil_div(width, ts), tiles_y = ceil_div(height, ts);
   const uint32_t n_tiles = (uint32_t)tiles_x * tiles_y;
@@ -648,19 +654,21 @@ int32_t tiles_and_blend(int width, int height, const uint32_t* vals, const Rende
     return VMS_ERR_INVALID;
   }
   const int gx = tiles_x + 1, gy = tiles_y + 1;
-  VMS_CUDA(cudaMemsetAsync(w.tdiff, 0, sizeof(uint32_t) * gx * gy, s));
+  if (!cleared) VMS_CUDA(cudaMemsetAsync(w.tdiff, 0, sizeof(uint32_t) * gx * gy, s));
   const size_t dsm = gx * gy <= kDiffSmemWords ? sizeof(uint32_t) * gx * gy : 0;
-  dup_count_k<<<2 * kSMs, T, dsm, s>>>(vals, w.rec, w.ctr, shift, gx, gy, w.cnt, w.rects, w.tdiff);
+  VMS_CUDA(launch(dup_count_k, 2 * kSMs, T, dsm, s, vals, (const BlendRec*)w.rec,
+                  (const RenderCounters*)w.ctr, shift, gx, gy, w.cnt, w.rects, w.tdiff));
   mark("dup_count", s);
   int32_t st = scan_exclusive_u32(w.cnt, w.off, &w.ctr->n_kept, 0, w.n_cap, &w.ctr->n_inst,
-                                  w.scan_ws, s);
+                                  w.scan_ws2, s, !cleared);
   if (st) return st;
   const RadixLayout rl = radix_layout(w.radix_ws, w.n_cap > w.m_cap ? w.n_cap : w.m_cap);
-  tile_prep_k<<<1, 1024, dsm, s>>>(w.tdiff, tiles_x, tiles_y, nb, w.m_cap, w.ctr, w.tcount,
-                                    w.ranges, w.order, rl.counters, rl.ghist);
+  VMS_CUDA(launch(tile_prep_k, 1, 1024, dsm, s, (const uint32_t*)w.tdiff, tiles_x, tiles_y, nb,
+                  w.m_cap, w.ctr, w.tcount, w.ranges, w.order, rl.counters, rl.ghist));
   mark("tile_prep", s);
-  dup_emit_k<<<4 * kSMs, T, 0, s>>>(vals, w.rects, w.off, w.ctr, tiles_x, w.tk0, w.tv0, rl.status,
-                                    rl.pass_stride, rl.tile_items);
+  VMS_CUDA(launch(dup_emit_k, 4 * kSMs, T, 0, s, vals, (const uint32_t*)w.rects,
+                  (const uint32_t*)w.off, (const RenderCounters*)w.ctr, tiles_x, w.tk0, w.tv0,
+                  rl.status, rl.pass_stride, rl.tile_items));
   mark("dup_emit", s);
   int alt = 0;
   st = radix_passes_u32(w.tk0, w.tv0, w.tk1, w.tv1, &w.ctr->n_inst,
@@ -724,7 +732,7 @@ size_t render_ws_bytes(uint32_t n_cap, uint32_t m_cap, uint32_t n_tiles) {
   b += sizeof(uint32_t) * (4 * (size_t)n_tiles + 2);  // tcount + tdiff
   b += sizeof(uint32_t) * 3 * (size_t)n_tiles; // ranges + order
   b += sizeof(RenderCounters) + sizeof(FrameDev);
-  b += scan_ws_bytes(n_cap) + radix_ws_bytes(n_cap > m_cap ? n_cap : m_cap);
+  b += 2 * scan_ws_bytes(n_cap) + radix_ws_bytes(n_cap > m_cap ? n_cap : m_cap);
   return b + 256 * 24;
 }
 
@@ -755,6 +763,7 @@ RenderWs render_carve(void* ws, uint32_t n_cap, uint32_t m_cap, uint32_t n_tiles
   w.ctr = carve<RenderCounters>(p, 1);
   w.fd = carve<FrameDev>(p, 1);
   w.scan_ws = carve<char>(p, scan_ws_bytes(n_cap));
+  w.scan_ws2 = carve<char>(p, scan_ws_bytes(n_cap));
   w.radix_ws = carve<char>(p, radix_ws_bytes(n_cap > m_cap ? n_cap : m_cap));
   return w;
 }
@@ -769,19 +778,32 @@ int32_t render_band(int width, int height, const RenderWs& w, int exact, int ban
   return launch_band(width, height, sorted_vals(w), w, nullptr, 0, exact, band, bands, s);
 }
 
+int32_t render_clear(int width, int height, const RenderWs& w, cudaStream_t s) {
+  const int ts = tile_size();
+  const size_t cells = (size_t)(ceil_div(width, ts) + 1) * (ceil_div(height, ts) + 1);
+  VMS_CUDA(cudaMemsetAsync(w.ctr, 0, sizeof(RenderCounters), s));
+  VMS_CUDA(cudaMemsetAsync(w.scan_ws, 0, scan_ws_bytes(w.n_cap), s));
+  VMS_CUDA(cudaMemsetAsync(w.scan_ws2, 0, scan_ws_bytes(w.n_cap), s));
+  VMS_CUDA(cudaMemsetAsync(w.radix_ws, 0, radix_clear_bytes(), s));
+  VMS_CUDA(cudaMemsetAsync(w.tdiff, 0, sizeof(uint32_t) * cells, s));
+  return VMS_OK;
+}
+
 int32_t render_finish(int width, int height, const RenderWs& w, int accumulate, int exact,
                       void* const* events, bool external, int bands, cudaStream_t s) {
+  // render_clear() ran before the preprocess: the kernels below chain with
+  // programmatic dependent launches, no memset nodes in between
   const int T = 256;
-  VMS_CUDA(cudaMemsetAsync(w.ctr, 0, sizeof(RenderCounters), s));
   int32_t st = scan_exclusive_u32(w.flag, w.pos, &w.fd->n_splats, 0, w.n_cap, &w.ctr->n_kept,
-                                  w.scan_ws, s);
+                                  w.scan_ws, s, false);
   if (st) return st;
-  compact_k<<<8 * kSMs, T, 0, s>>>(w.flag, w.pos, w.key_g, &w.fd->n_splats, 0, w.k0, w.v0);
+  VMS_CUDA(launch(compact_k, 8 * kSMs, T, 0, s, (const uint32_t*)w.flag, (const uint32_t*)w.pos,
+                  (const uint32_t*)w.key_g, (const uint32_t*)&w.fd->n_splats, 0u, w.k0, w.v0));
   mark("compact", s);
   int alt = 0;
   // keys are IEEE bits of positive f32 depths: bit 31 is always clear
   st = radix_sort_u32(w.k0, w.v0, w.k1, w.v1, &w.ctr->n_kept, 0, w.n_cap, 0, 31, &alt,
-                      w.radix_ws, s);
+                      w.radix_ws, s, false);
   if (st) return st;
   record(events, 1, external, s);
   if ((alt ? w.v1 : w.v0) != sorted_vals(w)) {
@@ -789,7 +811,7 @@ int32_t render_finish(int width, int height, const RenderWs& w, int accumulate, 
     return VMS_ERR_INVARIANT;
   }
   return tiles_and_blend(width, height, alt ? w.v1 : w.v0, w, nullptr, accumulate, exact, events,
-                         external, bands, s);
+                         external, bands, true, s);
 }
 
 int32_t composite_ordered(const float* centers, const float* conics, const float* colors,
@@ -807,7 +829,7 @@ int32_t composite_ordered(const float* centers, const float* conics, const float
     compact_k<<<ceil_div<uint32_t>(n, T), T, 0, s>>>(ws.flag, ws.pos, ws.v1, nullptr, n, ws.k0,
                                                      ws.v0);
   }
-  return tiles_and_blend(w, h, ws.v0, ws, image, 1, exact, nullptr, false, 1, s);
+  return tiles_and_blend(w, h, ws.v0, ws, image, 1, exact, nullptr, false, 1, false, s);
 }
 
 }  // namespace vms

@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <utility>
+
 #include "../../include/vmsplat_b200.h"
 
 #define VMS_DEV __device__ __forceinline__
@@ -60,6 +62,32 @@ VMS_DEV double dot3(int mode, double a0, double a1, double a2, double b0, double
                     double b2) {
   if (mode == 0) return __fma_rn(a2, b2, __fma_rn(a1, b1, __dmul_rn(a0, b0)));
   return __dadd_rn(__dadd_rn(__dmul_rn(a0, b0), __dmul_rn(a1, b1)), __dmul_rn(a2, b2));
+}
+
+// Programmatic dependent launch (sm_90+): the kernels of the frame graphs
+// are launched with programmatic stream serialization, so a kernel's CTAs
+// are scheduled while its predecessor drains; each kernel calls pdl_wait()
+// before it touches anything an earlier kernel wrote (it returns once the
+// predecessor grid has completed and its writes are visible - and the
+// predecessor itself waited, so the chain is transitive).  Without the
+// launch attribute the wait is a no-op.  VMSPLAT_PDL=0 disables it.
+VMS_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+bool pdl_enabled();
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                   cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
 template <typename T>

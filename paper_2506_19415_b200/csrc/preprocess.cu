@@ -218,6 +218,7 @@ __global__ void __launch_bounds__(kChunkRecords) preprocess_k(
   __shared__ Chunk s_chunk[kPreStages];
   __shared__ int s_tma[kPreStages];
   __shared__ RenderCamera cam;
+  pdl_wait();
   const uint32_t n = fd->n_chunks;
   if (blockIdx.x >= n) return;
   const uint32_t t = threadIdx.x;
@@ -350,7 +351,8 @@ int32_t render_preprocess(const float* pool, const Chunk* chunks, uint32_t max_c
     return VMS_ERR_INVALID;
   }
   const uint32_t g = std::min<uint32_t>(max_chunks, (uint32_t)g_pre_grid);
-  preprocess_k<<<g, kChunkRecords, kPreSmem, s>>>(pool, chunks, w.fd, w.key_g, w.flag, w.rec);
+  VMS_CUDA(launch(preprocess_k, g, kChunkRecords, kPreSmem, s, pool, chunks,
+                  (const FrameDev*)w.fd, w.key_g, w.flag, w.rec));
   mark("preprocess", s);
   VMS_LAUNCH_CHECK("render_preprocess");
   return VMS_OK;

@@ -120,6 +120,7 @@ __global__ void __launch_bounds__(kLbThreads) scan_lb_k(const uint32_t* __restri
                                                         const uint32_t* n_dev, uint32_t n_host,
                                                         uint32_t* total, uint32_t* status,
                                                         uint32_t* counter) {
+  pdl_wait();
   __shared__ uint32_t sdata[kLbTile + kLbTile / 32];
   __shared__ uint32_t scratch[33];
   __shared__ uint32_t s_tile, s_prefix;
@@ -190,6 +191,7 @@ __global__ void __launch_bounds__(kRBlock) radix_hist_k(const uint32_t* __restri
                                                         uint32_t* __restrict__ ghist,
                                                         uint32_t* __restrict__ status,
                                                         size_t pass_stride) {
+  pdl_wait();
   __shared__ uint32_t h[4][256];
   for (int i = threadIdx.x; i < 4 * 256; i += kRBlock) (&h[0][0])[i] = 0;
   __syncthreads();
@@ -220,6 +222,7 @@ __global__ void __launch_bounds__(kRBlock) radix_onesweep_k(
     uint32_t* __restrict__ kout, uint32_t* __restrict__ vout, const uint32_t* n_dev,
     uint32_t n_host, int shift, uint32_t mask, const uint32_t* __restrict__ hist,
     uint32_t* status, uint32_t* counter) {
+  pdl_wait();
   __shared__ uint32_t wcnt[kRWarps][257];
   __shared__ uint32_t skey[kRTile];
   __shared__ uint32_t sval[kRTile];
@@ -343,17 +346,20 @@ size_t scan_ws_bytes(uint32_t n_max) {
 
 int32_t scan_exclusive_u32(const uint32_t* in, uint32_t* out, const uint32_t* n_dev,
                            uint32_t n_host, uint32_t n_max, uint32_t* total, void* ws,
-                           cudaStream_t s) {
+                           cudaStream_t s, bool clear) {
   const uint32_t max_tiles = (n_max + kLbTile - 1) / kLbTile;
   uint32_t* counter = static_cast<uint32_t*>(ws);
   uint32_t* status = counter + 32;
-  VMS_CUDA(cudaMemsetAsync(ws, 0, scan_ws_bytes(n_max), s));
+  if (clear) VMS_CUDA(cudaMemsetAsync(ws, 0, scan_ws_bytes(n_max), s));
   const int grid = persistent_grid((const void*)scan_lb_k, kLbThreads, max_tiles ? max_tiles : 1);
-  scan_lb_k<<<grid, kLbThreads, 0, s>>>(in, out, n_dev, n_host, total, status, counter);
+  VMS_CUDA(launch(scan_lb_k, grid, kLbThreads, 0, s, in, out, n_dev, n_host, total, status,
+                  counter));
   mark("scan", s);
   VMS_LAUNCH_CHECK("scan_exclusive_u32");
   return VMS_OK;
 }
+
+size_t radix_clear_bytes() { return sizeof(uint32_t) * (64 + 4 * 256); }
 
 size_t radix_ws_bytes(uint32_t n_max) {
   const size_t tiles = ((size_t)n_max + kRTile - 1) / kRTile;
@@ -388,9 +394,10 @@ int32_t radix_passes_u32(uint32_t* k0, uint32_t* v0, uint32_t* k1, uint32_t* v1,
     const uint32_t mask = (1u << bits) - 1u;
     uint32_t *ki = alt ? k1 : k0, *vi = alt ? v1 : v0;
     uint32_t *ko = alt ? k0 : k1, *vo = alt ? v0 : v1;
-    radix_onesweep_k<<<grid, kRBlock, 0, s>>>(ki, vi, ko, vo, n_dev, 0, b, mask,
-                                              l.ghist + p * 256, l.status + p * l.pass_stride,
-                                              l.counters + p);
+    VMS_CUDA(launch(radix_onesweep_k, grid, kRBlock, 0, s, (const uint32_t*)ki,
+                    (const uint32_t*)vi, ko, vo, n_dev, 0u, b, mask,
+                    (const uint32_t*)(l.ghist + p * 256), l.status + p * l.pass_stride,
+                    l.counters + p));
     mark("radix_pass", s);
     alt ^= 1;
   }
@@ -401,7 +408,7 @@ int32_t radix_passes_u32(uint32_t* k0, uint32_t* v0, uint32_t* k1, uint32_t* v1,
 
 int32_t radix_sort_u32(uint32_t* k0, uint32_t* v0, uint32_t* k1, uint32_t* v1,
                        const uint32_t* n_dev, uint32_t n_host, uint32_t n_max, int begin_bit,
-                       int end_bit, int* in_alt, void* ws, cudaStream_t s) {
+                       int end_bit, int* in_alt, void* ws, cudaStream_t s, bool clear) {
   const int passes = (end_bit - begin_bit + 7) / 8;
   if (passes > 4) {
     set_error("radix_sort_u32: at most 32 key bits");
@@ -411,12 +418,12 @@ int32_t radix_sort_u32(uint32_t* k0, uint32_t* v0, uint32_t* k1, uint32_t* v1,
   uint32_t* counters = static_cast<uint32_t*>(ws);  // one per pass
   uint32_t* ghist = counters + 64;                  // [passes][256]
   uint32_t* status = ghist + 4 * 256;               // [passes][tiles][256]
-  VMS_CUDA(cudaMemsetAsync(ws, 0, sizeof(uint32_t) * (64 + 4 * 256), s));
+  if (clear) VMS_CUDA(cudaMemsetAsync(ws, 0, radix_clear_bytes(), s));
   // a few CTAs per SM: each flushes 4 x 256 bins with global atomics
   const int hgrid = persistent_grid((const void*)radix_hist_k, kRBlock,
                                     (int)std::min<size_t>(2 * 148, (n_max + 4095) / 4096 + 1));
-  radix_hist_k<<<hgrid, kRBlock, 0, s>>>(k0, n_dev, n_host, begin_bit, end_bit, ghist, status,
-                                         256 * tiles);
+  VMS_CUDA(launch(radix_hist_k, hgrid, kRBlock, 0, s, (const uint32_t*)k0, n_dev, n_host,
+                  begin_bit, end_bit, ghist, status, (size_t)(256 * tiles)));
   mark("radix_hist", s);
   const int grid = persistent_grid((const void*)radix_onesweep_k, kRBlock, tiles ? (int)tiles : 1);
   int alt = 0;
@@ -426,9 +433,10 @@ int32_t radix_sort_u32(uint32_t* k0, uint32_t* v0, uint32_t* k1, uint32_t* v1,
     const uint32_t mask = (1u << bits) - 1u;
     uint32_t *ki = alt ? k1 : k0, *vi = alt ? v1 : v0;
     uint32_t *ko = alt ? k0 : k1, *vo = alt ? v0 : v1;
-    radix_onesweep_k<<<grid, kRBlock, 0, s>>>(ki, vi, ko, vo, n_dev, n_host, b, mask,
-                                              ghist + p * 256, status + (size_t)p * 256 * tiles,
-                                              counters + p);
+    VMS_CUDA(launch(radix_onesweep_k, grid, kRBlock, 0, s, (const uint32_t*)ki,
+                    (const uint32_t*)vi, ko, vo, n_dev, n_host, b, mask,
+                    (const uint32_t*)(ghist + p * 256), status + (size_t)p * 256 * tiles,
+                    counters + p));
     mark("radix_pass", s);
     alt ^= 1;
   }

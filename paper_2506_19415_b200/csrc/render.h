@@ -73,6 +73,7 @@ struct RenderWs {
   RenderCounters* ctr;
   FrameDev* fd;
   void* scan_ws;
+  void* scan_ws2;  // the second scan of a frame (tile instance offsets)
   void* radix_ws;
 };
 
@@ -108,6 +109,10 @@ int32_t preprocess_init();
 
 // Per-CTA blend timing trace (profiling only; nullptr disables).
 int32_t debug_blend_trace(void* dev_ptr);
+
+// Zero the frame's counters and primitive workspaces (all memsets of a
+// frame, ahead of its first kernel); render_finish assumes it ran.
+int32_t render_clear(int width, int height, const RenderWs& w, cudaStream_t s);
 
 // Stage FrameDev from host memory (pageable or pinned) into w.fd.
 int32_t render_upload_frame(const RenderWs& w, const FrameDev& f, cudaStream_t s);

@@ -317,7 +317,9 @@ int32_t launch_render(vms_session* s, int w, int h, bool timing, bool banded, cu
     if (timing)
       for (int i = 0; i < 4; ++i) ev[i] = s->tev[4 + i];
     mark("begin", q);
-    int32_t rc = render_preprocess(s->d.pool, s->chunks_d, max_chunks, ws, q);
+    int32_t rc = render_clear(w, h, ws, q);
+    if (rc) return rc;
+    rc = render_preprocess(s->d.pool, s->chunks_d, max_chunks, ws, q);
     if (rc) return rc;
     if (timing)
       VMS_CUDA(cudaEventRecordWithFlags(s->tev[4], q,

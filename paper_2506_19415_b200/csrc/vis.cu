@@ -85,6 +85,7 @@ __device__ __forceinline__ void face_view(const VisCamera& c, const double* vert
 __global__ void vis_count_k(const VisFrameDev* __restrict__ fd, const double* __restrict__ verts,
                             const int32_t* __restrict__ faces, uint32_t nf,
                             uint32_t* __restrict__ counts) {
+  pdl_wait();
   __shared__ VisCamera cam;
   if (threadIdx.x == 0) cam = fd->cam;
   __syncthreads();
@@ -147,6 +148,7 @@ __global__ void vis_emit_k(const VisFrameDev* __restrict__ fd, const double* __r
                            const int32_t* __restrict__ faces,
                            const uint32_t* __restrict__ face_page, uint32_t nf,
                            const uint32_t* __restrict__ offsets, VisTri* __restrict__ tris) {
+  pdl_wait();
   __shared__ VisCamera cam;
   if (threadIdx.x == 0) cam = fd->cam;
   __syncthreads();
@@ -207,6 +209,7 @@ __global__ void __launch_bounds__(kFrontThreads) vis_back_k(
     const uint32_t* __restrict__ link_off, const uint32_t* __restrict__ link_tgt,
     uint32_t page_count, const VisFrameDev* __restrict__ fd, uint32_t* __restrict__ depth_g,
     uint32_t* __restrict__ meta, RequiredOut out) {
+  pdl_wait();
   extern __shared__ uint32_t dep[];  // page_count + 1 words
   __shared__ uint32_t scratch[33];
   for (uint32_t p = threadIdx.x; p <= page_count; p += kFrontThreads) dep[p] = base[p];
@@ -257,6 +260,7 @@ __global__ void __launch_bounds__(kVisThreads) vis_raster_k(
     int w, int h, uint32_t* __restrict__ id_image, double* __restrict__ invz_image,
     int init_from_images, uint32_t page_count, uint32_t* __restrict__ page_depth,
     uint8_t* __restrict__ page_direct, uint32_t* __restrict__ err) {
+  pdl_wait();
   constexpr int kBoxes = 4;  // triangle boxes tested per thread per round
   __shared__ VisTri stri[kVisThreads];
   __shared__ uint32_t sidx[kBoxes * kVisThreads];
@@ -509,28 +513,33 @@ int32_t vis_launch(const VisArgs& a, cudaStream_t s) {
   // page sets up to kBackMaxPages: a single-CTA fused back end (links,
   // flags, compaction, LOD) after the raster
   const bool back = a.page_count <= kBackMaxPages;
+  // all memsets first: the kernels then chain with programmatic launches
   VMS_CUDA(cudaMemsetAsync(w.n_tris, 0, sizeof(uint32_t) * 4, s));
   VMS_CUDA(cudaMemsetAsync(w.base, 0, sizeof(uint32_t) * (a.page_count + 1), s));
   VMS_CUDA(cudaMemsetAsync(w.direct, 0, a.page_count + 1, s));
+  const uint32_t scan_n = a.n_faces > a.page_count + 1 ? a.n_faces : a.page_count + 1;
+  VMS_CUDA(cudaMemsetAsync(w.scan, 0, scan_ws_bytes(scan_n), s));
   if (a.n_faces) {
-    vis_count_k<<<ceil_div<uint32_t>(a.n_faces, T), T, 0, s>>>(w.fd, a.verts, a.faces,
-                                                                a.n_faces, w.counts);
+    VMS_CUDA(launch(vis_count_k, ceil_div<uint32_t>(a.n_faces, T), T, 0, s,
+                    (const VisFrameDev*)w.fd, a.verts, a.faces, a.n_faces, w.counts));
     mark("vis_count", s);
     int32_t st = scan_exclusive_u32(w.counts, w.offsets, nullptr, a.n_faces, a.n_faces, w.n_tris,
-                                    w.scan, s);
+                                    w.scan, s, false);
     if (st) return st;
-    vis_emit_k<<<ceil_div<uint32_t>(a.n_faces, T), T, 0, s>>>(
-        w.fd, a.verts, a.faces, a.face_page, a.n_faces, w.offsets, w.tris);
+    VMS_CUDA(launch(vis_emit_k, ceil_div<uint32_t>(a.n_faces, T), T, 0, s,
+                    (const VisFrameDev*)w.fd, a.verts, a.faces, a.face_page, a.n_faces,
+                    (const uint32_t*)w.offsets, w.tris));
     mark("vis_emit", s);
   }
   dim3 grid(ceil_div(a.cam.width, kVisTile), ceil_div(a.cam.height, kVisTile));
-  vis_raster_k<<<grid, kVisThreads, 0, s>>>(w.tris, w.n_tris, 0, a.cam.width, a.cam.height,
-                                            a.id_image, a.invz_image, 0, a.page_count,
-                                            w.base, w.direct, w.err);
+  VMS_CUDA(launch(vis_raster_k, grid, kVisThreads, 0, s, (const VisTri*)w.tris,
+                  (const uint32_t*)w.n_tris, 0u, a.cam.width, a.cam.height, a.id_image,
+                  a.invz_image, 0, a.page_count, w.base, w.direct, w.err));
   mark("vis_raster", s);
   if (back) {
-    vis_back_k<<<1, kFrontThreads, sizeof(uint32_t) * (a.page_count + 1), s>>>(
-        w.base, w.direct, a.link_off, a.link_tgt, a.page_count, w.fd, w.depth, w.n_tris, a.out);
+    VMS_CUDA(launch(vis_back_k, 1, kFrontThreads, sizeof(uint32_t) * (a.page_count + 1), s,
+                    (const uint32_t*)w.base, (const uint8_t*)w.direct, a.link_off, a.link_tgt,
+                    a.page_count, (const VisFrameDev*)w.fd, w.depth, w.n_tris, a.out));
     mark("vis_back", s);
   } else {
   VMS_CUDA(cudaMemcpyAsync(w.depth, w.base, sizeof(uint32_t) * (a.page_count + 1),
