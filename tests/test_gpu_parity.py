@@ -500,3 +500,25 @@ def test_c2_streamed_pages_render_identically(cuda, c2_scene):
         copied += sb["bytes_copied"]
         assert np.array_equal(ia, ib), f
     assert copied > 100 << 20
+
+
+def test_resolution_change_mid_session(cuda):
+    """Frames of one session at alternating resolutions (new workspace, new
+    frame graphs, new tile grid each switch) match the oracle frame by frame."""
+    from paper_2506_19415_b200 import scenegen
+    from paper_2506_19415_b200.runtime import VmSession
+
+    lay = scenegen.CityLayout(n_pages=40, page_size=256, levels=3, seed=5, scale=0.12)
+    sc = scenegen.city_scene(lay)
+    paths = [scenegen.street_path(lay, frames=16, width=w, height=h)
+             for w, h in ((160, 96), (250, 130), (96, 160))]
+    s = VmSession(sc, buffer_pages=16, staging_pages=6.0, vis_scale=0.5)
+    o = core.OSession(sc, buffer_pages=16, staging_pages=6.0, vis_scale=0.5)
+    for f in range(6):
+        cam = paths[f % 3].frame_camera(f)
+        img, st = s.render_frame(cam, f)
+        ref, rst = o.render_frame(cam, f)
+        assert img.shape == ref.shape
+        for k in ("required_pages", "resident_pages", "bytes_copied", "thresholds"):
+            assert st[k] == rst[k], (f, k)
+        assert _maxabs(img, ref) <= EXACT_TOL, f
