@@ -53,7 +53,7 @@ def parse():
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", choices=("ours", "reference"), default="ours")
     p.add_argument("--fast", action="store_true", help="FP32 blend (default: FP64, reference-exact)")
-    p.add_argument("--upload-mode", type=int, default=1)
+    p.add_argument("--upload-mode", type=int, default=0)
     p.add_argument("--frames", type=int, default=120, help="trajectory length")
     p.add_argument("--width", type=int, default=1920)
     p.add_argument("--height", type=int, default=1080)

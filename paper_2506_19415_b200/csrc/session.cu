@@ -156,6 +156,13 @@ struct vms_session {
   uint32_t m_cap = 0, m_want = 0;
   uint32_t m_limit = 1u << 26;  // largest tile-instance buffer the session grows to
   bool trace = false;
+  // VMSPLAT_TRACE=2: per-frame timeline (host clock + device events, no
+  // syncs), printed every kTl frames
+  static constexpr int kTl = 32;
+  bool timeline = false;
+  int tl_n = 0;
+  cudaEvent_t tl_ev[kTl][4] = {};  // vis start, vis end, render start, render end
+  double tl_host[kTl][4] = {};     // enter, vis waited, host work done, exit
   int ws_w = 0, ws_h = 0;
   char* staging = nullptr;
   size_t staging_bytes = 0;
@@ -405,6 +412,10 @@ vms_session* vms_session_create(const vms_session_desc* desc) {
   s->use_graphs = !(g && g[0] == '0');
   const char* tr = std::getenv("VMSPLAT_TRACE");
   s->trace = tr && tr[0] == '1';
+  s->timeline = tr && tr[0] == '2';
+  if (s->timeline)
+    for (auto& r : s->tl_ev)
+      for (auto& e : r) cudaEventCreate(&e);
   if (const char* ml = std::getenv("VMSPLAT_MAX_INSTANCES")) {
     const long long v = std::atoll(ml);
     if (v > 0) s->m_limit = (uint32_t)(v < 0xFFFFFFF0ll ? v : 0xFFFFFFF0ll);
@@ -496,6 +507,12 @@ int32_t vms_session_frame(vms_session* s, const vms_frame_args* a, vms_frame_sta
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   std::memset(out, 0, sizeof(*out));
   const bool timing = a->timing != 0;
+  const int tl = s->timeline ? s->tl_n % vms_session::kTl : -1;
+  auto now_us = [] {
+    return std::chrono::duration<double, std::micro>(
+               std::chrono::steady_clock::now().time_since_epoch()).count();
+  };
+  if (tl >= 0) s->tl_host[tl][0] = now_us();
   const uint32_t P = s->d.page_count;
   const int par = s->parity;
   int32_t rc = recycle(s, par);
@@ -504,6 +521,7 @@ int32_t vms_session_frame(vms_session* s, const vms_frame_args* a, vms_frame_sta
   // [1]+[2] visibility on its own high-priority stream (overlaps the renders
   // in flight); the compacted required list lands in mapped pinned memory
   if (timing) VMS_CUDA(cudaEventRecord(s->tev[0], s->vis_stream));
+  if (tl >= 0) VMS_CUDA(cudaEventRecord(s->tl_ev[tl][0], s->vis_stream));
   s->vis_fd_h->cam = a->vis_cam;
   s->vis_fd_h->lod = a->lod;
   VMS_CUDA(cudaMemcpyAsync(vis_frame_dev(s->d.vis_ws, s->d.n_faces, P), s->vis_fd_h,
@@ -528,8 +546,10 @@ int32_t vms_session_frame(vms_session* s, const vms_frame_args* a, vms_frame_sta
                     [&](cudaStream_t q, bool) { return vis_launch(v, q); }, s->vis_stream);
   if (rc) return rc;
   if (timing) VMS_CUDA(cudaEventRecord(s->tev[1], s->vis_stream));
+  if (tl >= 0) VMS_CUDA(cudaEventRecord(s->tl_ev[tl][1], s->vis_stream));
   VMS_CUDA(cudaEventRecord(s->ev_vis, s->vis_stream));
   VMS_CUDA(cudaEventSynchronize(s->ev_vis));
+  if (tl >= 0) s->tl_host[tl][1] = now_us();
   const uint32_t n_req = s->req_meta[1];
   out->n_tris = s->req_meta[0];
   if (s->req_meta[2]) {
@@ -611,6 +631,10 @@ int32_t vms_session_frame(vms_session* s, const vms_frame_args* a, vms_frame_sta
   rc = ensure_ws(s, W, H, s->m_cap > s->m_want ? s->m_cap : s->m_want);
   if (rc) return rc;
   if (timing) VMS_CUDA(cudaEventRecord(s->tev[8], st));
+  if (tl >= 0) {
+    s->tl_host[tl][2] = now_us();
+    VMS_CUDA(cudaEventRecord(s->tl_ev[tl][2], st));
+  }
   if (n_plan) {
     VMS_CUDA(cudaStreamWaitEvent(st, s->ev_copy, 0));
     dim3 grid(64, (unsigned)(n_plan < 65535 ? n_plan : 65535));
@@ -665,6 +689,25 @@ int32_t vms_session_frame(vms_session* s, const vms_frame_args* a, vms_frame_sta
   VMS_CUDA(cudaMemcpyAsync(s->counters_h[par], ws.ctr, sizeof(uint32_t) * 4,
                            cudaMemcpyDeviceToHost, st));
   VMS_CUDA(cudaEventRecord(s->ev_done[par], st));
+  if (tl >= 0) {
+    VMS_CUDA(cudaEventRecord(s->tl_ev[tl][3], st));
+    s->tl_host[tl][3] = now_us();
+    if (++s->tl_n % vms_session::kTl == 0) {
+      // frame k: host enter / vis waited / enqueue start / exit (us, relative to
+      // frame 0 enter) and device vis start-end, render start-end (us, relative
+      // to frame 0 vis start)
+      VMS_CUDA(cudaEventSynchronize(s->tl_ev[tl][3]));
+      const double h0 = 0.0;
+      for (int k = 0; k < vms_session::kTl; ++k) {
+        float d[4];
+        for (int j = 0; j < 4; ++j) cudaEventElapsedTime(&d[j], s->tl_ev[0][0], s->tl_ev[k][j]);
+        fprintf(stderr,
+                "[tl] %2d host %12.1f %12.1f %12.1f %12.1f  dev vis %8.1f %8.1f render %8.1f %8.1f\n",
+                k, s->tl_host[k][0] - h0, s->tl_host[k][1] - h0, s->tl_host[k][2] - h0,
+                s->tl_host[k][3] - h0, 1e3 * d[0], 1e3 * d[1], 1e3 * d[2], 1e3 * d[3]);
+      }
+    }
+  }
   s->pending[par] = true;
   s->last_par = par;
   if (timing) VMS_CUDA(cudaEventRecord(s->tev[9], st));

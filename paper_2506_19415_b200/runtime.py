@@ -350,8 +350,10 @@ class VmSession:
 
     Extra (non-reference) knobs: ``exact`` (default) blends with the
     reference's FP64 arithmetic, False selects the FP32 blend;
-    ``upload_mode`` 1 uploads a frame's pages with one gather kernel over
-    mapped pinned memory, 0 with one cudaMemcpyAsync per page, 2 streams them
+    ``upload_mode`` 0 (default) uploads a frame's pages from the pinned host
+    copy of the scene with one batched copy-engine call (no SM time, overlaps
+    the render in flight), 1 with one gather kernel over mapped pinned
+    memory, 2 streams them
     from the scene's memory-mapped rows (host threads gather each frame's
     pages into a page-locked bounce buffer; for scenes larger than the
     page-locked memory one wants to commit - out-of-core); ``timing``
@@ -362,7 +364,7 @@ class VmSession:
     def __init__(self, scene, buffer_pages: int = 500, staging_pages: float = 40,
                  vis_scale: float = 0.25, band=(0.5, 0.8), step: float = 0.05,
                  lod_enabled: bool = True, links_enabled: bool = True, exact: bool = True,
-                 upload_mode: int = 1, timing: bool = True, device=None,
+                 upload_mode: int = 0, timing: bool = True, device=None,
                  instance_capacity: int | None = None):
         from paper_2506_19415_b200.render import VisibilityBuffers
 
