@@ -131,7 +131,7 @@ __global__ void __launch_bounds__(1024) tile_prep_k(
     const uint32_t* __restrict__ tdiff, int tiles_x, int tiles_y, int bands, uint32_t m_cap,
     RenderCounters* __restrict__ ctr, uint32_t* __restrict__ tcount,
     uint32_t* __restrict__ ranges, uint32_t* __restrict__ order, uint32_t* __restrict__ rcounters,
-    uint32_t* __restrict__ ghist) {
+    uint32_t* __restrict__ ghist, const FrameDev* __restrict__ fd) {
   pdl_wait();
   __shared__ uint32_t h[2][256];
   __shared__ uint32_t scratch[33];
@@ -214,6 +214,13 @@ __global__ void __launch_bounds__(1024) tile_prep_k(
     if (total > m_cap) {
       ctr->overflow = 1;
       ctr->n_inst = 0;  // no lists: blend_k takes the spill path
+    }
+    uint32_t* hc = fd ? fd->counters_host : nullptr;
+    if (hc) {
+      hc[0] = ctr->n_kept;
+      hc[1] = ctr->n_inst;
+      hc[2] = ctr->overflow;
+      hc[3] = total;
     }
   }
   // schedule
@@ -664,7 +671,8 @@ int32_t tiles_and_blend(int width, int height, const uint32_t* vals, const Rende
   if (st) return st;
   const RadixLayout rl = radix_layout(w.radix_ws, w.n_cap > w.m_cap ? w.n_cap : w.m_cap);
   VMS_CUDA(launch(tile_prep_k, 1, 1024, dsm, s, (const uint32_t*)w.tdiff, tiles_x, tiles_y, nb,
-                  w.m_cap, w.ctr, w.tcount, w.ranges, w.order, rl.counters, rl.ghist));
+                  w.m_cap, w.ctr, w.tcount, w.ranges, w.order, rl.counters, rl.ghist,
+                  (const FrameDev*)(cleared ? w.fd : nullptr)));
   mark("tile_prep", s);
   VMS_CUDA(launch(dup_emit_k, 4 * kSMs, T, 0, s, vals, (const uint32_t*)w.rects,
                   (const uint32_t*)w.off, (const RenderCounters*)w.ctr, tiles_x, w.tk0, w.tv0,

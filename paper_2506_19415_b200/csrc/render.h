@@ -46,7 +46,10 @@ struct FrameDev {
   float* image;       // (h, w, 3) f32 output of this frame
   uint32_t n_chunks;  // chunk-table rows in use
   uint32_t n_splats;  // gather indices in use (resident records)
-  uint32_t pad_[2];
+  // optional host-mapped copy of the counters (n_kept, n_inst, overflow,
+  // n_need), written by tile_prep_k: no copy-engine transfer queued behind
+  // a previous frame's image copy on the main stream
+  uint32_t* counters_host;
 };
 
 // Frame counters living in device memory.

@@ -161,7 +161,7 @@ struct vms_session {
   static constexpr int kTl = 32;
   bool timeline = false;
   int tl_n = 0;
-  cudaEvent_t tl_ev[kTl][4] = {};  // vis start, vis end, render start, render end
+  cudaEvent_t tl_ev[kTl][5] = {};  // vis start, vis end, render start, render end, d2h end
   double tl_host[kTl][4] = {};     // enter, vis waited, host work done, exit
   int ws_w = 0, ws_h = 0;
   char* staging = nullptr;
@@ -515,11 +515,14 @@ int32_t vms_session_frame(vms_session* s, const vms_frame_args* a, vms_frame_sta
   if (tl >= 0) s->tl_host[tl][0] = now_us();
   const uint32_t P = s->d.page_count;
   const int par = s->parity;
-  int32_t rc = recycle(s, par);
-  if (rc) return rc;
+  int32_t rc = VMS_OK;
   s->parity ^= 1;
   // [1]+[2] visibility on its own high-priority stream (overlaps the renders
-  // in flight); the compacted required list lands in mapped pinned memory
+  // in flight); the compacted required list lands in mapped pinned memory.
+  // It touches no per-parity buffer, so it starts before the frame two back
+  // (same parity) is recycled: that frame's image copy to the host and the
+  // visibility pass, which queues behind the render in flight for SM slots,
+  // then overlap instead of adding up.
   if (timing) VMS_CUDA(cudaEventRecord(s->tev[0], s->vis_stream));
   if (tl >= 0) VMS_CUDA(cudaEventRecord(s->tl_ev[tl][0], s->vis_stream));
   s->vis_fd_h->cam = a->vis_cam;
@@ -562,6 +565,9 @@ int32_t vms_session_frame(vms_session* s, const vms_frame_args* a, vms_frame_sta
   rc = vms_pt_update(s->pt, s->req_pid, s->req_enc, s->req_direct, s->req_level, n_req, a->frame,
                      a->budget, s->plan_pid.data(), s->plan_level.data(), s->plan_entry.data(),
                      s->plan_slot.data(), (int64_t)s->plan_pid.size(), &n_plan, &missing);
+  if (rc) return rc;
+  // the frame two back (this parity): its host copies, counters, image
+  rc = recycle(s, par);
   if (rc) return rc;
   // copy plan: scene rows -> packed staging, staging -> pool slot rows
   uint64_t bytes = 0;
@@ -649,6 +655,7 @@ int32_t vms_session_frame(vms_session* s, const vms_frame_args* a, vms_frame_sta
   f->image = a->image;
   f->n_chunks = (uint32_t)n_chunks;
   f->n_splats = (uint32_t)n_res;
+  f->counters_host = s->counters_h[par];  // mapped: written by tile_prep_k
   VMS_CUDA(cudaMemcpyAsync(ws.fd, f, sizeof(FrameDev), cudaMemcpyHostToDevice, st));
   if (n_chunks)
     VMS_CUDA(cudaMemcpyAsync(s->chunks_d, s->chunks_h[par], sizeof(vms_chunk) * n_chunks,
@@ -669,6 +676,7 @@ int32_t vms_session_frame(vms_session* s, const vms_frame_args* a, vms_frame_sta
     VMS_CUDA(cudaMemcpyAsync(a->host_image, a->image, sizeof(float) * 3 * (size_t)W * H,
                              cudaMemcpyDeviceToHost, s->d2h_stream));
     VMS_CUDA(cudaEventRecord(s->ev_out[par], s->d2h_stream));
+    if (tl >= 0) VMS_CUDA(cudaEventRecord(s->tl_ev[tl][4], s->d2h_stream));
     s->pending_out[par] = true;
   }
   if (banded) {
@@ -686,8 +694,6 @@ int32_t vms_session_frame(vms_session* s, const vms_frame_args* a, vms_frame_sta
     VMS_CUDA(cudaEventRecord(s->ev_d2h, s->d2h_stream));
     VMS_CUDA(cudaStreamWaitEvent(st, s->ev_d2h, 0));
   }
-  VMS_CUDA(cudaMemcpyAsync(s->counters_h[par], ws.ctr, sizeof(uint32_t) * 4,
-                           cudaMemcpyDeviceToHost, st));
   VMS_CUDA(cudaEventRecord(s->ev_done[par], st));
   if (tl >= 0) {
     VMS_CUDA(cudaEventRecord(s->tl_ev[tl][3], st));
@@ -699,12 +705,13 @@ int32_t vms_session_frame(vms_session* s, const vms_frame_args* a, vms_frame_sta
       VMS_CUDA(cudaEventSynchronize(s->tl_ev[tl][3]));
       const double h0 = 0.0;
       for (int k = 0; k < vms_session::kTl; ++k) {
-        float d[4];
-        for (int j = 0; j < 4; ++j) cudaEventElapsedTime(&d[j], s->tl_ev[0][0], s->tl_ev[k][j]);
+        float d[5] = {0, 0, 0, 0, 0};
+        for (int j = 0; j < 5; ++j) cudaEventElapsedTime(&d[j], s->tl_ev[0][0], s->tl_ev[k][j]);
         fprintf(stderr,
-                "[tl] %2d host %12.1f %12.1f %12.1f %12.1f  dev vis %8.1f %8.1f render %8.1f %8.1f\n",
+                "[tl] %2d host %12.1f %12.1f %12.1f %12.1f  dev vis %8.1f %8.1f render %8.1f %8.1f"
+                " d2h end %8.1f\n",
                 k, s->tl_host[k][0] - h0, s->tl_host[k][1] - h0, s->tl_host[k][2] - h0,
-                s->tl_host[k][3] - h0, 1e3 * d[0], 1e3 * d[1], 1e3 * d[2], 1e3 * d[3]);
+                s->tl_host[k][3] - h0, 1e3 * d[0], 1e3 * d[1], 1e3 * d[2], 1e3 * d[3], 1e3 * d[4]);
       }
     }
   }

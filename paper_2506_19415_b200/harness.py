@@ -122,9 +122,9 @@ def run_benchmark(scene, path, config: BenchConfig | None = None, frame_sink=Non
     (float32 (h, w, 3) host array); frames are not kept otherwise.
     B200 extensions: ``frames`` restricts the run to those frame indices, in
     order (a shard of the path); ``session`` reuses an existing one;
-    ``pipelined`` submits frame i + 1 before handing frame i to the sink, so
-    each frame's transfer to the host overlaps the next frame's render (the
-    durations are then not measured: zeros)."""
+    ``pipelined`` submits frames i + 1 and i + 2 before handing frame i to
+    the sink, so each frame's transfer to the host overlaps the next frame's
+    visibility pass and render (the durations are then not measured: zeros)."""
     cfg = config or BenchConfig()
     if scene.page_count == 0:
         raise DataError("benchmark needs a paged scene")
@@ -140,19 +140,23 @@ def run_benchmark(scene, path, config: BenchConfig | None = None, frame_sink=Non
             if frame_sink is not None:
                 frame_sink(i, image)
         return out
-    held = None  # (index, image) submitted, not yet handed over
+    # frames i - 1 and i in flight after submitting i: the session recycles
+    # frame i - 2 (its image copy complete) inside render_frame(i), so that
+    # frame goes to the sink without a wait, and each frame's copy to the host
+    # overlaps both the next render and the next visibility pass
+    held = []  # (index, image) submitted, not yet handed over, oldest first
     for i in indices:
         image, st = s.render_frame(path.frame_camera(i), i, wait=False)
         out.append(FrameStats.from_session(i, {**st, **{f"time_{k}": 0.0 for k in STAGES}}))
-        if held is not None:
-            s.wait(1)
+        if len(held) == 2:
+            done = held.pop(0)
             if frame_sink is not None:
-                frame_sink(*held)
-        held = (i, image)
-    if held is not None:
-        s.wait(0)
+                frame_sink(*done)
+        held.append((i, image))
+    for k, done in enumerate(held):
+        s.wait(len(held) - 1 - k)
         if frame_sink is not None:
-            frame_sink(*held)
+            frame_sink(*done)
     return out
 
 
