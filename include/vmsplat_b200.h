@@ -182,6 +182,21 @@ size_t vms_radix_workspace_bytes(int64_t n);
 int32_t vms_radix_sort_pairs(uint32_t* keys, int64_t* values, int64_t n, void* workspace,
                              size_t workspace_bytes, void* stream);
 
+/* bvh_nearest_points (kernels/__init__.py:54-63, _core.pyx:279-334): nearest
+ * face per query point over the flat median-split BVH of mesh/geometry.py
+ * FaceBvh (bounds (n_nodes, 6) f64 lo|hi, children (n_nodes, 2) i32 with
+ * (-1, -1) for leaves, ranges (n_nodes, 2) i32 half-open spans of tri_order,
+ * tri_verts (n_faces, 3, 3) f64).  out_face i64 (lowest face index on
+ * distance ties), out_dist f64 - bit-identical to the reference.  All
+ * pointers are device memory; *overflow (device i32) is set when a query
+ * needs more than the reference's 128-entry traversal stack (the reference
+ * raises RuntimeError; so does the Python wrapper). */
+int32_t vms_bvh_nearest_points(const double* points, int64_t n_points, const double* bounds,
+                               const int32_t* children, const int32_t* ranges, int64_t n_nodes,
+                               const int32_t* tri_order, const double* tri_verts,
+                               int64_t n_faces, int64_t* out_face, double* out_dist,
+                               int32_t* overflow, void* stream);
+
 /* Camera.world_to_view (render.py:79-81) on the device; also the probe that
  * picks dot_mode against the host BLAS. out (n, 3) f64. */
 int32_t vms_world_to_view(const double* points, int64_t n, const vms_camera* cam, double* out,

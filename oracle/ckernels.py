@@ -38,8 +38,9 @@ def _load():
         lib.oracle_composite_splats.argtypes = [P, P, P, P, P, I, P, I, I]
         lib.oracle_rasterize_triangles.argtypes = [P, P, I, P, P, I, I]
         lib.oracle_radix_sort_pairs.argtypes = [P, P, I]
+        lib.oracle_nearest_faces.argtypes = [P, I, P, I, P, P]
         for f in (lib.oracle_composite_splats, lib.oracle_rasterize_triangles,
-                  lib.oracle_radix_sort_pairs):
+                  lib.oracle_radix_sort_pairs, lib.oracle_nearest_faces):
             f.restype = ctypes.c_int
         _lib = lib
     return _lib
@@ -78,3 +79,15 @@ def radix_sort_pairs(keys, values):
     if lib.oracle_radix_sort_pairs(_p(k), _p(v), len(k)) != 0:
         raise MemoryError("oracle radix")
     return k, v
+
+
+def nearest_faces(points, tri_verts):
+    """(faces int64, distances float64) per point: the answer of
+    bvh_nearest_points (kernels/_core.pyx:279-334) by brute force."""
+    lib = _load()
+    pts = np.ascontiguousarray(points, dtype=np.float64).reshape(-1, 3)
+    tv = np.ascontiguousarray(tri_verts, dtype=np.float64).reshape(-1, 3, 3)
+    face = np.empty(len(pts), np.int64)
+    dist = np.empty(len(pts), np.float64)
+    lib.oracle_nearest_faces(_p(pts), len(pts), _p(tv), len(tv), _p(face), _p(dist))
+    return face, dist

@@ -164,3 +164,65 @@ int oracle_radix_sort_pairs(uint32_t *keys, int64_t *values, int64_t n) {
   free(v2);
   return 0;
 }
+
+/* Nearest face per point (kernels/_core.pyx:279-334, distance :208-258).
+ * Brute force over every face instead of the BVH walk: the reference's
+ * answer does not depend on the tree (boxes at equal distance are never
+ * pruned, ties go to the lowest face index), so this pins both the distance
+ * arithmetic and that claim.  Compiled with -ffp-contract=off like the
+ * reference. */
+static double o_d2(double x, double y, double z) { return x * x + y * y + z * z; }
+
+static double o_point_tri(double px, double py, double pz, const double *t) {
+  double ax = t[0], ay = t[1], az = t[2], bx = t[3], by = t[4], bz = t[5];
+  double cx = t[6], cy = t[7], cz = t[8];
+  double abx = bx - ax, aby = by - ay, abz = bz - az;
+  double acx = cx - ax, acy = cy - ay, acz = cz - az;
+  double apx = px - ax, apy = py - ay, apz = pz - az;
+  double d1 = abx * apx + aby * apy + abz * apz;
+  double d2 = acx * apx + acy * apy + acz * apz;
+  if (d1 <= 0.0 && d2 <= 0.0) return o_d2(apx, apy, apz);
+  double bpx = px - bx, bpy = py - by, bpz = pz - bz;
+  double d3 = abx * bpx + aby * bpy + abz * bpz;
+  double d4 = acx * bpx + acy * bpy + acz * bpz;
+  if (d3 >= 0.0 && d4 <= d3) return o_d2(bpx, bpy, bpz);
+  double vc = d1 * d4 - d3 * d2;
+  if (vc <= 0.0 && d1 >= 0.0 && d3 <= 0.0) {
+    double v = d1 / (d1 - d3);
+    return o_d2(apx - v * abx, apy - v * aby, apz - v * abz);
+  }
+  double cpx = px - cx, cpy = py - cy, cpz = pz - cz;
+  double d5 = abx * cpx + aby * cpy + abz * cpz;
+  double d6 = acx * cpx + acy * cpy + acz * cpz;
+  if (d6 >= 0.0 && d5 <= d6) return o_d2(cpx, cpy, cpz);
+  double vb = d5 * d2 - d1 * d6;
+  if (vb <= 0.0 && d2 >= 0.0 && d6 <= 0.0) {
+    double w = d2 / (d2 - d6);
+    return o_d2(apx - w * acx, apy - w * acy, apz - w * acz);
+  }
+  double va = d3 * d6 - d5 * d4;
+  if (va <= 0.0 && (d4 - d3) >= 0.0 && (d5 - d6) >= 0.0) {
+    double w = (d4 - d3) / ((d4 - d3) + (d5 - d6));
+    return o_d2(px - (bx + w * (cx - bx)), py - (by + w * (cy - by)), pz - (bz + w * (cz - bz)));
+  }
+  double denom = 1.0 / (va + vb + vc);
+  double v = vb * denom, w = vc * denom;
+  return o_d2(px - (ax + abx * v + acx * w), py - (ay + aby * v + acy * w),
+              pz - (az + abz * v + acz * w));
+}
+
+int oracle_nearest_faces(const double *points, int64_t nq, const double *tri_verts,
+                         int64_t nf, int64_t *out_face, double *out_dist) {
+  for (int64_t q = 0; q < nq; ++q) {
+    const double *p = points + 3 * q;
+    double best = INFINITY;
+    int64_t bf = -1;
+    for (int64_t f = 0; f < nf; ++f) {
+      double d = o_point_tri(p[0], p[1], p[2], tri_verts + 9 * f);
+      if (d < best) { best = d; bf = f; }  /* ascending f: the first minimum wins */
+    }
+    out_face[q] = bf;
+    out_dist[q] = sqrt(best);
+  }
+  return 0;
+}

@@ -139,6 +139,7 @@ SIGNATURES = {
     "vms_session_wait": (I32, [P, I32]),
     "vms_host_accessible": (I32, [P]),
     "vms_debug_blend_trace": (I32, [P]),
+    "vms_bvh_nearest_points": (I32, [P, I64, P, P, P, I64, P, P, I64, P, P, P, P]),
 }
 
 _lib = None

@@ -28,6 +28,7 @@ UNITS = {
     "blend.cu": [],
     "abi.cu": [],
     "session.cu": [],
+    "bvh.cu": ["-fmad=false"],
 }
 HOST_UNITS = {"pagetable.cpp": ["-O2", "-std=c++17", "-fPIC"]}
 HEADERS = ["common.cuh", "prims.h", "render.h", "vis.h"]

@@ -114,4 +114,38 @@ def radix_sort_pairs(keys, values):
     return k.cpu().numpy(), v.cpu().numpy()
 
 
-__all__ = ["BACKEND", "composite_splats", "rasterize_triangles", "radix_sort_pairs"]
+def bvh_nearest_points(points, bounds, children, ranges, tri_order, tri_verts):
+    """Nearest mesh face (int64, lowest index on ties) and its distance
+    (float64) for each query point, over the flat BVH arrays of
+    ``geometry.FaceBvh`` (kernels/__init__.py:54-63, _core.pyx:279-334).
+    Raises RuntimeError when a query overflows the 128-entry traversal
+    stack, as the reference does."""
+    t = _device.require_cuda()
+    on_dev = _device.is_torch(points) and points.is_cuda
+    pts = _device.to_dev(points, np.float64).reshape(-1, 3)
+    bnd = _device.to_dev(bounds, np.float64).reshape(-1, 6)
+    ch = _device.to_dev(children, np.int32).reshape(-1, 2)
+    rg = _device.to_dev(ranges, np.int32).reshape(-1, 2)
+    order = _device.to_dev(tri_order, np.int32).reshape(-1)
+    tv = _device.to_dev(tri_verts, np.float64).reshape(-1, 3, 3)
+    if len(bnd) != len(ch) or len(bnd) != len(rg) or len(bnd) == 0 or len(tv) == 0:
+        raise ValueError("bvh_nearest_points: inconsistent BVH arrays")
+    n = int(pts.shape[0])
+    face = t.empty(n, dtype=t.int64, device=pts.device)
+    dist = t.empty(n, dtype=t.float64, device=pts.device)
+    flag = t.zeros(1, dtype=t.int32, device=pts.device)
+    lib = _lib.load()
+    _lib.check(lib.vms_bvh_nearest_points(pts.data_ptr(), n, bnd.data_ptr(), ch.data_ptr(),
+                                          rg.data_ptr(), len(bnd), order.data_ptr(),
+                                          tv.data_ptr(), len(tv), face.data_ptr(),
+                                          dist.data_ptr(), flag.data_ptr(), _device.sptr()),
+               "bvh_nearest_points")
+    if int(flag.item()):
+        raise RuntimeError("BVH traversal stack overflow")
+    if on_dev:
+        return face, dist
+    return face.cpu().numpy(), dist.cpu().numpy()
+
+
+__all__ = ["BACKEND", "composite_splats", "rasterize_triangles", "radix_sort_pairs",
+           "bvh_nearest_points"]

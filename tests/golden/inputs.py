@@ -41,6 +41,36 @@ def random_tris(seed, t=120):
     return tris, ids
 
 
+def bvh_cases():
+    """Nearest-face query inputs (kernels/_core.pyx:279-334): (name, tri_verts
+    (F, 3, 3) f64, points (Q, 3) f64)."""
+    rng = np.random.default_rng(21)
+    out = []
+    # random triangles in a box, queries inside and around it
+    a = rng.uniform(-5.0, 5.0, (600, 1, 3))
+    tv = a + rng.normal(0.0, 0.6, (600, 3, 3))
+    pts = rng.uniform(-7.0, 7.0, (3000, 3))
+    out.append(("random", tv, pts))
+    # a regular grid of quads (two triangles each): queries on shared
+    # vertices and edges and above cell centres give exact distance ties
+    n = 24
+    g = np.stack(np.meshgrid(np.arange(n + 1.0), np.arange(n + 1.0), indexing="ij"), -1)
+    v = np.concatenate([g.reshape(-1, 2), np.zeros(((n + 1) ** 2, 1))], 1)
+    idx = np.arange((n + 1) ** 2).reshape(n + 1, n + 1)
+    f = []
+    for i in range(n):
+        for j in range(n):
+            f.append((idx[i, j], idx[i + 1, j], idx[i + 1, j + 1]))
+            f.append((idx[i, j], idx[i + 1, j + 1], idx[i, j + 1]))
+    tv = v[np.array(f)]
+    q = rng.integers(0, n + 1, (1500, 2)).astype(np.float64)
+    half = rng.integers(0, 2, (1500, 2)) * 0.5
+    h = rng.choice([0.0, 0.25, -1.0, 3.0], 1500)[:, None]
+    pts = np.concatenate([q + half, h], 1)
+    out.append(("grid", tv, pts))
+    return out
+
+
 def random_keys(seed, n):
     rng = np.random.default_rng(seed)
     keys = rng.integers(0, 2 ** 32, size=n, dtype=np.uint64).astype(np.uint32)

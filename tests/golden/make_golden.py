@@ -199,6 +199,36 @@ def c1_golden():
     np.savez_compressed(os.path.join(HERE, "c1.npz"), **out)
 
 
+def bvh_golden():
+    """Nearest-face queries: the reference's BVH arrays and answers."""
+    from vmsplat.mesh.geometry import FaceBvh
+
+    out = {}
+    for name, tv, pts in inputs.bvh_cases():
+        bvh = FaceBvh(tv)
+        faces, dist = bvh.nearest(pts)
+        out[f"{name}_tri_verts"] = tv
+        out[f"{name}_points"] = pts
+        out[f"{name}_bounds"] = bvh.bounds
+        out[f"{name}_children"] = bvh.children
+        out[f"{name}_ranges"] = bvh.ranges
+        out[f"{name}_order"] = bvh.order
+        out[f"{name}_faces"] = faces
+        out[f"{name}_dist"] = dist
+    # the city proxy mesh, queried at the scene's record positions
+    from paper_2506_19415_b200 import scenegen
+
+    sc = scenegen.city_scene(inputs.CITY_SMALL)
+    tv = np.asarray(sc.vertices, np.float64)[np.asarray(sc.faces, np.int64)]
+    pts = np.asarray(sc.gaussians[::7, 0:3], np.float64)
+    faces, dist = FaceBvh(tv).nearest(pts)
+    out["city_tri_verts"] = tv
+    out["city_points"] = pts
+    out["city_faces"] = faces
+    out["city_dist"] = dist
+    np.savez_compressed(os.path.join(HERE, "bvh.npz"), **out)
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["kernels", "render", "pagetable", "city", "c1"]
     for w in which:

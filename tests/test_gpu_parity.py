@@ -522,3 +522,76 @@ def test_resolution_change_mid_session(cuda):
         for k in ("required_pages", "resident_pages", "bytes_copied", "thresholds"):
             assert st[k] == rst[k], (f, k)
         assert _maxabs(img, ref) <= EXACT_TOL, f
+
+
+# -- nearest-face queries -------------------------------------
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", ["random", "grid"])
+def test_bvh_nearest_points_bit_exact(cuda, golden, case):
+    """kernels.bvh_nearest_points on the reference's own BVH arrays
+    (_core.pyx:279-334): faces and distances bit for bit, ties included."""
+    from paper_2506_19415_b200 import kernels
+
+    g = golden["bvh"]
+    faces, dist = kernels.bvh_nearest_points(
+        g[f"{case}_points"], g[f"{case}_bounds"], g[f"{case}_children"], g[f"{case}_ranges"],
+        g[f"{case}_order"], g[f"{case}_tri_verts"])
+    assert faces.dtype == np.int64 and dist.dtype == np.float64
+    assert np.array_equal(faces, g[f"{case}_faces"])
+    assert np.array_equal(dist.view(np.uint64), g[f"{case}_dist"].view(np.uint64))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", ["random", "grid", "city"])
+def test_face_bvh_nearest_matches_reference(cuda, golden, case):
+    """geometry.FaceBvh (host build) + the CUDA query against the
+    reference's answers, and against the brute-force oracle."""
+    from oracle import ckernels
+    from paper_2506_19415_b200.geometry import FaceBvh
+
+    g = golden["bvh"]
+    pts, tv = g[f"{case}_points"], g[f"{case}_tri_verts"]
+    faces, dist = FaceBvh(tv).nearest(pts)
+    assert np.array_equal(faces, g[f"{case}_faces"])
+    assert np.array_equal(dist.view(np.uint64), g[f"{case}_dist"].view(np.uint64))
+    of, od = ckernels.nearest_faces(pts[:200], tv)
+    assert np.array_equal(faces[:200], of) and np.array_equal(dist[:200], od)
+
+
+@pytest.mark.gpu
+def test_bvh_large_mesh_and_edge_cases(cuda):
+    """A 50 K-face mesh (deep tree) against the brute-force oracle on a
+    sample; no queries; a chain-shaped tree deeper than the reference's
+    128-entry stack raises RuntimeError like the reference."""
+    from oracle import ckernels
+    from paper_2506_19415_b200 import kernels
+    from paper_2506_19415_b200.geometry import FaceBvh
+
+    rng = np.random.default_rng(5)
+    tv = rng.uniform(-50, 50, (50000, 1, 3)) + rng.normal(0, 0.5, (50000, 3, 3))
+    pts = rng.uniform(-60, 60, (20000, 3))
+    bvh = FaceBvh(tv)
+    faces, dist = bvh.nearest(pts)
+    of, od = ckernels.nearest_faces(pts[::50], tv)
+    assert np.array_equal(faces[::50], of)
+    assert np.array_equal(dist[::50].view(np.uint64), od.view(np.uint64))
+    f0, d0 = bvh.nearest(np.zeros((0, 3)))
+    assert f0.shape == (0,) and d0.shape == (0,)
+    # chain: node k (internal) -> (leaf, node k + 2); depth 140
+    depth = 140
+    n_nodes = 2 * depth + 1
+    children = np.full((n_nodes, 2), -1, np.int32)
+    ranges = np.zeros((n_nodes, 2), np.int32)
+    for k in range(depth):
+        children[2 * k] = (2 * k + 1, 2 * k + 2)
+        ranges[2 * k] = (0, 1)
+        ranges[2 * k + 1] = (0, 1)
+    ranges[2 * depth] = (0, 1)
+    # internal boxes hold the query, leaf boxes are farther: every level
+    # descends before any leaf pops, so the stack grows by one per level
+    bounds = np.tile(np.array([0.0, 0, 0, 10, 10, 10]), (n_nodes, 1))
+    bounds[1::2] = (100.0, 100, 100, 101, 101, 101)
+    tri = np.array([[[0.0, 0, 0], [1, 0, 0], [0, 1, 0]]])
+    with pytest.raises(RuntimeError, match="stack overflow"):
+        kernels.bvh_nearest_points(np.array([[5.0, 5.0, 5.0]]), bounds, children, ranges,
+                                   np.zeros(1, np.int32), tri)

@@ -126,3 +126,30 @@ def test_oracle_c1_session_matches_reference(golden):
         stats.append(st)
         assert hashlib.sha256(img.tobytes()).digest() == g[f"image_sha_{f}"].tobytes(), f
     assert core.stats_csv(stats).encode() == g["stats"].tobytes()
+
+
+# -- nearest-face queries -----------------------------------
+@pytest.mark.parametrize("case", ["random", "grid", "city"])
+def test_oracle_nearest_faces_match_reference(golden, case):
+    """kernels/_core.pyx:279-334 by brute force: faces (ties -> lowest index,
+    the grid case has many) and distances bit for bit."""
+    from oracle import ckernels
+
+    g = golden["bvh"]
+    faces, dist = ckernels.nearest_faces(g[f"{case}_points"], g[f"{case}_tri_verts"])
+    assert np.array_equal(faces, g[f"{case}_faces"])
+    assert np.array_equal(dist.view(np.uint64), g[f"{case}_dist"].view(np.uint64))
+
+
+@pytest.mark.parametrize("case", ["random", "grid"])
+def test_face_bvh_arrays_match_reference(golden, case):
+    """geometry.FaceBvh builds mesh/geometry.py:86-142's flat BVH exactly
+    (node numbering, boxes, spans, face order) - host code, no GPU."""
+    from paper_2506_19415_b200.geometry import FaceBvh
+
+    g = golden["bvh"]
+    b = FaceBvh(g[f"{case}_tri_verts"])
+    assert np.array_equal(b.bounds, g[f"{case}_bounds"])
+    assert np.array_equal(b.children, g[f"{case}_children"])
+    assert np.array_equal(b.ranges, g[f"{case}_ranges"])
+    assert np.array_equal(b.order, g[f"{case}_order"])
