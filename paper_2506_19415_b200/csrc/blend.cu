@@ -347,20 +347,32 @@ struct SplatF64 {
 // 2^(j/64) as double-double, j = 0..63
 __constant__ double2 kExp2Tab[64];
 
+// FP64 constants of the exact blend in the constant bank: DFMA/DMUL/DSETP
+// take them as c[][] operands, where literals that do not fit an immediate
+// would be rematerialised with uniform moves on every pixel-splat.
+__constant__ double kBlendC[10] = {
+    0x1.71547652b82fep+6,   // 0: 64 / ln2
+    0x1.8p52,               // 1: round-to-integer magic
+    -0x1.62e4200000000p-7,  // 2: -ln2/64, 21 leading bits (k * kLhi exact)
+    -0x1.fdf473de6af28p-28, // 3: -(ln2/64 - kLhi)
+    1.0 / 120.0,            // 4
+    1.0 / 24.0,             // 5
+    1.0 / 6.0,              // 6
+    1.0 / 255.0,            // 7: stop threshold (_core.pyx:60)
+    0.99,                   // 8: weight clamp (_core.pyx:70)
+    0.5,                    // 9
+};
+
 __device__ __forceinline__ double exp_tab(double x, const double2* __restrict__ tab) {
   // exp(x), x in [-700, 0]: x = (64 m + j) ln2/64 + r, |r| <= ln2/128
-  const double kInvL = 0x1.71547652b82fep+6;  // 64 / ln2
-  const double kLhi = 0x1.62e4200000000p-7;   // ln2/64, 21 leading bits (k * kLhi exact)
-  const double kLlo = 0x1.fdf473de6af28p-28;  // ln2/64 - kLhi
-  const double kMagic = 0x1.8p52;
-  const double t = __fma_rn(x, kInvL, kMagic);
+  const double t = __fma_rn(x, kBlendC[0], kBlendC[1]);
   const int k = __double2loint(t);
-  const double kd = __dsub_rn(t, kMagic);
-  double r = __fma_rn(kd, -kLhi, x);
-  r = __fma_rn(kd, -kLlo, r);
-  double q = __fma_rn(1.0 / 120.0, r, 1.0 / 24.0);
-  q = __fma_rn(q, r, 1.0 / 6.0);
-  q = __fma_rn(q, r, 0.5);
+  const double kd = __dsub_rn(t, kBlendC[1]);
+  double r = __fma_rn(kd, kBlendC[2], x);
+  r = __fma_rn(kd, kBlendC[3], r);
+  double q = __fma_rn(kBlendC[4], r, kBlendC[5]);
+  q = __fma_rn(q, r, kBlendC[6]);
+  q = __fma_rn(q, r, kBlendC[9]);
   q = __fma_rn(q, r, 1.0);
   const double sr = __dmul_rn(q, r);  // exp(r) - 1
   const double2 tj = tab[k & 63];
@@ -488,7 +500,7 @@ __global__ void __launch_bounds__(kBlendThreads) blend_k(const uint32_t* __restr
           if (px < s.x0 || px >= s.x1 || py < s.y0 || py >= s.y1) continue;
           // _core.pyx:56-78: FP64 arithmetic, f32 storage of T and colour
           const double t = (double)T;
-          if (t < 1.0 / 255.0) {
+          if (t < kBlendC[7]) {
             done = true;
             continue;
           }
@@ -501,7 +513,7 @@ __global__ void __launch_bounds__(kBlendThreads) blend_k(const uint32_t* __restr
           // < 2^-36 (far tails of elongated splats) - skip the exp
           if (sig < s.skip) continue;
           double wgt = __dmul_rn(s.al, exp_tab(sig, tab));
-          if (wgt > 0.99) wgt = 0.99;
+          if (wgt > kBlendC[8]) wgt = kBlendC[8];
           const double wt = __dmul_rn(wgt, t);
           cr = __double2float_rn(__dadd_rn((double)cr, __dmul_rn(wt, s.r)));
           cg = __double2float_rn(__dadd_rn((double)cg, __dmul_rn(wt, s.g)));
