@@ -350,6 +350,8 @@ __constant__ double2 kExp2Tab[64];
 // FP64 constants of the exact blend in the constant bank: DFMA/DMUL/DSETP
 // take them as c[][] operands, where literals that do not fit an immediate
 // would be rematerialised with uniform moves on every pixel-splat.
+constexpr float kStopF = 0x1.010102p-8f;  // RN32(1/255) = smallest float >= 1/255
+
 __constant__ double kBlendC[10] = {
     0x1.71547652b82fep+6,   // 0: 64 / ln2
     0x1.8p52,               // 1: round-to-integer magic
@@ -391,7 +393,7 @@ __device__ unsigned long long* g_blend_trace = nullptr;
 // same per-tile order, so the image is identical, only slower.  The host
 // sees the overflow counter afterwards and grows the buffer for later frames.
 template <bool kExact, int TS>
-__global__ void __launch_bounds__(kBlendThreads) blend_k(const uint32_t* __restrict__ ranges,
+__global__ void __launch_bounds__(kBlendThreads, 4) blend_k(const uint32_t* __restrict__ ranges,
                                                          const uint32_t* __restrict__ order,
                                                          const uint32_t* __restrict__ tv_tiles,
                                                          const uint32_t* __restrict__ vals,
@@ -425,17 +427,19 @@ __global__ void __launch_bounds__(kBlendThreads) blend_k(const uint32_t* __restr
   const uint32_t end = spill ? ctr->n_kept : ranges[2 * tile + 1];
   const uint32_t* __restrict__ tv = spill ? vals : tv_tiles;
   float* __restrict__ image = image_arg ? image_arg : fd->image;
-  float cr = 0.f, cg = 0.f, cb = 0.f, T = 1.f;
+  // a pixel is finished once T < 1/255 (the reference's stop test, exactly:
+  // for f32 T, T < 1/255 in FP64 <=> T < RN32(1/255)); pixels outside the
+  // image start finished
+  float cr = 0.f, cg = 0.f, cb = 0.f, T = inside ? 1.f : 0.f;
   if (accumulate && inside) {
     const float* p = image + ((size_t)py * w + px) * 3;
     cr = p[0];
     cg = p[1];
     cb = p[2];
   }
-  bool done = !inside;
   const double fx = (double)px + 0.5, fy = (double)py + 0.5;
   for (uint32_t base = start; base < end; base += kBlendThreads) {
-    if (__syncthreads_and(done)) break;
+    if (__syncthreads_and(T < kStopF)) break;
     const uint32_t i = base + threadIdx.x;
     bool hit = false;
     BlendRec r;
@@ -460,9 +464,10 @@ __global__ void __launch_bounds__(kBlendThreads) blend_k(const uint32_t* __restr
         SplatF64 d;
         d.cx = r.cx;
         d.cy = r.cy;
-        d.ca = r.ca;
-        d.cb2 = 2.0 * (double)r.cb;  // exact: power-of-two scaling
-        d.cc = r.cc;
+        // sigma's -0.5 folded into the conic: power-of-two scalings are exact
+        d.ca = -0.5 * (double)r.ca;
+        d.cb2 = -(double)r.cb;
+        d.cc = -0.5 * (double)r.cc;
         d.al = r.alpha;
         d.skip = r.skip;
         d.r = r.r;
@@ -479,7 +484,7 @@ __global__ void __launch_bounds__(kBlendThreads) blend_k(const uint32_t* __restr
     }
     __syncthreads();
     // this warp: the staged splats touching its 8x4 block, 32 at a time
-    for (uint32_t c0 = 0; c0 < cnt && !__all_sync(0xffffffffu, done); c0 += 32) {
+    for (uint32_t c0 = 0; c0 < cnt && !__all_sync(0xffffffffu, T < kStopF); c0 += 32) {
       bool mine = false;
       if (c0 + lane < cnt) {
         const Staged& q = sp[c0 + lane];
@@ -495,20 +500,16 @@ __global__ void __launch_bounds__(kBlendThreads) blend_k(const uint32_t* __restr
       while (m) {
         const Staged& s = sp[c0 + __ffs(m) - 1];
         m &= m - 1;
-        if (done) continue;
+        if (T < kStopF) continue;
         if constexpr (kExact) {
           if (px < s.x0 || px >= s.x1 || py < s.y0 || py >= s.y1) continue;
           // _core.pyx:56-78: FP64 arithmetic, f32 storage of T and colour
           const double t = (double)T;
-          if (t < kBlendC[7]) {
-            done = true;
-            continue;
-          }
           const double dx = __dsub_rn(fx, s.cx);
           const double dy = __dsub_rn(fy, s.cy);
-          const double sig = -0.5 * __dadd_rn(__dadd_rn(__dmul_rn(__dmul_rn(s.ca, dx), dx),
-                                                        __dmul_rn(__dmul_rn(s.cb2, dy), dx)),
-                                              __dmul_rn(__dmul_rn(s.cc, dy), dy));
+          const double sig = __dadd_rn(__dadd_rn(__dmul_rn(__dmul_rn(s.ca, dx), dx),
+                                                 __dmul_rn(__dmul_rn(s.cb2, dy), dx)),
+                                       __dmul_rn(__dmul_rn(s.cc, dy), dy));
           // weight < 2^-36: T is unchanged bit for bit and the colour moves by
           // < 2^-36 (far tails of elongated splats) - skip the exp
           if (sig < s.skip) continue;
@@ -522,10 +523,6 @@ __global__ void __launch_bounds__(kBlendThreads) blend_k(const uint32_t* __restr
         } else {
           const int x0 = s.bx & 0xFFFF, x1 = s.bx >> 16, y0 = s.by & 0xFFFF, y1 = s.by >> 16;
           if (px < x0 || px >= x1 || py < y0 || py >= y1) continue;
-          if (T < (1.0f / 255.0f)) {
-            done = true;
-            continue;
-          }
           const float dx = ((float)px + 0.5f) - s.cx, dy = ((float)py + 0.5f) - s.cy;
           const float sig = -0.5f * (s.ca * dx * dx + 2.0f * s.cb * dy * dx + s.cc * dy * dy);
           const float wgt = fminf(s.alpha * __expf(sig), 0.99f);
@@ -537,7 +534,6 @@ __global__ void __launch_bounds__(kBlendThreads) blend_k(const uint32_t* __restr
         }
       }
     }
-    if (!done && T < (1.0f / 255.0f)) done = true;
     __syncthreads();
   }
   // output: the 16x16 block goes through shared memory and out as whole
