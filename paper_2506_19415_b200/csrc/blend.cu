@@ -341,7 +341,7 @@ __global__ void __launch_bounds__(kEmitThreads) dup_emit_k(
 struct SplatF64 {
   double cx, cy, ca, cb2, cc, al, r, g, b;
   double skip;  // sigma below which alpha * exp(sigma) < 2^-36 (no effect on f32 T)
-  int x0, x1, y0, y1;
+  int x0, xw, y0, yh;  // clamped box: [x0, x0 + xw) x [y0, y0 + yh)
 };
 
 // 2^(j/64) as double-double, j = 0..63
@@ -474,9 +474,9 @@ __global__ void __launch_bounds__(kBlendThreads, 4) blend_k(const uint32_t* __re
         d.g = r.g;
         d.b = r.b;
         d.x0 = r.bx & 0xFFFF;
-        d.x1 = r.bx >> 16;
+        d.xw = (int)(r.bx >> 16) - d.x0;
         d.y0 = r.by & 0xFFFF;
-        d.y1 = r.by >> 16;
+        d.yh = (int)(r.by >> 16) - d.y0;
         sp[o] = d;
       } else {
         sp[o] = r;
@@ -490,19 +490,22 @@ __global__ void __launch_bounds__(kBlendThreads, 4) blend_k(const uint32_t* __re
         const Staged& q = sp[c0 + lane];
         int x0, x1, y0, y1;
         if constexpr (kExact) {
-          x0 = q.x0; x1 = q.x1; y0 = q.y0; y1 = q.y1;
+          x0 = q.x0; x1 = q.x0 + q.xw; y0 = q.y0; y1 = q.y0 + q.yh;
         } else {
           x0 = q.bx & 0xFFFF; x1 = q.bx >> 16; y0 = q.by & 0xFFFF; y1 = q.by >> 16;
         }
         mine = x0 < wx0 + 8 && x1 > wx0 && y0 < wy0 + 4 && y1 > wy0;
       }
       uint32_t m = __ballot_sync(0xffffffffu, mine);
+      const Staged* __restrict__ grp = sp + c0;
       while (m) {
-        const Staged& s = sp[c0 + __ffs(m) - 1];
+        const Staged& s = grp[__ffs(m) - 1];
         m &= m - 1;
         if (T < kStopF) continue;
         if constexpr (kExact) {
-          if (px < s.x0 || px >= s.x1 || py < s.y0 || py >= s.y1) continue;
+          // the pixel in the splat's half-open box, as two unsigned range tests
+          if (((unsigned)(px - s.x0) >= (unsigned)s.xw) | ((unsigned)(py - s.y0) >= (unsigned)s.yh))
+            continue;
           // _core.pyx:56-78: FP64 arithmetic, f32 storage of T and colour
           const double t = (double)T;
           const double dx = __dsub_rn(fx, s.cx);
