@@ -157,7 +157,8 @@ def launches_per_frame(stats, n_faces, upload_mode, n_pages=1000):
       visibility graph  vis_count, scan, vis_emit, vis_raster, vis_back
                         (links + flags + compaction + LOD)                5
                         (4 separate back-end kernels past 32767 pages)
-      page copies       upload_k (copy stream), scatter_k                 2
+      page copies       scatter_k (the uploads are copy-engine DMA;
+                        upload_mode 1 adds the upload_k gather kernel)   1
       render graph      preprocess, scan, compact, radix hist + 4 passes,
                         dup_count, scan, dup_emit, clamp, radix hist + 2
                         passes, ranges, tile_order, blend                18
