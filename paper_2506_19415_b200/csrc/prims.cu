@@ -60,8 +60,8 @@ __device__ __forceinline__ uint32_t block_exclusive(uint32_t v, uint32_t* scratc
 // ---------------------------------------------------------------- radix
 constexpr int kRBlock = 256;  // threads; one per digit bin
 constexpr int kRWarps = kRBlock / 32;
-constexpr int kRItems = 8;
-constexpr int kRTile = kRBlock * kRItems;  // 2048 pairs per tile
+constexpr int kRItems = 12;
+constexpr int kRTile = kRBlock * kRItems;  // 3072 pairs per tile
 
 // ------------------------------------------------ single-pass primitives
 // Decoupled look-back (Merrill & Garland): tiles are claimed in order through
