@@ -595,3 +595,33 @@ def test_bvh_large_mesh_and_edge_cases(cuda):
     with pytest.raises(RuntimeError, match="stack overflow"):
         kernels.bvh_nearest_points(np.array([[5.0, 5.0, 5.0]]), bounds, children, ranges,
                                    np.zeros(1, np.int32), tri)
+
+
+@pytest.mark.gpu
+def test_session_frame_with_nothing_visible(cuda):
+    """A camera looking away from every page: no required pages and no
+    uploads, yet - as in the reference, which renders every resident page
+    (gather_resident, runtime.py:377-390) - the pages still resident from
+    earlier frames are drawn; stats and image match the oracle, and the
+    session carries on normally."""
+    from paper_2506_19415_b200 import render as R
+    from paper_2506_19415_b200.runtime import VmSession
+
+    sc = _city()
+    path = inputs.city_path(inputs.CITY_SMALL)
+    kw = inputs.SESSION_VARIANTS["default"]
+    gpu = VmSession(sc, **kw)
+    cpu = core.OSession(sc, **kw)
+    away = R.Camera(position=(0.0, -500.0, 0.0), orientation=(1.0, 0.0, 0.0, 0.0),
+                    fov_y=0.5, width=64, height=48)
+    for f, cam in enumerate([away, path.frame_camera(0), away, path.frame_camera(1)]):
+        img, st = gpu.render_frame(cam, f)
+        ref, rst = cpu.render_frame(cam, f)
+        for k in ("required_pages", "resident_pages", "missing_pages", "bytes_copied",
+                  "resident_per_level", "thresholds", "usage"):
+            assert st[k] == rst[k], (f, k, st[k], rst[k])
+        assert _maxabs(img, ref) <= EXACT_TOL, f
+    img, st = gpu.render_frame(away, 4)
+    ref, rst = cpu.render_frame(away, 4)
+    assert st["required_pages"] == 0 and st["bytes_copied"] == 0
+    assert _maxabs(img, ref) <= EXACT_TOL
