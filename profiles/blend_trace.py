@@ -58,6 +58,10 @@ def main():
     for i in range(len(t)):
         last[sms[i]] = max(last[sms[i]], en[i])
     print(f"  SM finish time: min {last.min():.1f} median {np.median(last):.1f} max {last.max():.1f} us")
+    big = np.flatnonzero(ln >= 4096)
+    print(f"  CTAs with lists >= 4096: {len(big)}; launch index, start, dur, length:")
+    for i in big[:64]:
+        print(f"    {i:6d} {st[i]:8.1f} {dur[i]:8.1f} {ln[i]:7d}")
     corr = np.corrcoef(ln, dur)[0, 1]
     print(f"  corr(list length, CTA duration) = {corr:.3f}; launch index of longest: "
           f"{sorted(order.tolist())}")
