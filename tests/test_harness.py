@@ -169,3 +169,47 @@ def test_pipelined_harness_frames_identical(cuda):
         assert ia == ib and np.array_equal(x, y), ia
     assert [(f.required, f.missing, f.bytes_copied, f.resident_per_level) for f in sa] == \
            [(f.required, f.missing, f.bytes_copied, f.resident_per_level) for f in sb]
+
+
+def test_pipelined_delivery_order_without_gpu():
+    """harness.run_benchmark(pipelined=True) against a stand-in session that
+    models the real one's two-deep recycling: frame i - 2 is complete once
+    frame i has been submitted.  Every frame reaches the sink exactly once, in
+    order, and only when complete."""
+
+    class Paged:
+        page_count = 1
+
+    class Path:
+        def frame_camera(self, i):
+            return i
+
+    class Session:
+        def __init__(self):
+            self.submitted = []
+            self.done = set()
+
+        def render_frame(self, cam, i, wait=True):
+            assert not wait
+            self.submitted.append(i)
+            if len(self.submitted) >= 3:
+                self.done.add(self.submitted[-3])  # recycled inside the call
+            st = {"required_pages": 1, "missing_pages": 0, "bytes_copied": 0, "usage": 0.5,
+                  "resident_per_level": (1,), "thresholds": (1.0,)}
+            st.update({f"time_{s}": 0.1 for s in harness.STAGES})
+            return np.full((2, 2, 3), float(i), np.float32), st
+
+        def wait(self, back):
+            self.done.update(self.submitted[len(self.submitted) - 1 - back:])
+
+    for n in (1, 2, 3, 7):
+        sess, got = Session(), []
+
+        def sink(i, im, sess=sess, got=got):
+            assert i in sess.done, f"frame {i} handed over before it was complete"
+            assert float(im[0, 0, 0]) == float(i)
+            got.append(i)
+
+        stats = harness.run_benchmark(Paged(), Path(), frames=range(n), session=sess,
+                                      frame_sink=sink, pipelined=True)
+        assert got == list(range(n)) and [s.frame for s in stats] == list(range(n))
