@@ -66,23 +66,6 @@ __global__ void compact_k(const uint32_t* __restrict__ flag, const uint32_t* __r
   }
 }
 
-__device__ __forceinline__ void tile_rect(const BlendRec& r, int shift, int* tx0, int* tx1,
-                                          int* ty0, int* ty1) {
-  const int x0 = r.bx & 0xFFFF, x1 = r.bx >> 16, y0 = r.by & 0xFFFF, y1 = r.by >> 16;
-  *tx0 = x0 >> shift;
-  *tx1 = (x1 - 1) >> shift;
-  *ty0 = y0 >> shift;
-  *ty1 = (y1 - 1) >> shift;
-}
-
-// Tile rectangle of a splat's clamped pixel box, inclusive tile bounds
-// packed tx0 | tx1 << 8 | ty0 << 16 | ty1 << 24 (tile grids up to 256 x 256).
-__device__ __forceinline__ uint32_t rect_of(const BlendRec& r, int shift) {
-  int tx0, tx1, ty0, ty1;
-  tile_rect(r, shift, &tx0, &tx1, &ty0, &ty1);
-  return (uint32_t)tx0 | ((uint32_t)tx1 << 8) | ((uint32_t)ty0 << 16) | ((uint32_t)ty1 << 24);
-}
-
 constexpr int kDiffSmemWords = 12288;  // 48 KB
 constexpr int kMaxBands = 8;           // blend launches per frame (host-output banding)
 
@@ -104,15 +87,32 @@ __global__ void dup_count_k(const uint32_t* __restrict__ vals, const BlendRec* _
     __syncthreads();
   }
   const uint32_t n = ctr->n_kept;
-  for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < n; s += gridDim.x * blockDim.x) {
-    const uint32_t rc = rect_of(rec[vals[s]], shift);
-    const int tx0 = rc & 0xFF, tx1 = (rc >> 8) & 0xFF, ty0 = (rc >> 16) & 0xFF, ty1 = rc >> 24;
+  // tile rectangle of the splat's clamped pixel box, inclusive tile bounds
+  // packed tx0 | tx1 << 8 | ty0 << 16 | ty1 << 24 (tile grids up to 256 x 256)
+  auto one = [&](uint32_t s, uint32_t bx, uint32_t by) {
+    const int x0 = bx & 0xFFFF, x1 = bx >> 16, y0 = by & 0xFFFF, y1 = by >> 16;
+    const int tx0 = x0 >> shift, tx1 = (x1 - 1) >> shift, ty0 = y0 >> shift, ty1 = (y1 - 1) >> shift;
     cnt[s] = (uint32_t)((tx1 - tx0 + 1) * (ty1 - ty0 + 1));
-    rects[s] = rc;
+    rects[s] = (uint32_t)tx0 | ((uint32_t)tx1 << 8) | ((uint32_t)ty0 << 16) | ((uint32_t)ty1 << 24);
     atomicAdd(&d[ty0 * gx + tx0], 1u);
     atomicAdd(&d[ty0 * gx + tx1 + 1], 0xFFFFFFFFu);
     atomicAdd(&d[(ty1 + 1) * gx + tx0], 0xFFFFFFFFu);
     atomicAdd(&d[(ty1 + 1) * gx + tx1 + 1], 1u);
+  };
+  // two splats per thread per step: both gathers in flight together (only
+  // the packed box words of the 48-byte record are read)
+  const uint32_t stride = gridDim.x * blockDim.x;
+  uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+  for (; s + stride < n; s += 2 * stride) {
+    const BlendRec* r0 = rec + vals[s];
+    const BlendRec* r1 = rec + vals[s + stride];
+    const uint32_t bx0 = r0->bx, by0 = r0->by, bx1 = r1->bx, by1 = r1->by;
+    one(s, bx0, by0);
+    one(s + stride, bx1, by1);
+  }
+  if (s < n) {
+    const BlendRec* r0 = rec + vals[s];
+    one(s, r0->bx, r0->by);
   }
   if (local) {
     __syncthreads();
