@@ -228,9 +228,8 @@ __global__ void __launch_bounds__(kChunkRecords) preprocess_k(
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  // thread 0: start chunk c into stage st
-  auto issue = [&](uint32_t c, int st) {
-    const Chunk ch = chunks[c];
+  // thread 0: start a chunk (descriptor already loaded) into stage st
+  auto issue = [&](const Chunk& ch, int st) {
     s_chunk[st] = ch;
     const uint32_t bytes = ch.count * kRecordFloats * 4u;
     const bool tma = (ch.row & 3u) == 0 && (ch.count & 3u) == 0 && ch.count > 0;
@@ -244,10 +243,19 @@ __global__ void __launch_bounds__(kChunkRecords) preprocess_k(
   };
   uint32_t phase = 0;  // bit k: parity of stage k's next completion
   int st = 0;
-  if (t == 0) issue(blockIdx.x, 0);
+  // thread 0 keeps the next chunk's descriptor one iteration ahead, so its
+  // table load never delays the bulk copy it starts
+  Chunk next{};
+  if (t == 0) {
+    issue(chunks[blockIdx.x], 0);
+    if (blockIdx.x + gridDim.x < n) next = chunks[blockIdx.x + gridDim.x];
+  }
   for (uint32_t c = blockIdx.x; c < n; c += gridDim.x, st ^= 1) {
     const uint32_t cn = c + gridDim.x;
-    if (t == 0 && cn < n) issue(cn, st ^ 1);  // freed by the barrier ending the last iteration
+    if (t == 0 && cn < n) {
+      issue(next, st ^ 1);  // stage freed by the barrier ending the last iteration
+      if (cn + gridDim.x < n) next = chunks[cn + gridDim.x];
+    }
     mbar_wait(&bar[st], (phase >> st) & 1u);
     phase ^= 1u << st;
     const Chunk ch = s_chunk[st];
