@@ -498,7 +498,50 @@ __global__ void __launch_bounds__(kBlendThreads, 4) blend_k(const uint32_t* __re
       }
       uint32_t m = __ballot_sync(0xffffffffu, mine);
       const Staged* __restrict__ grp = sp + c0;
-      while (m) {
+      if constexpr (kExact) {
+        // two splats per step: their box tests and sigmas (independent of T)
+        // are evaluated together, so rejections - most of the walk for pixels
+        // that never saturate - overlap; the exp and the T/colour updates then
+        // run in list order.
+        auto sigma = [&](const Staged& q, bool& live) -> double {
+          const bool in = ((unsigned)(px - q.x0) < (unsigned)q.xw) &
+                          ((unsigned)(py - q.y0) < (unsigned)q.yh);
+          const double dx = __dsub_rn(fx, q.cx);
+          const double dy = __dsub_rn(fy, q.cy);
+          const double sg = __dadd_rn(__dadd_rn(__dmul_rn(__dmul_rn(q.ca, dx), dx),
+                                                __dmul_rn(__dmul_rn(q.cb2, dy), dx)),
+                                      __dmul_rn(__dmul_rn(q.cc, dy), dy));
+          // weight < 2^-36 (sigma below the staged threshold): T is unchanged
+          // bit for bit and the colour moves by < 2^-36 - no effect
+          live = in & (sg >= q.skip);
+          return sg;
+        };
+        auto blend = [&](const Staged& q, double sg) {
+          // _core.pyx:56-78: FP64 arithmetic, f32 storage of T and colour
+          const double t = (double)T;
+          double wgt = __dmul_rn(q.al, exp_tab(sg, tab));
+          if (wgt > kBlendC[8]) wgt = kBlendC[8];
+          const double wt = __dmul_rn(wgt, t);
+          cr = __double2float_rn(__dadd_rn((double)cr, __dmul_rn(wt, q.r)));
+          cg = __double2float_rn(__dadd_rn((double)cg, __dmul_rn(wt, q.g)));
+          cb = __double2float_rn(__dadd_rn((double)cb, __dmul_rn(wt, q.b)));
+          T = __double2float_rn(__dmul_rn(t, __dsub_rn(1.0, wgt)));
+        };
+        while (m) {
+          const Staged& q0 = grp[__ffs(m) - 1];
+          m &= m - 1;
+          const bool two = m != 0u;
+          const Staged& q1 = grp[two ? __ffs(m) - 1 : 0];
+          if (two) m &= m - 1;
+          if (T < kStopF) continue;
+          bool l0, l1;
+          const double s0 = sigma(q0, l0);
+          const double s1 = sigma(q1, l1);
+          if (l0) blend(q0, s0);
+          if (two && l1 && T >= kStopF) blend(q1, s1);
+        }
+      }
+      while (!kExact && m) {
         const Staged& s = grp[__ffs(m) - 1];
         m &= m - 1;
         if (T < kStopF) continue;
