@@ -351,6 +351,7 @@ __constant__ double2 kExp2Tab[64];
 // take them as c[][] operands, where literals that do not fit an immediate
 // would be rematerialised with uniform moves on every pixel-splat.
 constexpr float kStopF = 0x1.010102p-8f;  // RN32(1/255) = smallest float >= 1/255
+constexpr int kPairStep = 2;  // splats whose box tests and sigmas are evaluated together
 
 __constant__ double kBlendC[10] = {
     0x1.71547652b82fep+6,   // 0: 64 / ln2
@@ -528,17 +529,22 @@ __global__ void __launch_bounds__(kBlendThreads, 4) blend_k(const uint32_t* __re
           T = __double2float_rn(__dmul_rn(t, __dsub_rn(1.0, wgt)));
         };
         while (m) {
-          const Staged& q0 = grp[__ffs(m) - 1];
-          m &= m - 1;
-          const bool two = m != 0u;
-          const Staged& q1 = grp[two ? __ffs(m) - 1 : 0];
-          if (two) m &= m - 1;
+          int j[kPairStep];
+          int got = 0;
+#pragma unroll
+          for (int k = 0; k < kPairStep; ++k) {
+            j[k] = m ? __ffs(m) - 1 : 0;
+            got += m ? 1 : 0;
+            m &= m - 1;
+          }
           if (T < kStopF) continue;
-          bool l0, l1;
-          const double s0 = sigma(q0, l0);
-          const double s1 = sigma(q1, l1);
-          if (l0) blend(q0, s0);
-          if (two && l1 && T >= kStopF) blend(q1, s1);
+          bool l[kPairStep];
+          double sg[kPairStep];
+#pragma unroll
+          for (int k = 0; k < kPairStep; ++k) sg[k] = sigma(grp[j[k]], l[k]);
+#pragma unroll
+          for (int k = 0; k < kPairStep; ++k)
+            if (k < got && l[k] && T >= kStopF) blend(grp[j[k]], sg[k]);
         }
       }
       while (!kExact && m) {
