@@ -517,6 +517,14 @@ __global__ void __launch_bounds__(kBlendThreads, 4) blend_k(const uint32_t* __re
           live = in & (sg >= q.skip);
           return sg;
         };
+        auto apply = [&](const Staged& q, double wgt) {
+          const double t = (double)T;
+          const double wt = __dmul_rn(wgt, t);
+          cr = __double2float_rn(__dadd_rn((double)cr, __dmul_rn(wt, q.r)));
+          cg = __double2float_rn(__dadd_rn((double)cg, __dmul_rn(wt, q.g)));
+          cb = __double2float_rn(__dadd_rn((double)cb, __dmul_rn(wt, q.b)));
+          T = __double2float_rn(__dmul_rn(t, __dsub_rn(1.0, wgt)));
+        };
         auto blend = [&](const Staged& q, double sg) {
           // _core.pyx:56-78: FP64 arithmetic, f32 storage of T and colour
           const double t = (double)T;
@@ -537,14 +545,27 @@ __global__ void __launch_bounds__(kBlendThreads, 4) blend_k(const uint32_t* __re
             got += m ? 1 : 0;
             m &= m - 1;
           }
-          if (T < kStopF) continue;
           bool l[kPairStep];
           double sg[kPairStep];
 #pragma unroll
           for (int k = 0; k < kPairStep; ++k) sg[k] = sigma(grp[j[k]], l[k]);
+          bool any = false;
+#pragma unroll
+          for (int k = 0; k < kPairStep; ++k) any |= k < got && l[k];
+          // warp-uniform skip (no lane may leave before the vote)
+          if (!__any_sync(0xffffffffu, any && T >= kStopF)) continue;
+          // the step's weights (independent of T) together, branch-free
+          double wv[kPairStep];
+#pragma unroll
+          for (int k = 0; k < kPairStep; ++k) {
+            const Staged& q = grp[j[k]];
+            double wk = __dmul_rn(q.al, exp_tab(l[k] ? sg[k] : 0.0, tab));
+            if (wk > kBlendC[8]) wk = kBlendC[8];
+            wv[k] = wk;
+          }
 #pragma unroll
           for (int k = 0; k < kPairStep; ++k)
-            if (k < got && l[k] && T >= kStopF) blend(grp[j[k]], sg[k]);
+            if (k < got && l[k] && T >= kStopF) apply(grp[j[k]], wv[k]);
         }
       }
       while (!kExact && m) {
