@@ -23,8 +23,13 @@
  *  - No hot-path allocation: callers size workspaces with the *_bytes
  *    queries and own every buffer (kernels hold no state).
  *  - Results are bit-exact with the reference for every integer/index output
- *    (page-ID images, required lists, plans, sort orders); images are within
- *    1e-3 max-abs in fast mode and FP64-faithful in exact mode.
+ *    (page-ID images, required lists, plans, sort orders).  Images: exact
+ *    mode (the default; FP64 blend arithmetic like the reference) is within
+ *    1e-5 max-abs of the reference; fast mode (opt-in FP32 blend) is within
+ *    PSNR >= 50 dB and 1e-2 max-abs - an FP32 exponent can move a pixel's
+ *    transmittance across the 1/255 stop threshold one splat earlier or
+ *    later, which changes that pixel by up to ~4e-3 (tests/test_gpu_parity.py
+ *    checks both bounds).
  */
 #ifndef VMSPLAT_B200_H
 #define VMSPLAT_B200_H
@@ -144,6 +149,16 @@ int32_t vms_tile_size(void);
 /* 1 if `ptr` is page-locked host memory the device can address (zero-copy
  * target), 0 otherwise. */
 int32_t vms_host_accessible(const void* ptr);
+/* Page-lock (and map into the device address space) an existing host range,
+ * e.g. the read-only memory map of a .vms file's record section
+ * (scene_io.py:318-321 read_scene(mmap)), so several sessions - and several
+ * processes, one per GPU, mapping the same file - stream pages from ONE
+ * host-resident copy of the scene instead of each holding a private pinned
+ * copy.  The range is widened to whole pages; *base_out receives the
+ * registered base for vms_host_unregister.  read_only adds
+ * cudaHostRegisterReadOnly (required for PROT_READ mappings). */
+int32_t vms_host_register(const void* ptr, uint64_t bytes, int32_t read_only, void** base_out);
+int32_t vms_host_unregister(void* base);
 
 /* Per-launch device timing for profiling runs: when enabled every kernel
  * launch records a CUDA event; the report (CSV "kernel,count,total_us")
@@ -154,6 +169,9 @@ int64_t vms_profile_report(char* buf, int64_t len);
 /* Profiling: when dev_ptr is non-NULL every blend CTA writes {start ns, end
  * ns, SM id, (list length << 32) | tile} (4 x u64) at dev_ptr[4 * block]. */
 int32_t vms_debug_blend_trace(void* dev_ptr);
+/* The exact blend's table-driven FP64 exp(x), x in [-700, 0], evaluated on
+ * [dev] x -> [dev] out (accuracy test against libm; not on the hot path). */
+int32_t vms_debug_exp(const double* x, int64_t n, double* out, void* stream);
 
 /* ---- kernel-level drop-ins (pkg/src/vmsplat/kernels/__init__.py) ------ */
 

@@ -217,6 +217,58 @@ def render_flat(records, cam, kern=None):
     return composite_in_order(records, order_of(records, cam, kern), cam, kern)
 
 
+def render_window(records, cam, window, kern=None, chunk=1 << 20):
+    """Pixels [x0, x1) x [y0, y1) of render_records(records, cam)
+    (render.py:251-253) without projecting every record: SURVEY 8(c)(ii).
+
+    Order: keys and the stable sort over ALL records, exactly as
+    render_records.  Selection: a record can only touch the window if its
+    projected bbox does; its bbox radius is 3*sqrt(lambda_max(cov2 + 0.3 I))
+    with lambda_max(cov2) <= ||J||_F^2 * max(scale)^2 (the camera rotation
+    and the record's rotation are orthogonal), so records whose centre lies
+    farther than that bound (+2 px) from the window are dropped before the
+    projection.  The survivors are projected (in sorted order) and the ones
+    whose exact bounds meet the window are composited into a window-sized
+    image with centres shifted by the window origin (an exact f64 shift of an
+    f32 centre) and bounds clipped to the window.  Each window pixel then sees
+    exactly the splats, in exactly the order, that render_records gives it."""
+    kern = kern or ckernels
+    records = np.asarray(records, dtype=np.float32)
+    x0, x1, y0, y1 = (int(v) for v in window)
+    order = order_of(records, cam, kern)
+    if not len(order):
+        return np.zeros((y1 - y0, x1 - x0, 3), np.float32), 0
+    f = cam.focal
+    pos = np.asarray(cam.position, dtype=np.float64)
+    crot = cam.rot()
+    keep = []
+    for a in range(0, len(order), chunk):
+        idx = order[a:a + chunk]
+        r = records[idx]
+        v = (r[:, 0:3].astype(np.float64) - pos) @ crot
+        z = v[:, 2]
+        cx = f * v[:, 0] / z + cam.width / 2.0
+        cy = f * v[:, 1] / z + cam.height / 2.0
+        smax = np.max(r[:, 7:10].astype(np.float64), axis=1)
+        jf2 = 2.0 * f * f / (z * z) + f * f * (v[:, 0] ** 2 + v[:, 1] ** 2) / (z ** 4)
+        rad = 3.0 * np.sqrt(jf2 * smax * smax * 1.0001 + LOW_PASS) + 2.0
+        near = ((cx + rad >= x0) & (cx - rad <= x1) & (cy + rad >= y0) & (cy - rad <= y1))
+        keep.append(idx[near])
+    sel = np.concatenate(keep)
+    centers, conics, colors, alphas, bounds, _ = project(records[sel], cam)
+    b = bounds
+    hit = (b[:, 0] < x1) & (b[:, 1] > x0) & (b[:, 2] < y1) & (b[:, 3] > y0)
+    bb = b[hit].copy()
+    bb[:, 0] = np.maximum(bb[:, 0], x0)
+    bb[:, 1] = np.minimum(bb[:, 1], x1)
+    bb[:, 2] = np.maximum(bb[:, 2], y0)
+    bb[:, 3] = np.minimum(bb[:, 3], y1)
+    full = np.zeros((cam.height, cam.width, 3), np.float32)
+    kern.composite_splats(centers[hit], conics[hit], colors[hit], alphas[hit], bb, full)
+    img = np.ascontiguousarray(full[y0:y1, x0:x1])
+    return img, int(hit.sum())
+
+
 # -- render._clip_near / render_visibility (render.py:256-307) --------------
 def clip_near(tv, near):
     inside = tv[:, 2] > near
@@ -237,17 +289,39 @@ def clip_near(tv, near):
 
 
 def clipped_triangles(vertices, faces, face_page, cam):
-    """Per-face clip + project, emitted in (face, fan) order."""
-    tris, ids = [], []
-    if len(faces):
-        view = cam.to_view(np.asarray(vertices, dtype=np.float64))
-        for fi in range(len(faces)):
-            for cl in clip_near(view[faces[fi]], cam.near):
-                tris.append(cam.to_pixels(cl))
-                ids.append(face_page[fi])
-    if not tris:
+    """Per-face clip + project, emitted in (face, fan) order
+    (render.py:288-304).  Faces entirely beyond the near plane are projected
+    in one vectorised pass (elementwise, the same operations per vertex as
+    the per-face loop); only faces crossing the plane take the clip loop."""
+    faces = np.asarray(faces)
+    if not len(faces):
         return np.zeros((0, 3, 3)), np.zeros(0, np.uint32)
-    return np.ascontiguousarray(np.stack(tris)), np.asarray(ids, dtype=np.uint32)
+    view = cam.to_view(np.asarray(vertices, dtype=np.float64))
+    tv = view[faces]                                   # (F, 3, 3)
+    n_in = (tv[:, :, 2] > cam.near).sum(axis=1)
+    full = n_in == 3
+    part = np.flatnonzero((n_in > 0) & ~full)
+    pieces = {}
+    for fi in part:
+        pieces[int(fi)] = [cam.to_pixels(cl) for cl in clip_near(tv[fi], cam.near)]
+    counts = full.astype(np.int64)
+    for fi, lst in pieces.items():
+        counts[fi] = len(lst)
+    total = int(counts.sum())
+    if total == 0:
+        return np.zeros((0, 3, 3)), np.zeros(0, np.uint32)
+    start = np.cumsum(counts) - counts
+    tris = np.empty((total, 3, 3))
+    ids = np.empty(total, np.uint32)
+    fidx = np.flatnonzero(full)
+    if len(fidx):
+        tris[start[fidx]] = cam.to_pixels(tv[fidx].reshape(-1, 3)).reshape(-1, 3, 3)
+        ids[start[fidx]] = np.asarray(face_page)[fidx]
+    for fi, lst in pieces.items():
+        for k, t in enumerate(lst):
+            tris[start[fi] + k] = t
+            ids[start[fi] + k] = face_page[fi]
+    return np.ascontiguousarray(tris), ids
 
 
 def visibility(vertices, faces, face_page, cam, kern=None):

@@ -126,6 +126,11 @@ def probe_dot_mode() -> tuple[int, bool]:
             result = (mode, True)
             break
     if result is None:
+        import warnings
+
+        warnings.warn("neither FP64 dot order reproduces this host's BLAS (p - pos) @ R bit "
+                      "for bit: visibility page sets and sort keys may differ from the "
+                      "reference in rare ties (SURVEY Appendix A.1)", RuntimeWarning)
         result = (0, False)
     _dot_mode = result
     return result

@@ -138,7 +138,10 @@ SIGNATURES = {
     "vms_session_counters": (I32, [P, P, P]),
     "vms_session_wait": (I32, [P, I32]),
     "vms_host_accessible": (I32, [P]),
+    "vms_host_register": (I32, [P, ctypes.c_uint64, I32, ctypes.POINTER(P)]),
+    "vms_host_unregister": (I32, [P]),
     "vms_debug_blend_trace": (I32, [P]),
+    "vms_debug_exp": (I32, [P, I64, P, P]),
     "vms_bvh_nearest_points": (I32, [P, I64, P, P, P, I64, P, P, I64, P, P, P, P]),
 }
 

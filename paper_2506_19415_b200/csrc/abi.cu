@@ -175,6 +175,14 @@ int32_t vms_tile_size(void) { return tile_size(); }
 
 int32_t vms_debug_blend_trace(void* dev_ptr) { return debug_blend_trace(dev_ptr); }
 
+int32_t vms_debug_exp(const double* x, int64_t n, double* out, void* stream) {
+  if (n < 0 || (n > 0 && (!x || !out))) {
+    set_error("debug_exp: bad arguments");
+    return VMS_ERR_INVALID;
+  }
+  return debug_exp(x, (uint64_t)n, out, static_cast<cudaStream_t>(stream));
+}
+
 int32_t vms_host_accessible(const void* ptr) {
   if (!ptr) return 0;
   cudaPointerAttributes at{};
@@ -183,6 +191,37 @@ int32_t vms_host_accessible(const void* ptr) {
     return 0;
   }
   return at.type == cudaMemoryTypeHost && at.devicePointer == ptr ? 1 : 0;
+}
+
+int32_t vms_host_register(const void* ptr, uint64_t bytes, int32_t read_only, void** base_out) {
+  // page-align the range: the record section of a memory-mapped .vms file
+  // starts at a section offset, not on a page boundary
+  if (!ptr || !bytes || !base_out) {
+    set_error("host_register: null pointer or empty range");
+    return VMS_ERR_INVALID;
+  }
+  const uintptr_t pg = 4096;
+  const uintptr_t a = (uintptr_t)ptr & ~(pg - 1);
+  const uintptr_t b = ((uintptr_t)ptr + bytes + pg - 1) & ~(pg - 1);
+  unsigned flags = cudaHostRegisterPortable | cudaHostRegisterMapped;
+  if (read_only) flags |= cudaHostRegisterReadOnly;
+  cudaError_t e = cudaHostRegister((void*)a, (size_t)(b - a), flags);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return cuda_status(e, "cudaHostRegister");
+  }
+  *base_out = (void*)a;
+  return VMS_OK;
+}
+
+int32_t vms_host_unregister(void* base) {
+  if (!base) return VMS_OK;
+  cudaError_t e = cudaHostUnregister(base);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return cuda_status(e, "cudaHostUnregister");
+  }
+  return VMS_OK;
 }
 
 size_t vms_composite_workspace_bytes(int64_t n, int64_t n_instances, int32_t h, int32_t w) {

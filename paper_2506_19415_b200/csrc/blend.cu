@@ -383,6 +383,12 @@ __device__ __forceinline__ double exp_tab(double x, const double2* __restrict__ 
   return __hiloint2double(__double2hiint(v) + ((k >> 6) << 20), __double2loint(v));
 }
 
+// The exact blend's exp, exposed for its accuracy test (vms_debug_exp).
+__global__ void exp_eval_k(const double* __restrict__ x, uint64_t n, double* __restrict__ out) {
+  const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (i < n) out[i] = exp_tab(x[i], kExp2Tab);
+}
+
 // Optional per-CTA timing trace for schedule studies (vms_debug_blend_trace):
 // 8 u64 per CTA: globaltimer at start and end, SM id, list length << 32 |
 // tile, then 4 zero words.
@@ -802,6 +808,13 @@ int32_t blend_init() {
                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)(sizeof(uint32_t) * kDiffSmemWords)));
   done = true;
+  return VMS_OK;
+}
+
+int32_t debug_exp(const double* x, uint64_t n, double* out, cudaStream_t s) {
+  if (const int32_t rc = blend_init()) return rc;
+  if (n) exp_eval_k<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(x, n, out);
+  VMS_LAUNCH_CHECK("debug_exp");
   return VMS_OK;
 }
 

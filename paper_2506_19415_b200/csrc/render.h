@@ -112,6 +112,7 @@ int32_t preprocess_init();
 
 // Per-CTA blend timing trace (profiling only; nullptr disables).
 int32_t debug_blend_trace(void* dev_ptr);
+int32_t debug_exp(const double* x, uint64_t n, double* out, cudaStream_t s);
 
 // Zero the frame's counters and primitive workspaces (all memsets of a
 // frame, ahead of its first kernel); render_finish assumes it ran.

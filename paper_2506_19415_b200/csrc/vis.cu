@@ -16,6 +16,7 @@
 //        pre-propagation snapshot, LOD level per page, ordered compaction of
 //        the required list into host-mapped memory (runtime.py:89-96,129-132).
 #include <cfloat>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "prims.h"
@@ -255,11 +256,80 @@ __global__ void vis_setup_raw_k(const double* __restrict__ raw, const uint32_t* 
   setup_tri(r[0], r[1], r[2], r[3], r[4], r[5], r[6], r[7], r[8], ids[i], w, h, &tris[i]);
 }
 
+// Binned raster for large proxy meshes (C4: 600K faces).  Each clipped
+// triangle is listed under every 16x16 raster tile its pixel box touches;
+// a stable radix sort by tile keeps each tile's list in triangle order, so
+// the raster walks only its own list and the first-triangle-wins rule is
+// unchanged.  Triangles with an empty box (off screen) are listed nowhere.
+__device__ __forceinline__ uint32_t tri_tiles(const int4 b, int* tx0, int* ty0, int* tx1,
+                                              int* ty1) {
+  if (b.x > b.y || b.z > b.w) return 0u;
+  *tx0 = b.x / kVisTile;
+  *tx1 = b.y / kVisTile;
+  *ty0 = b.z / kVisTile;
+  *ty1 = b.w / kVisTile;
+  return (uint32_t)(*tx1 - *tx0 + 1) * (uint32_t)(*ty1 - *ty0 + 1);
+}
+
+__global__ void vis_bin_count_k(const VisTri* __restrict__ tris,
+                                const uint32_t* __restrict__ n_tris, uint32_t* __restrict__ cnt) {
+  pdl_wait();
+  const uint32_t n = *n_tris;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int4 b = __ldg(reinterpret_cast<const int4*>(&tris[i].x0));
+    int a0, a1, c0, c1;
+    cnt[i] = tri_tiles(b, &a0, &c0, &a1, &c1);
+  }
+}
+
+__global__ void vis_bin_emit_k(const VisTri* __restrict__ tris,
+                               const uint32_t* __restrict__ n_tris,
+                               const uint32_t* __restrict__ off, const uint32_t* __restrict__ n_pairs,
+                               uint32_t pair_cap, int tiles_x, uint32_t* __restrict__ keys,
+                               uint32_t* __restrict__ vals) {
+  pdl_wait();
+  const uint32_t n = *n_tris;
+  if (*n_pairs > pair_cap) return;  // the raster walks every triangle instead
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int4 b = __ldg(reinterpret_cast<const int4*>(&tris[i].x0));
+    int x0, y0, x1, y1;
+    if (!tri_tiles(b, &x0, &y0, &x1, &y1)) continue;
+    uint32_t o = off[i];
+    for (int ty = y0; ty <= y1; ++ty)
+      for (int tx = x0; tx <= x1; ++tx) {
+        keys[o] = (uint32_t)(ty * tiles_x + tx);
+        vals[o] = i;
+        ++o;
+      }
+  }
+}
+
+// [start, end) of every tile's run in the sorted pair list.
+__global__ void vis_bin_ranges_k(const uint32_t* __restrict__ keys,
+                                 const uint32_t* __restrict__ n_pairs, uint32_t pair_cap,
+                                 uint2* __restrict__ ranges) {
+  pdl_wait();
+  const uint32_t n = *n_pairs;
+  if (n > pair_cap) return;
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+    const uint32_t k = keys[j];
+    if (j == 0 || keys[j - 1] != k) ranges[k].x = j;
+    if (j + 1 == n || keys[j + 1] != k) ranges[k].y = j + 1;
+  }
+}
+
+struct VisBins {
+  const uint32_t* vals;     // sorted triangle indices (nullptr: unbinned raster)
+  const uint2* ranges;      // per raster tile
+  const uint32_t* n_pairs;
+  uint32_t pair_cap;
+};
+
 __global__ void __launch_bounds__(kVisThreads) vis_raster_k(
     const VisTri* __restrict__ tris, const uint32_t* __restrict__ n_tris_dev, uint32_t n_host,
     int w, int h, uint32_t* __restrict__ id_image, double* __restrict__ invz_image,
     int init_from_images, uint32_t page_count, uint32_t* __restrict__ page_depth,
-    uint8_t* __restrict__ page_direct, uint32_t* __restrict__ err) {
+    uint8_t* __restrict__ page_direct, uint32_t* __restrict__ err, VisBins bins) {
   pdl_wait();
   constexpr int kBoxes = 4;  // triangle boxes tested per thread per round
   __shared__ VisTri stri[kVisThreads];
@@ -280,16 +350,29 @@ __global__ void __launch_bounds__(kVisThreads) vis_raster_k(
     best_id = id_image[(int64_t)py * w + px];
     best_z = invz_image[(int64_t)py * w + px];
   }
-  const uint32_t n = n_tris_dev ? *n_tris_dev : n_host;
-  for (uint32_t base = 0; base < n; base += kBoxes * kVisThreads) {
+  // the triangles to test: all of them, or this tile's binned list (in
+  // triangle order) when the frame's pair list fit its buffer
+  uint32_t first = 0, n = n_tris_dev ? *n_tris_dev : n_host;
+  const uint32_t* list = nullptr;
+  if (bins.vals && *bins.n_pairs <= bins.pair_cap) {
+    const uint2 r = bins.ranges[blockIdx.y * gridDim.x + blockIdx.x];
+    list = bins.vals;
+    first = r.x;
+    n = r.y;
+  }
+  for (uint32_t base = first; base < n; base += kBoxes * kVisThreads) {
     // test kBoxes 16-byte boxes per thread (loads in flight together) and
     // compact the indices of the triangles touching this tile, in order
     bool hit[kBoxes];
+    uint32_t tid[kBoxes];
 #pragma unroll
     for (int k = 0; k < kBoxes; ++k) {
-      const uint32_t ti = base + k * kVisThreads + threadIdx.x;
+      const uint32_t li = base + k * kVisThreads + threadIdx.x;
       hit[k] = false;
-      if (ti < n) {
+      tid[k] = li;
+      if (li < n) {
+        const uint32_t ti = list ? __ldg(list + li) : li;
+        tid[k] = ti;
         const int4 bx = __ldg(reinterpret_cast<const int4*>(&tris[ti].x0));
         hit[k] = bx.x <= bx.y && bx.x <= tx1 && bx.y >= tx0 && bx.z <= ty1 && bx.w >= ty0;
       }
@@ -307,7 +390,7 @@ __global__ void __launch_bounds__(kVisThreads) vis_raster_k(
         pre += q < warp ? c : 0u;
         tot += c;
       }
-      if (hit[k]) sidx[cnt + pre + __popc(bal & lanemask_lt())] = base + k * kVisThreads + threadIdx.x;
+      if (hit[k]) sidx[cnt + pre + __popc(bal & lanemask_lt())] = tid[k];
       cnt += tot;
       __syncthreads();
     }
@@ -430,8 +513,38 @@ __global__ void vis_required_k(const uint32_t* __restrict__ depth,
 
 }  // namespace
 
+// Binned raster (per-tile triangle lists) for large proxy meshes; the
+// walk-everything raster is cheaper below ~64K faces (C2 2K, C3 20K).
+// VMSPLAT_VIS_BIN=0/1 forces it off/on.
+bool vis_binned(uint32_t n_faces) {
+  static int force = -2;
+  if (force == -2) {
+    const char* e = getenv("VMSPLAT_VIS_BIN");
+    force = (e && *e) ? (atoi(e) ? 1 : 0) : -1;
+  }
+  return force >= 0 ? force == 1 : n_faces >= 65536u;
+}
+
+constexpr uint32_t kVisMaxTiles = 1u << 16;  // 16-bit tile keys: 2 radix passes
+
+uint32_t vis_pair_cap(uint32_t n_faces) {
+  const uint64_t c = 8ull * n_faces;
+  return (uint32_t)(c < (1u << 20) ? (1u << 20) : (c > (1ull << 30) ? (1ull << 30) : c));
+}
+
+size_t vis_bin_bytes(uint32_t n_faces) {
+  if (!vis_binned(n_faces)) return 0;
+  const uint32_t nt = 2 * n_faces + 1, cap = vis_pair_cap(n_faces);
+  size_t b = sizeof(uint32_t) * (size_t)nt * 2;   // per-triangle counts + offsets
+  b += sizeof(uint32_t) * 4;                       // n_pairs
+  b += sizeof(uint32_t) * (size_t)cap * 4;         // keys/vals ping-pong
+  b += sizeof(uint2) * kVisMaxTiles;               // tile ranges
+  b += radix_ws_bytes(cap) + scan_ws_bytes(nt);
+  return b + 8 * 256;
+}
+
 size_t vis_ws_bytes(uint32_t n_faces, uint32_t page_count) {
-  size_t b = 0;
+  size_t b = vis_bin_bytes(n_faces);
   b += sizeof(uint32_t) * (n_faces + 1) * 2;        // counts + offsets
   b += sizeof(uint32_t) * 4;                         // n_tris, n_req
   b += sizeof(VisTri) * ((size_t)n_faces * 2 + 1);   // clipped triangles
@@ -449,6 +562,11 @@ struct VisWs {
   uint8_t* direct;
   void* scan;
   VisFrameDev* fd;
+  // binned raster (nullptr when the mesh is small)
+  uint32_t *bcnt, *boff, *n_pairs, *k0, *v0, *k1, *v1;
+  uint2* ranges;
+  void *radix, *scan2;
+  uint32_t pair_cap;
 };
 
 template <typename T>
@@ -474,6 +592,24 @@ VisWs carve_ws(void* ws, uint32_t nf, uint32_t P) {
   w.direct = carve<uint8_t>(p, P + 1);
   w.scan = carve<char>(p, scan_ws_bytes(nf > P + 1 ? nf : P + 1));
   w.fd = carve<VisFrameDev>(p, 1);
+  w.bcnt = w.boff = w.n_pairs = w.k0 = w.v0 = w.k1 = w.v1 = nullptr;
+  w.ranges = nullptr;
+  w.radix = w.scan2 = nullptr;
+  w.pair_cap = 0;
+  if (vis_binned(nf)) {
+    const uint32_t nt = 2 * nf + 1;
+    w.pair_cap = vis_pair_cap(nf);
+    w.bcnt = carve<uint32_t>(p, nt);
+    w.boff = carve<uint32_t>(p, nt);
+    w.n_pairs = carve<uint32_t>(p, 4);
+    w.k0 = carve<uint32_t>(p, w.pair_cap);
+    w.v0 = carve<uint32_t>(p, w.pair_cap);
+    w.k1 = carve<uint32_t>(p, w.pair_cap);
+    w.v1 = carve<uint32_t>(p, w.pair_cap);
+    w.ranges = carve<uint2>(p, kVisMaxTiles);
+    w.radix = carve<char>(p, radix_ws_bytes(w.pair_cap));
+    w.scan2 = carve<char>(p, scan_ws_bytes(nt));
+  }
   return w;
 }
 }  // namespace
@@ -519,6 +655,12 @@ int32_t vis_launch(const VisArgs& a, cudaStream_t s) {
   VMS_CUDA(cudaMemsetAsync(w.direct, 0, a.page_count + 1, s));
   const uint32_t scan_n = a.n_faces > a.page_count + 1 ? a.n_faces : a.page_count + 1;
   VMS_CUDA(cudaMemsetAsync(w.scan, 0, scan_ws_bytes(scan_n), s));
+  if (w.bcnt && a.n_faces) {
+    VMS_CUDA(cudaMemsetAsync(w.n_pairs, 0, sizeof(uint32_t) * 4, s));
+    VMS_CUDA(cudaMemsetAsync(w.scan2, 0, scan_ws_bytes(2 * a.n_faces + 1), s));
+    VMS_CUDA(cudaMemsetAsync(w.radix, 0, radix_clear_bytes(), s));
+    VMS_CUDA(cudaMemsetAsync(w.ranges, 0, sizeof(uint2) * kVisMaxTiles, s));
+  }
   if (a.n_faces) {
     VMS_CUDA(launch(vis_count_k, ceil_div<uint32_t>(a.n_faces, T), T, 0, s,
                     (const VisFrameDev*)w.fd, a.verts, a.faces, a.n_faces, w.counts));
@@ -532,9 +674,45 @@ int32_t vis_launch(const VisArgs& a, cudaStream_t s) {
     mark("vis_emit", s);
   }
   dim3 grid(ceil_div(a.cam.width, kVisTile), ceil_div(a.cam.height, kVisTile));
+  VisBins bins{nullptr, nullptr, nullptr, 0u};
+  if (w.bcnt && a.n_faces) {
+    // per-tile triangle lists: count tiles per triangle, scan, emit (tile,
+    // triangle) pairs in triangle order, stable sort by tile, tile ranges
+    const uint32_t tiles = grid.x * grid.y;
+    if (tiles > kVisMaxTiles) {
+      set_error("vis_frame: visibility raster larger than %u tiles", kVisMaxTiles);
+      return VMS_ERR_INVALID;
+    }
+    const uint32_t nt_max = 2 * a.n_faces;
+    const int g = 4 * kSMs;
+    VMS_CUDA(launch(vis_bin_count_k, g, T, 0, s, (const VisTri*)w.tris,
+                    (const uint32_t*)w.n_tris, w.bcnt));
+    mark("vis_bin_count", s);
+    int32_t st = scan_exclusive_u32(w.bcnt, w.boff, w.n_tris, 0, nt_max, w.n_pairs, w.scan2, s,
+                                    false);
+    if (st) return st;
+    VMS_CUDA(launch(vis_bin_emit_k, g, T, 0, s, (const VisTri*)w.tris, (const uint32_t*)w.n_tris,
+                    (const uint32_t*)w.boff, (const uint32_t*)w.n_pairs, w.pair_cap,
+                    (int)grid.x, w.k0, w.v0));
+    mark("vis_bin_emit", s);
+    int bits = 1;
+    while ((1u << bits) < tiles) ++bits;
+    int alt = 0;
+    // an overflowing frame sorts garbage it never reads (the emit and the
+    // ranges skip it; the raster walks every triangle)
+    st = radix_sort_u32(w.k0, w.v0, w.k1, w.v1, w.n_pairs, 0, w.pair_cap, 0, bits, &alt,
+                        w.radix, s, false);
+    if (st) return st;
+    uint32_t* ks = alt ? w.k1 : w.k0;
+    uint32_t* vs = alt ? w.v1 : w.v0;
+    VMS_CUDA(launch(vis_bin_ranges_k, g, T, 0, s, (const uint32_t*)ks, (const uint32_t*)w.n_pairs,
+                    w.pair_cap, w.ranges));
+    mark("vis_bin_ranges", s);
+    bins = VisBins{vs, w.ranges, w.n_pairs, w.pair_cap};
+  }
   VMS_CUDA(launch(vis_raster_k, grid, kVisThreads, 0, s, (const VisTri*)w.tris,
                   (const uint32_t*)w.n_tris, 0u, a.cam.width, a.cam.height, a.id_image,
-                  a.invz_image, 0, a.page_count, w.base, w.direct, w.err));
+                  a.invz_image, 0, a.page_count, w.base, w.direct, w.err, bins));
   mark("vis_raster", s);
   if (back) {
     VMS_CUDA(launch(vis_back_k, 1, kFrontThreads, sizeof(uint32_t) * (a.page_count + 1), s,
@@ -604,7 +782,8 @@ int32_t raster_triangles(const double* raw, const uint32_t* ids, uint32_t n, uin
   if (n) vis_setup_raw_k<<<ceil_div<uint32_t>(n, T), T, 0, s>>>(raw, ids, n, w, h, tris);
   dim3 grid(ceil_div(w, kVisTile), ceil_div(h, kVisTile));
   vis_raster_k<<<grid, kVisThreads, 0, s>>>(tris, nullptr, n, w, h, id_image, invz_image, 1, 0,
-                                            nullptr, nullptr, nullptr);
+                                            nullptr, nullptr, nullptr,
+                                            VisBins{nullptr, nullptr, nullptr, 0u});
   VMS_LAUNCH_CHECK("raster_triangles");
   return VMS_OK;
 }

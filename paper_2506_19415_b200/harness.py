@@ -385,7 +385,9 @@ def run_sharded(scene, path, config: BenchConfig | None = None, dist=None, frame
                 device=None):
     """View sharding: rank r renders the contiguous
     block [r F / G, (r + 1) F / G) of the path with its own session (page
-    table, device pool, pinned scene copy) - no data-path collective - and
+    table, device pool; the host-resident scene is shared: every rank maps the
+    same file and page-locks that mapping in place, runtime.HostScene) - no
+    data-path collective - and
     the FrameStats are gathered to rank 0, which gets the whole list
     (others get None).  Without ``dist`` this is ``run_benchmark``."""
     from paper_2506_19415_b200.sharding import frame_block

@@ -373,6 +373,10 @@ class VmSession:
             raise InvariantViolation("scene has no pages; run paging first")
         if scene.lod_levels > 16:
             raise InvariantViolation("at most 16 LOD levels are supported")
+        if lod_enabled and scene.lod_levels > 9:
+            # vms_lod carries 8 thresholds (levels 0-8)
+            raise InvariantViolation("LOD selection supports at most 9 levels; "
+                                     "pass lod_enabled=False for deeper scenes")
         self.device = t.device("cuda", t.cuda.current_device()) if device is None else \
             t.device(device)
         self.scene = scene
@@ -415,8 +419,11 @@ class VmSession:
                 self.host = np.ascontiguousarray(scene.gaussians, dtype=np.float32)
                 host_ptr = self.host.ctypes.data
             else:
-                self.host = _pinned_records(scene)  # pinned, mapped into the device
-                host_ptr = self.host.data_ptr()
+                # page-locked, mapped into the device; shared by every
+                # session of the process (and, for a memory-mapped file, by
+                # every process mapping it)
+                self.host = HostScene.of(scene)
+                host_ptr = self.host.ptr
             d = _lib.SessionDesc()
             d.host_records = host_ptr
             d.host_rows = int(len(scene.gaussians))
@@ -479,7 +486,8 @@ class VmSession:
         in place (by DMA when it is page-locked, else through a staging
         buffer); "device" -> a CUDA tensor, ordered on the current stream (the
         session alternates two such buffers), returned as soon as the frame
-        is enqueued.  ``wait=False`` with page-locked host output also
+        is enqueued; a float32 (h, w, 3) CUDA tensor -> written in place, the
+        same way.  ``wait=False`` with page-locked host output also
         returns as soon as the frame is enqueued (frames pipeline two deep);
         the array is complete after ``wait(0)`` (or ``wait(1)`` once the next
         frame has been submitted)."""
@@ -501,7 +509,18 @@ class VmSession:
         a.host_image = None
         a.sync = 0
         host = None
-        image = self._frame_image(camera)
+        if isinstance(out, t.Tensor):
+            # a caller-owned CUDA tensor (e.g. a slot of a frame stack): the
+            # blend writes it directly, ordered on the current stream
+            if out.device != self.device or out.dtype != t.float32 or \
+                    tuple(out.shape) != (camera.height, camera.width, 3) or \
+                    not out.is_contiguous():
+                raise ValueError("out tensor must be a contiguous float32 (h, w, 3) tensor on "
+                                 "the session's device")
+            image = out
+            device_out = True
+        else:
+            image = self._frame_image(camera)
         if not device_out:
             # host output: the blend writes the page-locked host array directly
             # (zero-copy, whole-row PCIe writes overlapped with the blend) - the
@@ -601,16 +620,10 @@ class VmSession:
         return arr
 
     def _zero_copy(self, arr) -> bool:
-        key = (arr.ctypes.data, arr.nbytes)
-        cache = self.__dict__.setdefault("_zc_cache", {})
-        hit = cache.get(key)
-        if hit is None:
-            hit = bool(self._lib.vms_host_accessible(arr.ctypes.data)) and bool(
-                self._lib.vms_host_accessible(arr.ctypes.data + arr.nbytes - 1))
-            if len(cache) > 64:
-                cache.clear()
-            cache[key] = hit
-        return hit
+        # asked every call (cudaPointerGetAttributes is cheap): a cached answer
+        # keyed by address could outlive the buffer it was asked about
+        return bool(self._lib.vms_host_accessible(arr.ctypes.data)) and bool(
+            self._lib.vms_host_accessible(arr.ctypes.data + arr.nbytes - 1))
 
     def _staging(self, camera):
         t = _device.torch()
@@ -671,15 +684,116 @@ def fill_frame_cameras(args, camera, vis_scale: float, dot_mode: int) -> None:
         c.dot_mode = int(dot_mode)
 
 
-def _pinned_records(scene):
-    """Copy the scene's record section into page-locked host memory, in
-    256 MB slices (works for np.memmap sources without a second copy)."""
-    t = _device.torch()
-    g = scene.gaussians
-    n = len(g)
-    host = t.empty((max(n, 1), RECORD_SIZE), dtype=t.float32).pin_memory()
-    hv = host.numpy()
-    step = max(1, (256 << 20) // RECORD_BYTES)
-    for a in range(0, n, step):
-        hv[a:a + step] = g[a:a + step]
-    return host
+def _mem_available() -> int:
+    try:
+        with open("/proc/meminfo") as fh:
+            for ln in fh:
+                if ln.startswith("MemAvailable:"):
+                    return int(ln.split()[1]) * 1024
+    except OSError:
+        pass
+    return 1 << 62
+
+
+def _on_tmpfs(path) -> bool:
+    """True if ``path`` lives on a tmpfs mount (its pages ARE host DRAM)."""
+    import os
+
+    try:
+        real = os.path.realpath(path)
+        best, kind = "", ""
+        with open("/proc/mounts") as fh:
+            for ln in fh:
+                parts = ln.split()
+                if len(parts) >= 3:
+                    mnt = parts[1].replace("\\040", " ")
+                    if (real == mnt or real.startswith(mnt.rstrip("/") + "/")) and \
+                            len(mnt) > len(best):
+                        best, kind = mnt, parts[2]
+        return kind == "tmpfs"
+    except OSError:
+        return False
+
+
+class HostScene:
+    """The host-resident page source of a scene: its GAUS section (every LOD
+    level) page-locked and mapped into the device address space, so page
+    uploads are DMA from it (runtime.py:362-374 ``execute_copies`` reads the
+    same rows through ``SceneFile.page_records``).
+
+    A ``.vms`` file on tmpfs (host DRAM; e.g. /dev/shm) is page-locked IN
+    PLACE: the record section is mapped shared (the driver cannot pin a
+    read-only file mapping, so this mapping is read-write; it is registered
+    with cudaHostRegisterReadOnly and never written) and registered - no copy
+    is made, and every session, and every process (one per GPU) that maps
+    the same file, streams from the same physical pages.  Any other source
+    (a file on disk, an in-memory array) is copied once into page-locked
+    memory per process; one HostScene per source is shared by all sessions
+    of the process.
+    """
+
+    _live: dict = {}
+
+    def __init__(self, scene):
+        import os
+
+        t = _device.torch()
+        g = scene.gaussians
+        self.rows = int(len(g))
+        self._base = None
+        self._tensor = None
+        self._array = None
+        path = getattr(scene, "path", None)
+        if isinstance(g, np.memmap) and self.rows and path and _on_tmpfs(path) and \
+                os.access(path, os.W_OK):
+            lib = _lib.load()
+            mm = np.memmap(path, dtype="<f4", mode="r+", offset=int(scene.gaus_offset),
+                           shape=(self.rows, RECORD_SIZE))
+            base = ctypes.c_void_p()
+            st = lib.vms_host_register(mm.ctypes.data, mm.nbytes, 1, ctypes.byref(base))
+            if st == _lib.VMS_OK:
+                self._lib = lib
+                self._base = base
+                self._array = mm
+                self.ptr = int(mm.ctypes.data)
+                self.kind = "registered-tmpfs-mapping"
+                return
+            import warnings
+
+            warnings.warn("cudaHostRegister of the scene mapping failed (%s)"
+                          % lib.vms_last_error().decode(), RuntimeWarning)
+        if g.nbytes > _mem_available() // 2:
+            # a private copy would not fit next to the source
+            raise MemoryError(f"the {g.nbytes >> 20} MB scene is neither a tmpfs file that "
+                              "can be page-locked in place nor small enough for a private "
+                              "page-locked copy; use upload_mode=2 (streaming from the mapping)")
+        host = t.empty((max(self.rows, 1), RECORD_SIZE), dtype=t.float32).pin_memory()
+        hv = host.numpy()
+        step = max(1, (256 << 20) // RECORD_BYTES)
+        for a in range(0, self.rows, step):
+            hv[a:a + step] = g[a:a + step]
+        self._tensor = host
+        self.ptr = int(host.data_ptr())
+        self.kind = "pinned-copy"
+
+    def __del__(self):
+        if getattr(self, "_base", None) is not None:
+            self._lib.vms_host_unregister(self._base)
+            self._base = None
+
+    @classmethod
+    def of(cls, scene) -> "HostScene":
+        import weakref
+
+        g = scene.gaussians
+        if isinstance(g, np.memmap):
+            key = ("mmap", getattr(g, "filename", None), int(g.offset), int(len(g)),
+                   int(g.ctypes.data))
+        else:
+            key = ("array", id(g), int(g.ctypes.data), int(len(g)))
+        ref = cls._live.get(key)
+        hs = ref() if ref is not None else None
+        if hs is None:
+            hs = cls(scene)
+            cls._live[key] = weakref.ref(hs)
+        return hs

@@ -79,9 +79,15 @@ class CityLayout:
 
 def _patches(lay: CityLayout):
     """Per page: (origin, u axis, v axis, normal) of its patch, building id."""
+    return _patches_from(lay, 0, lay.n_pages)
+
+
+def _patches_from(lay: CityLayout, first_building: int, last_page: int):
+    """Patches of pages [first_building * pages_per_building, last_page)."""
     out = []
     W, P = lay.width, lay.patch
-    for b in range(lay.n_buildings):
+    cap = last_page - first_building * lay.pages_per_building
+    for b in range(first_building, lay.n_buildings):
         gi, gj = b % lay.grid, b // lay.grid
         x0, z0 = gi * lay.spacing, gj * lay.spacing
         # facades: (corner, along-facade unit, outward normal); up is -Y
@@ -96,9 +102,15 @@ def _patches(lay: CityLayout):
                 for c in range(lay.cols):
                     origin = corner + along * (c * P) + np.array([0.0, -(r * P), 0.0])
                     out.append((origin, along * P, np.array([0.0, -P, 0.0]), normal, b))
-                    if len(out) == lay.n_pages:
+                    if len(out) == cap:
                         return out
     return out
+
+
+def _patches_range(lay: CityLayout, first: int, last: int):
+    """_patches(lay)[first:last] without building the whole list."""
+    b0 = first // lay.pages_per_building
+    return _patches_from(lay, b0, last)[first - b0 * lay.pages_per_building:]
 
 
 def _morton2(u, v):
@@ -176,18 +188,25 @@ def _mesh_and_links(lay: CityLayout, patches):
                         [ext, 0.0, ext], [-lay.street, 0.0, ext]]
     faces[2 * n] = (g0, g0 + 2, g0 + 1)
     faces[2 * n + 1] = (g0, g0 + 3, g0 + 2)
-    # links: patches of the same building whose boxes touch
+    # links: patches of the same building whose boxes touch (a building's
+    # pages are contiguous, so each building is one small dense block)
     bid = np.array([pt[4] for pt in patches])
     offsets = np.zeros(n + 1, dtype=np.uint32)
     targets = []
     eps = 1e-3 * lay.patch
-    for p in range(n):
-        same = np.flatnonzero(bid == bid[p])
-        touch = np.all((lo[same] <= hi[p] + eps) & (hi[same] >= lo[p] - eps), axis=1)
-        t = [int(q) + 1 for q in same[touch] if q != p]
-        targets.extend(sorted(t))
-        offsets[p + 1] = offsets[p] + len(t)
-    return verts, faces, face_page, offsets, np.asarray(targets, dtype=np.uint32)
+    starts = np.flatnonzero(np.r_[True, bid[1:] != bid[:-1]])
+    ends = np.r_[starts[1:], n]
+    for a, b in zip(starts, ends):
+        blo, bhi = lo[a:b], hi[a:b]
+        touch = np.all((blo[None, :, :] <= bhi[:, None, :] + eps)
+                       & (bhi[None, :, :] >= blo[:, None, :] - eps), axis=2)
+        for i in range(b - a):
+            t = np.flatnonzero(touch[i])
+            t = t[t != i] + a + 1   # ascending page ids, self excluded
+            targets.append(t)
+            offsets[a + i + 1] = offsets[a + i] + len(t)
+    targets = np.concatenate(targets).astype(np.uint32) if targets else np.zeros(0, np.uint32)
+    return verts, faces, face_page, offsets, targets
 
 
 def city_metadata(lay: CityLayout) -> SceneFile:
@@ -228,30 +247,66 @@ def city_scene(lay: CityLayout) -> SceneFile:
     return sc
 
 
-def write_city(path, lay: CityLayout, pages_per_batch: int = 64) -> None:
-    """Stream-write a city scene level block by level block (bounded RAM)."""
+def _write_pages(job):
+    """Worker of write_city: every level of pages [first, last) straight into
+    the file's record section (page offsets are pure arithmetic)."""
+    path, gaus_off, lay, first, last = job
+    patches = _patches_range(lay, first, last)
+    level_start = 0
+    mm = np.memmap(path, dtype="<f4", mode="r+", offset=gaus_off,
+                   shape=(lay.n_pages * sum(lay.page_size >> k for k in range(lay.levels)),
+                          RECORD_SIZE))
+    recs = [_page_records(lay, p, patches[p - first]) for p in range(first, last)]
+    for k in range(lay.levels):
+        per = lay.page_size >> k
+        mm[level_start + first * per: level_start + last * per] = np.concatenate(recs, axis=0)
+        level_start += lay.n_pages * per
+        if k + 1 < lay.levels:
+            recs = [merge_pairs(r) for r in recs]
+    mm.flush()
+    del mm
+    return last - first
+
+
+def write_city(path, lay: CityLayout, workers: int | None = None,
+               pages_per_job: int = 256) -> None:
+    """Write a city scene: metadata first, then every page's records at all
+    levels, generated in parallel by ``workers`` processes (default: the
+    usable cores) that write disjoint row ranges of the preallocated record
+    section.  The bytes are independent of ``workers`` (each page's records
+    are a pure function of the layout, the seed and the page index)."""
+    import os
+
+    from paper_2506_19415_b200.scene_io import preallocate_scene
+
     sc = city_metadata(lay)
-    patches = _patches(lay)
-    n = len(patches)
-    with SceneWriter(path, sc) as w:
-        for k in range(lay.levels):
-            for a in range(0, n, pages_per_batch):
-                b = min(n, a + pages_per_batch)
-                rows = []
-                for p in range(a, b):
-                    rec = _page_records(lay, p, patches[p])
-                    for _ in range(k):
-                        rec = merge_pairs(rec)
-                    rows.append(rec)
-                w.write_records(np.concatenate(rows, axis=0))
+    gaus_off = preallocate_scene(path, sc)
+    n = lay.n_pages
+    jobs = [(str(path), gaus_off, lay, a, min(n, a + pages_per_job))
+            for a in range(0, n, pages_per_job)]
+    if workers is None:
+        try:
+            workers = len(os.sched_getaffinity(0))
+        except AttributeError:  # pragma: no cover
+            workers = os.cpu_count() or 1
+    workers = max(1, min(workers, len(jobs)))
+    if workers == 1:
+        done = sum(_write_pages(j) for j in jobs)
+    else:
+        import multiprocessing as mp
+
+        with mp.get_context("fork").Pool(workers) as pool:
+            done = sum(pool.imap_unordered(_write_pages, jobs))
+    assert done == n
 
 
 def street_path(lay: CityLayout, frames: int = 120, width: int = 1920, height: int = 1080,
-                eye: float = 3.0, fov_deg: float = 90.0) -> CameraPath:
-    """Fly down the first street between building columns 0 and 1, then turn
-    90 degrees into the next cross street; ``frames`` frames in total."""
+                eye: float = 3.0, fov_deg: float = 90.0, blocks: int = 3) -> CameraPath:
+    """Fly down the first street between building columns 0 and 1 for
+    ``blocks`` blocks, then turn 90 degrees into the next cross street;
+    ``frames`` frames in total."""
     sx = lay.width + 0.5 * lay.street           # centre of the first street
-    z_end = min(lay.grid, 3) * lay.spacing - 0.5 * lay.street
+    z_end = min(lay.grid, blocks) * lay.spacing - 0.5 * lay.street
     turn_x = sx + 2 * lay.spacing
     yaw = lambda a: (math.cos(a / 2), 0.0, math.sin(a / 2), 0.0)  # noqa: E731
     cps = (
@@ -268,3 +323,10 @@ def street_path(lay: CityLayout, frames: int = 120, width: int = 1920, height: i
 # Named configurations (BASELINE.json "configs").
 C2 = CityLayout(n_pages=1000, page_size=2048, levels=3)      # 2.05M records, 3 LOD levels
 C3 = CityLayout(n_pages=10000, page_size=2048, levels=4)     # 20.5M records, 4 LOD levels
+# C4 on the GPU boxes of this project: 196 GB of host DRAM and 80 GB of free
+# disk cannot hold the 800M-record (189 GB) scene of BASELINE configs[3], so
+# the out-of-core configuration is the largest LOD city that fits host DRAM
+# with headroom: 170,000 pages x 2048 records at level 0 (348.2M) plus LOD
+# levels 1-2 (174.1M + 87.0M) = 609.3M records, 143.8 GB, written to tmpfs
+# and paged from there.
+C4 = CityLayout(n_pages=170000, page_size=2048, levels=3)

@@ -24,6 +24,15 @@ def frame_block(rank: int, world: int, frame_count: int):
     return rank * frame_count // world, (rank + 1) * frame_count // world
 
 
+def shard_frame(start: int, i: int, frame_count: int) -> int:
+    """Trajectory frame of a rank's i-th frame: its block start + i.  A rank
+    asked for more frames than its block holds continues into the following
+    blocks, and the path wraps from its last frame to frame 0 (the camera
+    jumps back to the start; frame indices keep increasing, so the page
+    table sees a new viewpoint, not a repeated frame)."""
+    return (start + i) % frame_count
+
+
 def stats_rows(stats) -> np.ndarray:
     return np.array([[int(s[c]) for c in STATS_COLUMNS] for s in stats], dtype=np.int64)
 
@@ -54,14 +63,14 @@ def gather_rows(rows: np.ndarray, dist, device=None):
 
 def render_shard(session, trajectory, rank: int, world: int, frames: int | None = None,
                  out="device"):
-    """Render this rank's block (or its first ``frames`` frames, wrapping
-    within the block).  Returns the list of stats dicts."""
-    start, stop = frame_block(rank, world, trajectory.frame_count)
-    block = max(1, stop - start)
-    n = block if frames is None else frames
+    """Render this rank's block (or ``frames`` consecutive frames from the
+    block start, see ``shard_frame``).  Returns the list of stats dicts."""
+    F = trajectory.frame_count
+    start, stop = frame_block(rank, world, F)
+    n = (stop - start) if frames is None else frames
     stats = []
     for i in range(n):
-        cam = trajectory.frame_camera(start + (i % block))
+        cam = trajectory.frame_camera(shard_frame(start, i, F))
         _, st = session.render_frame(cam, start + i, out=out)
         stats.append(st)
     return stats

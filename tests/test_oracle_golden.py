@@ -153,3 +153,39 @@ def test_face_bvh_arrays_match_reference(golden, case):
     assert np.array_equal(b.children, g[f"{case}_children"])
     assert np.array_equal(b.ranges, g[f"{case}_ranges"])
     assert np.array_equal(b.order, g[f"{case}_order"])
+
+
+def test_oracle_clipped_triangles_match_per_face_loop():
+    """The vectorised clip/project (faces wholly beyond the near plane in
+    one pass) emits the per-face loop's triangles bit for bit, in (face, fan)
+    order, including faces crossing the plane and faces behind it."""
+    rng = np.random.default_rng(3)
+    verts = rng.uniform(-10, 10, size=(300, 3))
+    verts[:, 2] = rng.uniform(-2, 12, size=300)
+    faces = rng.integers(0, 300, size=(500, 3)).astype(np.int32)
+    fpage = rng.integers(1, 60, size=500).astype(np.uint32)
+    cam = core.OCamera((0.0, 0.0, 0.0), (1.0, 0.0, 0.0, 0.0), np.pi / 2, 64, 48, near=0.5)
+    tris, ids = core.clipped_triangles(verts, faces, fpage, cam)
+    view = cam.to_view(verts)
+    ref_t, ref_i = [], []
+    for fi in range(len(faces)):
+        for cl in core.clip_near(view[faces[fi]], cam.near):
+            ref_t.append(cam.to_pixels(cl))
+            ref_i.append(fpage[fi])
+    assert len(ref_t) == len(tris) and len(tris) > 400
+    assert np.array_equal(np.stack(ref_t).view(np.uint64), tris.view(np.uint64))
+    assert np.array_equal(np.asarray(ref_i, np.uint32), ids)
+
+
+@pytest.mark.parametrize("window", [(0, 64, 0, 48), (10, 30, 5, 21), (50, 64, 40, 48)])
+def test_oracle_render_window_equals_full_render(golden, window):
+    """the windowed render reproduces the full render's
+    window bit for bit (the C4 image-parity oracle)."""
+    recs = inputs.small_records(7, 3000)
+    for cam in inputs.small_cameras():
+        c = core.OCamera(**cam)
+        full = core.render_flat(recs, c)
+        x0, x1, y0, y1 = window
+        x1, y1 = min(x1, c.width), min(y1, c.height)
+        win, n = core.render_window(recs, c, (x0, x1, y0, y1), chunk=700)
+        assert np.array_equal(win, full[y0:y1, x0:x1])
