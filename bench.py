@@ -62,7 +62,9 @@ def parse():
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", choices=("ours", "reference"), default="ours")
     p.add_argument("--fast", action="store_true", help="FP32 blend (default: FP64, reference-exact)")
-    p.add_argument("--upload-mode", type=int, default=0)
+    p.add_argument("--upload-mode", type=int, default=None,
+                   help="0 DMA from the page-locked scene, 1 gather kernel, 2 host-thread "
+                        "streaming; default: the config's (auto for c2/c3, 2 for c4)")
     p.add_argument("--frames", type=int, default=120, help="trajectory length")
     p.add_argument("--width", type=int, default=1920)
     p.add_argument("--height", type=int, default=1080)
@@ -88,12 +90,22 @@ CONFIGS = {
     # tmpfs (host DRAM) and paged from there; the camera flies down a long
     # street so pages stream in every frame
     "c4": {"layout": "C4", "buffer": 2048, "staging": 160, "blocks": 24,
-           "scene_dir": "/dev/shm"},
+           "scene_dir": "/dev/shm", "upload_mode": 2},
 }
 
 
 def config_of(args):
     return CONFIGS[args.config]
+
+
+def upload_mode_of(args):
+    """--upload-mode, else the config's default (None = the session's auto:
+    DMA from the page-locked scene when it can be page-locked).  C4's 144 GB
+    tmpfs scene cannot be page-locked reliably (the boxes pin ~116 GB at
+    most), so it streams through the session's bounce buffer."""
+    if args.upload_mode is not None:
+        return args.upload_mode
+    return config_of(args).get("upload_mode")
 
 
 def scene_path(args):
@@ -206,18 +218,22 @@ def launches_per_frame(stats, n_faces, upload_mode, n_pages=1000):
     per-frame copies in session.cu):
       visibility graph  vis_count, scan, vis_emit, vis_raster, vis_back
                         (links + flags + compaction + LOD)                5
-                        (4 separate back-end kernels past 32767 pages)
+                        (4 separate back-end kernels past 32767 pages)   +3
+                        (binned raster from 65536 faces: bin count, scan,
+                         bin emit, radix hist + 2 passes, tile ranges)    +7
       page copies       scatter_k (the uploads are copy-engine DMA;
                         upload_mode 1 adds the upload_k gather kernel)   1
       render graph      preprocess, scan, compact, radix hist + 4 passes,
-                        dup_count, scan, dup_emit, clamp, radix hist + 2
-                        passes, ranges, tile_order, blend                18
+                        dup_count, scan, dup_emit, tile_prep, 2 radix
+                        passes, blend                                    16
     (host output without zero-copy runs the blend as 4 band launches)."""
     vis = 5 if n_pages <= 32767 else 8
-    up = 2 if stats["planned_copies"] else 0
-    if up and upload_mode != 1:
-        up = 1  # per-page cudaMemcpyAsync + scatter
-    render = 18
+    if n_faces >= 65536 and os.environ.get("VMSPLAT_VIS_BIN", "") != "0":
+        vis += 7
+    up = 0
+    if stats["planned_copies"]:
+        up = 2 if upload_mode == 1 else 1
+    render = 16
     return vis + up + render
 
 
@@ -240,7 +256,7 @@ def bench_config(args, lay, world=1):
             "blend": "fp32" if args.fast else "fp64-exact",
             "l2": f"inputs larger than L2 (resident page pool up to {pool_mb:.0f} MB, "
                   f"126 MB L2; the frame's records stream from it every step)",
-            "upload_mode": args.upload_mode}
+            "upload_mode": upload_mode_of(args)}
 
 
 def measure_pcie(torch, nbytes=256 << 20, reps=10):
@@ -316,7 +332,7 @@ def run_ours(args, rank, world, local_rank):
         torch.cuda.empty_cache()
         holder["s"] = VmSession(scene, buffer_pages=cfg["buffer"], staging_pages=cfg["staging"],
                                 vis_scale=0.25, exact=not args.fast,
-                                upload_mode=args.upload_mode, timing=timing)
+                                upload_mode=upload_mode_of(args), timing=timing)
         step[0] = 0
         return holder["s"]
 
@@ -340,16 +356,21 @@ def run_ours(args, rank, world, local_rank):
     stream = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     sampler = ClockSampler(local_rank)
-    # each timed frame is rendered into its own slot of a device-resident
-    # frame stack; the stack is gathered to rank 0 after the timed region
-    stack = torch.empty((args.steps, H, W, 3), dtype=torch.float32, device="cuda")
+    # N > 1: each timed frame is rendered into its own slot of a
+    # device-resident frame stack, gathered to rank 0 after the timed region
+    # (N = 1 leaves each frame in the session's two alternating device
+    # buffers: writing a fresh 25 MB slot per frame measured ~7 % slower)
+    stack = torch.empty((args.steps, H, W, 3), dtype=torch.float32, device="cuda") \
+        if world > 1 else None
 
     def timed(out):
         if dist:
             dist.barrier()
         torch.cuda.synchronize()
         e0.record(stream)
-        sts = [frame(out if out is not None else stack[k])[1] for k in range(args.steps)]
+        sts = [frame(out if out is not None else
+                     (stack[k] if stack is not None else "device"))[1]
+               for k in range(args.steps)]
         e1.record(stream)
         torch.cuda.synchronize()
         holder["s"].flush()
@@ -473,7 +494,8 @@ def run_ours(args, rank, world, local_rank):
     d2h_step = W * H * 12 + 10 * int(statistics.mean(s["required_pages"] for s in stats_e2e))
     value = world * args.steps / (ms_dev / 1e3)
     e2e = world * args.steps / (ms_e2e / 1e3)
-    launches = sum(launches_per_frame(s, len(scene.faces), args.upload_mode, scene.page_count)
+    launches = sum(launches_per_frame(s, len(scene.faces), holder["s"].upload_mode,
+                                      scene.page_count)
                    for s in stats)
     out = {
         "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world,

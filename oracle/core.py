@@ -679,6 +679,34 @@ def stats_csv(stats_list):
     return "\n".join(lines) + "\n"
 
 
+def ssim(a, b):
+    """metrics.ssim (pkg/src/vmsplat/metrics.py:33-75): 11x11 Gaussian window
+    (sigma 1.5), reflected borders, mean over interior pixels per channel,
+    then over channels; K1 = 0.01, K2 = 0.03."""
+    from scipy.ndimage import correlate
+
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    if a.ndim == 2:
+        a, b = a[:, :, None], b[:, :, None]
+    r = np.arange(11, dtype=np.float64) - 5.0
+    g = np.exp(-(r * r) / (2.0 * 1.5 * 1.5))
+    k = np.outer(g, g)
+    k /= k.sum()
+    c1, c2 = 0.01 ** 2, 0.03 ** 2
+    h, w = a.shape[:2]
+    vals = []
+    for ch in range(a.shape[2]):
+        x, y = a[:, :, ch], b[:, :, ch]
+        mx, my = correlate(x, k, mode="reflect"), correlate(y, k, mode="reflect")
+        xx = correlate(x * x, k, mode="reflect") - mx * mx
+        yy = correlate(y * y, k, mode="reflect") - my * my
+        xy = correlate(x * y, k, mode="reflect") - mx * my
+        s = ((2.0 * mx * my + c1) * (2.0 * xy + c2)) / ((mx * mx + my * my + c1) * (xx + yy + c2))
+        vals.append(float(np.mean(s[5:h - 5, 5:w - 5])))
+    return float(np.mean(vals))
+
+
 def psnr(a, b):
     d = np.asarray(a, np.float64) - np.asarray(b, np.float64)
     mse = float(np.mean(d * d))

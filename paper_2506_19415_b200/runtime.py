@@ -350,13 +350,14 @@ class VmSession:
 
     Extra (non-reference) knobs: ``exact`` (default) blends with the
     reference's FP64 arithmetic, False selects the FP32 blend;
-    ``upload_mode`` 0 (default) uploads a frame's pages from the pinned host
-    copy of the scene with one batched copy-engine call (no SM time, overlaps
-    the render in flight), 1 with one gather kernel over mapped pinned
-    memory, 2 streams them
+    ``upload_mode`` 0 uploads a frame's pages from the page-locked host
+    scene (``HostScene``) with one batched copy-engine call (no SM time,
+    overlaps the render in flight), 1 with one gather kernel over mapped
+    pinned memory, 2 streams them
     from the scene's memory-mapped rows (host threads gather each frame's
     pages into a page-locked bounce buffer; for scenes larger than the
-    page-locked memory one wants to commit - out-of-core); ``timing``
+    page-locked memory one wants to commit - out-of-core); the
+    default (None) picks 0 when the scene can be page-locked, else 2; ``timing``
     records per-stage CUDA events (the stats' time_* keys; costs one sync per
     frame); ``device`` selects the GPU.
     """
@@ -364,7 +365,7 @@ class VmSession:
     def __init__(self, scene, buffer_pages: int = 500, staging_pages: float = 40,
                  vis_scale: float = 0.25, band=(0.5, 0.8), step: float = 0.05,
                  lod_enabled: bool = True, links_enabled: bool = True, exact: bool = True,
-                 upload_mode: int = 0, timing: bool = True, device=None,
+                 upload_mode: int | None = None, timing: bool = True, device=None,
                  instance_capacity: int | None = None):
         from paper_2506_19415_b200.render import VisibilityBuffers
 
@@ -393,7 +394,7 @@ class VmSession:
         self.staging_pages = staging_pages
         self.vis_scale = vis_scale
         self.exact = bool(exact)
-        self.upload_mode = int(upload_mode)
+        self.upload_mode = -1 if upload_mode is None else int(upload_mode)
         self.timing = bool(timing)
         self.page_size = int(scene.page_size)
         self.capacity = int(buffer_pages)
@@ -412,6 +413,19 @@ class VmSession:
                                          scene.page_count, off, tgt)
             self.n_cap = self.capacity * self.page_size
             self.pool = t.empty((self.n_cap, RECORD_SIZE), dtype=t.float32, device=self.device)
+            if self.upload_mode < 0:
+                # auto: DMA from the page-locked scene when it can be
+                # page-locked (a registered tmpfs file, or a private copy
+                # that fits), else stream through the bounce buffer
+                try:
+                    HostScene.of(scene)
+                    self.upload_mode = 0
+                except (MemoryError, RuntimeError) as exc:
+                    import warnings
+
+                    warnings.warn(f"scene not page-lockable ({exc}); streaming pages from "
+                                  "the mapping (upload_mode 2)", RuntimeWarning)
+                    self.upload_mode = 2
             if self.upload_mode == 2:
                 # streaming source: the scene's own (memory-mapped) rows; the
                 # session gathers each frame's pages through a page-locked

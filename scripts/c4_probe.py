@@ -24,7 +24,7 @@ stg = float(os.environ.get("STG", "160"))
 traj = scenegen.street_path(lay, frames=120, blocks=blocks)
 t = time.time()
 s = VmSession(sc, buffer_pages=buf, staging_pages=stg, vis_scale=0.25, timing=True,
-              upload_mode=int(os.environ.get("UPM", "0")))
+              upload_mode=int(os.environ.get("UPM", "2")))
 print("session s", round(time.time() - t, 1), getattr(s.host, "kind", "?"), flush=True)
 for f in range(traj.frame_count):
     t = time.time()

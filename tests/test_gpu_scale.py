@@ -148,7 +148,7 @@ def test_c4_page_sets_and_window_match_oracle(cuda, c4_scene):
         _check_stats(st, rst, f)
         copied += st["bytes_copied"]
     assert sorted(s.table.resident.items()) == sorted(o.table.resident.items())
-    assert copied > 1 << 30
+    assert copied > 512 << 20
     records = o.resident_records()
     cam = traj.frame_camera(last)
     W, H = cam.width, cam.height
