@@ -220,7 +220,8 @@ def launches_per_frame(stats, n_faces, upload_mode, n_pages=1000):
                         (links + flags + compaction + LOD)                5
                         (4 separate back-end kernels past 32767 pages)   +3
                         (binned raster from 65536 faces: bin count, scan,
-                         bin emit, radix hist + 2 passes, tile ranges)    +7
+                         bin emit, radix hist + 2 passes, tile ranges,
+                         chunk count, scan, merge)                       +10
       page copies       scatter_k (the uploads are copy-engine DMA;
                         upload_mode 1 adds the upload_k gather kernel)   1
       render graph      preprocess, scan, compact, radix hist + 4 passes,
@@ -229,7 +230,7 @@ def launches_per_frame(stats, n_faces, upload_mode, n_pages=1000):
     (host output without zero-copy runs the blend as 4 band launches)."""
     vis = 5 if n_pages <= 32767 else 8
     if n_faces >= 65536 and os.environ.get("VMSPLAT_VIS_BIN", "") != "0":
-        vis += 7
+        vis += 10
     up = 0
     if stats["planned_copies"]:
         up = 2 if upload_mode == 1 else 1

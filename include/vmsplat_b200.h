@@ -321,6 +321,11 @@ typedef struct vms_session_desc {
   int32_t upload_mode;          /* 0/1: see vms_upload_pages; 2: streaming - planned rows are
                                    gathered by host threads into a page-locked bounce buffer,
                                    one cudaMemcpyAsync per frame */
+  int32_t host_fd;              /* upload_mode 2: >= 0 -> the rows are read with pread() from
+                                   this file (the .vms) at host_fd_offset + row * 236 instead
+                                   of being copied out of host_records (no page faults on a
+                                   fresh mapping); -1 -> copy from host_records */
+  uint64_t host_fd_offset;      /* byte offset of the record section in host_fd */
 } vms_session_desc;
 
 typedef struct vms_frame_args {
@@ -348,7 +353,8 @@ typedef struct vms_frame_stats {
   uint32_t n_kept, n_inst, overflow, n_need;  /* valid when the call synchronised */
   uint32_t pad_;
   int64_t resident_per_level[16];
-  float ms_vis, ms_copy, ms_preprocess, ms_sort, ms_tiles, ms_blend, ms_frame, ms_pad;
+  float ms_vis, ms_copy, ms_preprocess, ms_sort, ms_tiles, ms_blend, ms_frame;
+  float ms_host_gather;         /* upload_mode 2: host time reading the planned rows */
   double host_update_s;
 } vms_frame_stats;
 

@@ -74,7 +74,8 @@ class SessionDesc(ctypes.Structure):
                 ("link_off", P), ("link_tgt", P), ("pool", P), ("capacity", U32),
                 ("m_cap", U32), ("vis_ws", P), ("render_ws", P),
                 ("render_ws_bytes", ctypes.c_uint64), ("width", I32), ("height", I32),
-                ("exact", I32), ("upload_mode", I32)]
+                ("exact", I32), ("upload_mode", I32), ("host_fd", I32),
+                ("host_fd_offset", ctypes.c_uint64)]
 
 
 class FrameArgs(ctypes.Structure):
@@ -92,7 +93,7 @@ class FrameStats(ctypes.Structure):
                 ("ms_copy", ctypes.c_float), ("ms_preprocess", ctypes.c_float),
                 ("ms_sort", ctypes.c_float), ("ms_tiles", ctypes.c_float),
                 ("ms_blend", ctypes.c_float), ("ms_frame", ctypes.c_float),
-                ("ms_pad", ctypes.c_float), ("host_update_s", D)]
+                ("ms_host_gather", ctypes.c_float), ("host_update_s", D)]
 
 
 # name -> (restype, argtypes); every symbol include/vmsplat_b200.h declares

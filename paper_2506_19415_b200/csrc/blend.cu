@@ -399,8 +399,21 @@ __device__ unsigned long long* g_blend_trace = nullptr;
 // depth-sorted splat list `vals` instead, filtering by its own sub-tile - the
 // same per-tile order, so the image is identical, only slower.  The host
 // sees the overflow counter afterwards and grows the buffer for later frames.
-template <bool kExact, int TS>
-__global__ void __launch_bounds__(kBlendThreads, 4) blend_k(const uint32_t* __restrict__ ranges,
+// kSparse (exact mode): the splats of a warp's group are processed splat-
+// parallel instead of pixel-parallel - lane k evaluates the weights of splat
+// k of the group over the pixels of its box inside the warp's 8x4 block
+// (skipping saturated pixels) into shared memory, a ballot transpose gives
+// every pixel the (list-ordered) mask of splats with a live weight for it,
+// and each lane then applies only those, in list order.  Same arithmetic,
+// same order per pixel - only the lanes' work assignment changes: small
+// splats (the vanishing-point tiles' long lists) no longer occupy all 32
+// lanes for the few pixels they touch.
+constexpr int kSparseGroup = 16;   // splats per weight pass (shared-memory budget)
+constexpr int kSparseRow = 33;     // padded row of doubles (bank spread)
+constexpr size_t kSparseSmem = sizeof(double) * (kBlendThreads / 32) * kSparseGroup * kSparseRow;
+
+template <bool kExact, int TS, bool kSparse = false>
+__global__ void __launch_bounds__(kBlendThreads, kSparse ? 3 : 4) blend_k(const uint32_t* __restrict__ ranges,
                                                          const uint32_t* __restrict__ order,
                                                          const uint32_t* __restrict__ tv_tiles,
                                                          const uint32_t* __restrict__ vals,
@@ -410,17 +423,20 @@ __global__ void __launch_bounds__(kBlendThreads, 4) blend_k(const uint32_t* __re
                                                          uint32_t order_offset,
                                                          float* image_arg,
                                                          const FrameDev* __restrict__ fd,
-                                                         int accumulate) {
+                                                         int accumulate,
+                                                         const uint32_t* __restrict__ tile_hot) {
   pdl_wait();
   constexpr int SUB = TS / 16;  // sub-tiles per tile edge
   using Staged = typename std::conditional<kExact, SplatF64, BlendRec>::type;
   __shared__ Staged sp[kBlendThreads];
   __shared__ uint32_t wsum[kBlendThreads / 32];
   __shared__ double2 tab[kExact ? 64 : 1];
+  extern __shared__ double wbuf[];  // kSparse: (warps) x kSparseGroup x kSparseRow
   unsigned long long t_start = 0;
   unsigned long long* trace = g_blend_trace;
   if (trace && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
   const int tile = order[order_offset + blockIdx.x / (SUB * SUB)], sub = blockIdx.x % (SUB * SUB);
+  if (tile_hot && tile_hot[tile]) return;  // blend_hot_k owns this tile's pixels
   const int sx0 = (tile % tiles_x) * TS + (sub % SUB) * 16;
   const int sy0 = (tile / tiles_x) * TS + (sub / SUB) * 16;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -505,7 +521,70 @@ __global__ void __launch_bounds__(kBlendThreads, 4) blend_k(const uint32_t* __re
       }
       uint32_t m = __ballot_sync(0xffffffffu, mine);
       const Staged* __restrict__ grp = sp + c0;
-      if constexpr (kExact) {
+      if constexpr (kExact && kSparse) {
+        double* __restrict__ wrow = wbuf + warp * (kSparseGroup * kSparseRow);
+        for (int g0 = 0; g0 < 32 && (m >> g0); g0 += kSparseGroup) {
+          const uint32_t gm = (m >> g0) & ((1u << kSparseGroup) - 1u);
+          if (!gm) continue;
+          // saturated (or off-image) pixels of the block: lane = pixel
+          const uint32_t done = __ballot_sync(0xffffffffu, T < kStopF);
+          if (done == 0xffffffffu) break;
+          // weight pass: lane l owns splat g0 + (l & 15) over block rows
+          // 2 (l >> 4) and 2 (l >> 4) + 1
+          uint32_t pm = 0;
+          const int k = lane & (kSparseGroup - 1), half = lane >> 4;
+          if ((gm >> k) & 1u) {
+            const Staged& q = grp[g0 + k];
+            const int bx0 = max(q.x0 - wx0, 0), bx1 = min(q.x0 + q.xw - wx0, 8);
+            const int by0 = max(q.y0 - wy0, 2 * half), by1 = min(q.y0 + q.yh - wy0, 2 * half + 2);
+            double* __restrict__ row = wrow + k * kSparseRow;
+            for (int yy = by0; yy < by1; ++yy) {
+              const double fyq = (double)(wy0 + yy) + 0.5;
+              const double dy = __dsub_rn(fyq, q.cy);
+              const double syy = __dmul_rn(__dmul_rn(q.cc, dy), dy);
+              const double sxy = __dmul_rn(q.cb2, dy);
+              for (int xx = bx0; xx < bx1; ++xx) {
+                const int pbit = yy * 8 + xx;
+                if ((done >> pbit) & 1u) continue;
+                const double dx = __dsub_rn((double)(wx0 + xx) + 0.5, q.cx);
+                // the dense loop's sigma: ((a dx) dx + (2b dy) dx) + (c dy) dy
+                const double sg = __dadd_rn(__dadd_rn(__dmul_rn(__dmul_rn(q.ca, dx), dx),
+                                                      __dmul_rn(sxy, dx)),
+                                            syy);
+                if (sg < q.skip) continue;
+                double wk = __dmul_rn(q.al, exp_tab(sg, tab));
+                if (wk > kBlendC[8]) wk = kBlendC[8];
+                row[pbit] = wk;
+                pm |= 1u << pbit;
+              }
+            }
+          }
+          // transpose: this lane's pixel gets the mask of splats with a live
+          // weight for it (bit k = splat g0 + k: list order = bit order); a
+          // pixel's bits come from one half of the lanes only
+          uint32_t mine_w = 0;
+#pragma unroll
+          for (int pbit = 0; pbit < 32; ++pbit) {
+            const uint32_t b = __ballot_sync(0xffffffffu, (pm >> pbit) & 1u);
+            if (lane == pbit) mine_w = (b | (b >> 16)) & 0xFFFFu;
+          }
+          __syncwarp();
+          while (mine_w) {
+            const int j = __ffs(mine_w) - 1;
+            mine_w &= mine_w - 1;
+            if (T < kStopF) break;
+            const Staged& q = grp[g0 + j];
+            const double wgt = wrow[j * kSparseRow + lane];
+            const double t = (double)T;
+            const double wt = __dmul_rn(wgt, t);
+            cr = __double2float_rn(__dadd_rn((double)cr, __dmul_rn(wt, q.r)));
+            cg = __double2float_rn(__dadd_rn((double)cg, __dmul_rn(wt, q.g)));
+            cb = __double2float_rn(__dadd_rn((double)cb, __dmul_rn(wt, q.b)));
+            T = __double2float_rn(__dmul_rn(t, __dsub_rn(1.0, wgt)));
+          }
+          __syncwarp();
+        }
+      } else if constexpr (kExact) {
         // two splats per step: their box tests and sigmas (independent of T)
         // are evaluated together, so rejections - most of the walk for pixels
         // that never saturate - overlap; the exp and the T/colour updates then
@@ -654,6 +733,240 @@ __global__ void __launch_bounds__(kBlendThreads, 4) blend_k(const uint32_t* __re
   }
 }
 
+// ---- hot tiles: long lists (a street's vanishing point) ---------------------
+// A tile whose list holds >= kHotLen instances is blended by blend_hot_k
+// instead: one CTA per 8x4 pixel block (the regular kernel's warp block), so
+// the tile's pixels spread over many SMs, and inside the CTA the work of
+// one pixel chain is split - 7 producer warps take the list in 32-entry
+// chunks (round robin), test each entry's box against the block and compute
+// the FP64 weights of the hits for all 32 pixels into a shared-memory ring
+// (plus a live-pixel mask per hit), while 1 consumer warp applies them in
+// list order (chunk order, then hit order) to its 32 pixels.  The weight and
+// the update are the regular kernel's arithmetic, in the same order per
+// pixel; only the chain of T/colour updates is serial, and it no longer
+// waits for the exp.
+// Measured: C2's vanishing-point lists (4-12 K) blend faster in the regular
+// kernel; C4's (50-560 K) twice as fast here (profiles/r2)
+constexpr uint32_t kHotLen = 32768;
+constexpr int kMaxHot = 64;        // tiles per frame on the hot path
+constexpr int kHotRing = 6;        // chunks in flight
+constexpr int kHotProducers = 7;
+
+struct HotSlot {
+  double w[32][32];  // [hit][pixel]
+  float col[32][3];
+  uint32_t mask[32];
+  uint32_t n;
+  uint32_t pad_[3];
+};
+
+struct HotSmem {
+  HotSlot ring[kHotRing];
+  SplatF64 stage[kHotProducers][32];
+  uint32_t full_seq[kHotRing];   // chunk j in slot j % R is ready: == j + 1
+  uint32_t empty_seq[kHotRing];  // chunk j consumed: == j + 1
+  uint32_t done;
+};
+constexpr size_t kHotSmem = sizeof(HotSmem);
+
+// The hot tiles of the frame (list length >= kHotLen, at most kMaxHot, in
+// tile order) and a per-tile flag the regular blend skips them by.
+__global__ void __launch_bounds__(1024) hot_list_k(const uint32_t* __restrict__ ranges,
+                                                   uint32_t n_tiles, uint32_t hot_len,
+                                                   const RenderCounters* __restrict__ ctr,
+                                                   uint32_t* __restrict__ hot,
+                                                   uint32_t* __restrict__ tile_hot) {
+  pdl_wait();
+  __shared__ uint32_t wsum[32];
+  __shared__ uint32_t run;
+  const bool ok = ctr->overflow == 0u;
+  if (threadIdx.x == 0) run = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (uint32_t t0 = 0; t0 < n_tiles; t0 += 1024) {
+    const uint32_t t = t0 + threadIdx.x;
+    bool f = false;
+    if (t < n_tiles && ok) f = ranges[2 * t + 1] - ranges[2 * t] >= hot_len;
+    const uint32_t bal = __ballot_sync(0xffffffffu, f);
+    if (lane == 0) wsum[warp] = __popc(bal);
+    __syncthreads();
+    uint32_t pre = 0, tot = 0;
+    for (int q = 0; q < 32; ++q) {
+      pre += q < warp ? wsum[q] : 0u;
+      tot += wsum[q];
+    }
+    const uint32_t rank = run + pre + __popc(bal & lanemask_lt());
+    const bool take = f && rank < (uint32_t)kMaxHot;
+    if (take) hot[1 + rank] = t;
+    if (t < n_tiles) tile_hot[t] = take ? 1u : 0u;
+    __syncthreads();
+    if (threadIdx.x == 0) run += tot;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) hot[0] = run < (uint32_t)kMaxHot ? run : (uint32_t)kMaxHot;
+}
+
+template <int TS>
+__global__ void __launch_bounds__(kBlendThreads, 2) blend_hot_k(
+    const uint32_t* __restrict__ ranges, const uint32_t* __restrict__ tv,
+    const BlendRec* __restrict__ rec, const uint32_t* __restrict__ hot, int w, int h,
+    int tiles_x, float* image_arg, const FrameDev* __restrict__ fd, int accumulate) {
+  pdl_wait();
+  constexpr int SUB = TS / 16;
+  constexpr int kItemsPerTile = SUB * SUB * 8;  // 8x4 blocks per tile
+  extern __shared__ __align__(16) unsigned char hot_raw[];
+  HotSmem& sm = *reinterpret_cast<HotSmem*>(hot_raw);
+  __shared__ double2 tab[64];
+  volatile uint32_t* full_seq = sm.full_seq;
+  volatile uint32_t* empty_seq = sm.empty_seq;
+  volatile uint32_t* done = &sm.done;
+  if (threadIdx.x < 64) tab[threadIdx.x] = kExp2Tab[threadIdx.x];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  float* __restrict__ image = image_arg ? image_arg : fd->image;
+  const uint32_t items = hot[0] * (uint32_t)kItemsPerTile;
+  for (uint32_t item = blockIdx.x; item < items; item += gridDim.x) {
+    const int tile = (int)hot[1 + item / kItemsPerTile];
+    const int rem = (int)(item % kItemsPerTile), sub = rem / 8, blk = rem % 8;
+    const int sx0 = (tile % tiles_x) * TS + (sub % SUB) * 16;
+    const int sy0 = (tile / tiles_x) * TS + (sub / SUB) * 16;
+    const int wx0 = sx0 + (blk & 1) * 8, wy0 = sy0 + (blk >> 1) * 4;
+    const int px = wx0 + (lane & 7), py = wy0 + (lane >> 3);
+    const uint32_t start = ranges[2 * tile], end = ranges[2 * tile + 1];
+    const uint32_t nchunks = (end - start + 31) / 32;
+    if (threadIdx.x < kHotRing) {
+      full_seq[threadIdx.x] = 0;
+      empty_seq[threadIdx.x] = 0;
+    }
+    if (threadIdx.x == 0) *done = 0;
+    __syncthreads();
+    if (warp == 0) {
+      // consumer: lane = pixel of the 8x4 block
+      const bool inside = px < w && py < h;
+      float cr = 0.f, cg = 0.f, cb = 0.f, T = inside ? 1.f : 0.f;
+      if (accumulate && inside) {
+        const float* p = image + ((size_t)py * w + px) * 3;
+        cr = p[0];
+        cg = p[1];
+        cb = p[2];
+      }
+      for (uint32_t j = 0; j < nchunks; ++j) {
+        if (__all_sync(0xffffffffu, T < kStopF)) {
+          if (lane == 0) *done = 1;
+          break;
+        }
+        const int slot = (int)(j % kHotRing);
+        while (full_seq[slot] != j + 1) __nanosleep(32);
+        __threadfence_block();
+        const HotSlot& S = sm.ring[slot];
+        const uint32_t n = S.n;
+        for (uint32_t k = 0; k < n; ++k) {
+          if (!((S.mask[k] >> lane) & 1u) || T < kStopF) continue;
+          // _core.pyx:56-78: FP64 arithmetic, f32 storage of T and colour
+          const double wgt = S.w[k][lane];
+          const double t = (double)T;
+          const double wt = __dmul_rn(wgt, t);
+          cr = __double2float_rn(__dadd_rn((double)cr, __dmul_rn(wt, (double)S.col[k][0])));
+          cg = __double2float_rn(__dadd_rn((double)cg, __dmul_rn(wt, (double)S.col[k][1])));
+          cb = __double2float_rn(__dadd_rn((double)cb, __dmul_rn(wt, (double)S.col[k][2])));
+          T = __double2float_rn(__dmul_rn(t, __dsub_rn(1.0, wgt)));
+        }
+        __syncwarp();
+        __threadfence_block();
+        if (lane == 0) empty_seq[slot] = j + 1;
+      }
+      if (lane == 0) *done = 1;
+      if (inside) {
+        float* p = image + ((size_t)py * w + px) * 3;
+        p[0] = cr;
+        p[1] = cg;
+        p[2] = cb;
+      }
+    } else {
+      // producer p: chunks p, p + 7, ...
+      const int pw = warp - 1;
+      const double fx = (double)px + 0.5, fy = (double)py + 0.5;
+      SplatF64* __restrict__ st = sm.stage[pw];
+      for (uint32_t j = (uint32_t)pw; j < nchunks; j += kHotProducers) {
+        if (*done) break;
+        const int slot = (int)(j % kHotRing);
+        if (j >= (uint32_t)kHotRing) {
+          bool quit = false;
+          while (empty_seq[slot] < j + 1 - kHotRing) {
+            if (*done) {
+              quit = true;
+              break;
+            }
+            __nanosleep(32);
+          }
+          if (quit) break;
+          __threadfence_block();
+        }
+        // this chunk's entries touching the block, in list order
+        const uint32_t i = start + 32 * j + lane;
+        bool hit = false;
+        BlendRec r;
+        if (i < end) {
+          r = rec[tv[i]];
+          const int x0 = r.bx & 0xFFFF, x1 = r.bx >> 16, y0 = r.by & 0xFFFF, y1 = r.by >> 16;
+          hit = x0 < wx0 + 8 && x1 > wx0 && y0 < wy0 + 4 && y1 > wy0;
+        }
+        const uint32_t bal = __ballot_sync(0xffffffffu, hit);
+        if (hit) {
+          SplatF64 d;
+          d.cx = r.cx;
+          d.cy = r.cy;
+          d.ca = -0.5 * (double)r.ca;
+          d.cb2 = -(double)r.cb;
+          d.cc = -0.5 * (double)r.cc;
+          d.al = r.alpha;
+          d.skip = r.skip;
+          d.r = r.r;
+          d.g = r.g;
+          d.b = r.b;
+          d.x0 = r.bx & 0xFFFF;
+          d.xw = (int)(r.bx >> 16) - d.x0;
+          d.y0 = r.by & 0xFFFF;
+          d.yh = (int)(r.by >> 16) - d.y0;
+          st[__popc(bal & lanemask_lt())] = d;
+        }
+        __syncwarp();
+        HotSlot& S = sm.ring[slot];
+        const int nh = __popc(bal);
+        for (int k = 0; k < nh; ++k) {
+          const SplatF64& q = st[k];
+          const bool in = ((unsigned)(px - q.x0) < (unsigned)q.xw) &
+                          ((unsigned)(py - q.y0) < (unsigned)q.yh);
+          const double dx = __dsub_rn(fx, q.cx);
+          const double dy = __dsub_rn(fy, q.cy);
+          const double sg = __dadd_rn(__dadd_rn(__dmul_rn(__dmul_rn(q.ca, dx), dx),
+                                                __dmul_rn(__dmul_rn(q.cb2, dy), dx)),
+                                      __dmul_rn(__dmul_rn(q.cc, dy), dy));
+          const bool live = in & (sg >= q.skip);
+          const uint32_t lm = __ballot_sync(0xffffffffu, live);
+          double wk = 0.0;
+          if (lm) {
+            wk = __dmul_rn(q.al, exp_tab(live ? sg : 0.0, tab));
+            if (wk > kBlendC[8]) wk = kBlendC[8];
+          }
+          S.w[k][lane] = wk;
+          if (lane == 0) {
+            S.mask[k] = lm;
+            S.col[k][0] = (float)q.r;
+            S.col[k][1] = (float)q.g;
+            S.col[k][2] = (float)q.b;
+          }
+        }
+        if (lane == 0) S.n = (uint32_t)nh;
+        __syncwarp();
+        __threadfence_block();
+        if (lane == 0) full_seq[slot] = j + 1;
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+  }
+}
+
 __global__ void pack_ordered_k(const float* __restrict__ centers, const float* __restrict__ conics,
                                const float* __restrict__ colors, const float* __restrict__ alphas,
                                const int32_t* __restrict__ bounds, uint32_t n, int w, int h,
@@ -711,22 +1024,76 @@ const uint32_t* sorted_tiles(const RenderWs& w, uint32_t n_tiles) {
   return ((tile_bits(n_tiles) + 7) / 8) % 2 ? w.tv1 : w.tv0;
 }
 
+// Side stream + fork/join events of the hot-tile blend, per device (made
+// outside graph capture by blend_init; a launch without them blends every
+// tile with the regular kernel - the same image).
+struct HotStreams {
+  cudaStream_t side = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+HotStreams g_hot[16];
+
+bool hot_enabled() {
+  static const int on = [] {
+    const char* e = getenv("VMSPLAT_BLEND_HOT");
+    return e && *e ? atoi(e) : 1;
+  }();
+  return on != 0;
+}
+
+uint32_t hot_len() {
+  static const uint32_t n = [] {
+    const char* e = getenv("VMSPLAT_HOT_LEN");
+    return e && *e ? (uint32_t)atoi(e) : kHotLen;
+  }();
+  return n;
+}
+
 int32_t launch_band(int width, int height, const uint32_t* vals, const RenderWs& w, float* image,
                     int accumulate, int exact, int band, int bands, cudaStream_t s) {
   const int ts = tile_size();
   const int tiles_x = ceil_div(width, ts), tiles_y = ceil_div(height, ts);
   const uint32_t n_tiles = (uint32_t)tiles_x * tiles_y;
-  auto* kern = exact ? (ts == 16 ? blend_k<true, 16> : blend_k<true, 32>)
+  static const int sparse = [] {
+    const char* e = getenv("VMSPLAT_BLEND_SPARSE");
+    return e && *e ? atoi(e) : 0;
+  }();
+  auto* kern = exact ? (sparse ? (ts == 16 ? blend_k<true, 16, true> : blend_k<true, 32, true>)
+                               : (ts == 16 ? blend_k<true, 16> : blend_k<true, 32>))
                      : (ts == 16 ? blend_k<false, 16> : blend_k<false, 32>);
   const uint32_t subs = (uint32_t)(ts / 16) * (ts / 16);
   const int r0 = blend_band_row(band, bands, tiles_y), r1 = blend_band_row(band + 1, bands, tiles_y);
   const uint32_t first = (uint32_t)r0 * tiles_x, count = (uint32_t)(r1 - r0) * tiles_x;
+  const size_t dsmem = (exact && sparse) ? kSparseSmem : 0;
+  // hot tiles (single-band frames, exact blend): their own kernel on a
+  // forked stream, concurrent with the regular blend of the other tiles
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const HotStreams& hs = g_hot[dev & 15];
+  const bool hot = exact && !sparse && bands == 1 && hot_enabled() && hs.side;
+  if (hot) {
+    VMS_CUDA(launch(hot_list_k, 1, 1024, 0, s, (const uint32_t*)w.ranges, n_tiles, hot_len(),
+                    (const RenderCounters*)w.ctr, w.hot, w.tile_hot));
+    mark("hot_list", s);
+    VMS_CUDA(cudaEventRecord(hs.fork, s));
+    VMS_CUDA(cudaStreamWaitEvent(hs.side, hs.fork, 0));
+    auto* hk = ts == 16 ? blend_hot_k<16> : blend_hot_k<32>;
+    // one CTA per 8x4 block of every possible hot tile (the blocks past the
+    // frame's hot count exit at once): the blocks run concurrently
+    hk<<<kMaxHot * (ts / 16) * (ts / 16) * 8, kBlendThreads, kHotSmem, hs.side>>>(
+        (const uint32_t*)w.ranges, sorted_tiles(w, n_tiles), (const BlendRec*)w.rec,
+        (const uint32_t*)w.hot, width, height, tiles_x, image, (const FrameDev*)w.fd,
+        accumulate);
+    VMS_CUDA(cudaEventRecord(hs.join, hs.side));
+  }
   if (count)
-    VMS_CUDA(launch(kern, count * subs, kBlendThreads, 0, s, (const uint32_t*)w.ranges,
+    VMS_CUDA(launch(kern, count * subs, kBlendThreads, dsmem, s, (const uint32_t*)w.ranges,
                     (const uint32_t*)w.order, sorted_tiles(w, n_tiles), vals,
                     (const RenderCounters*)w.ctr, (const BlendRec*)w.rec, width, height, tiles_x,
-                    first, image, (const FrameDev*)w.fd, accumulate));
+                    first, image, (const FrameDev*)w.fd, accumulate,
+                    (const uint32_t*)(hot ? w.tile_hot : nullptr)));
   mark("blend", s);
+  if (hot) VMS_CUDA(cudaStreamWaitEvent(s, hs.join, 0));
   VMS_LAUNCH_CHECK("blend");
   return VMS_OK;
 }
@@ -792,6 +1159,21 @@ int32_t tiles_and_blend(int width, int height, const uint32_t* vals, const Rende
 // any graph capture (session create, ABI entries).
 int32_t blend_init() {
   static bool done = false;
+  {
+    // per device: the hot-tile blend's side stream and fork/join events
+    int dev = 0;
+    VMS_CUDA(cudaGetDevice(&dev));
+    HotStreams& hs = g_hot[dev & 15];
+    if (!hs.side) {
+      cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+      cudaStreamIsCapturing(cudaStreamLegacy, &cs);
+      if (cs == cudaStreamCaptureStatusNone) {
+        VMS_CUDA(cudaStreamCreateWithFlags(&hs.side, cudaStreamNonBlocking));
+        VMS_CUDA(cudaEventCreateWithFlags(&hs.fork, cudaEventDisableTiming));
+        VMS_CUDA(cudaEventCreateWithFlags(&hs.join, cudaEventDisableTiming));
+      }
+    }
+  }
   if (done) return VMS_OK;
   {
     const int32_t rc = preprocess_init();
@@ -804,6 +1186,12 @@ int32_t blend_init() {
     t[j].y = (double)(v - (long double)t[j].x);
   }
   VMS_CUDA(cudaMemcpyToSymbol(kExp2Tab, t, sizeof(t)));
+  for (const void* f : {(const void*)blend_k<true, 16, true>, (const void*)blend_k<true, 32, true>})
+    VMS_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)kSparseSmem));
+  for (const void* f : {(const void*)blend_hot_k<16>, (const void*)blend_hot_k<32>})
+    VMS_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)kHotSmem));
   VMS_CUDA(cudaFuncSetAttribute((const void*)tile_prep_k,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)(sizeof(uint32_t) * kDiffSmemWords)));
@@ -833,9 +1221,10 @@ size_t render_ws_bytes(uint32_t n_cap, uint32_t m_cap, uint32_t n_tiles) {
   b += sizeof(uint32_t) * (size_t)n_cap;      // rects
   b += sizeof(uint32_t) * (4 * (size_t)n_tiles + 2);  // tcount + tdiff
   b += sizeof(uint32_t) * 3 * (size_t)n_tiles; // ranges + order
+  b += sizeof(uint32_t) * (kMaxHot + 1 + (size_t)n_tiles);  // hot list + flags
   b += sizeof(RenderCounters) + sizeof(FrameDev);
   b += 2 * scan_ws_bytes(n_cap) + radix_ws_bytes(n_cap > m_cap ? n_cap : m_cap);
-  return b + 256 * 24;
+  return b + 256 * 26;
 }
 
 RenderWs render_carve(void* ws, uint32_t n_cap, uint32_t m_cap, uint32_t n_tiles) {
@@ -862,6 +1251,8 @@ RenderWs render_carve(void* ws, uint32_t n_cap, uint32_t m_cap, uint32_t n_tiles
   w.tdiff = carve<uint32_t>(p, 2 * (size_t)n_tiles + 2);  // >= (tx + 1)(ty + 1)
   w.ranges = carve<uint32_t>(p, 2 * (size_t)n_tiles);
   w.order = carve<uint32_t>(p, (size_t)n_tiles);
+  w.hot = carve<uint32_t>(p, kMaxHot + 1);
+  w.tile_hot = carve<uint32_t>(p, (size_t)n_tiles);
   w.ctr = carve<RenderCounters>(p, 1);
   w.fd = carve<FrameDev>(p, 1);
   w.scan_ws = carve<char>(p, scan_ws_bytes(n_cap));

@@ -73,6 +73,8 @@ struct RenderWs {
   uint32_t* tdiff;   // 2D difference array of tcount ((tiles_x + 1) x (tiles_y + 1))
   uint32_t* ranges;  // 2 per tile
   uint32_t* order;   // blend schedule: tiles, longest list first
+  uint32_t* hot;     // [0] hot tiles this frame, [1..] their ids (blend_hot_k)
+  uint32_t* tile_hot;  // per tile: 1 if blend_hot_k owns it
   RenderCounters* ctr;
   FrameDev* fd;
   void* scan_ws;

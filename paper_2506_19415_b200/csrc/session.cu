@@ -36,6 +36,8 @@
 #include <cstring>
 #include <vector>
 
+#include <unistd.h>
+
 #include "common.cuh"
 #include "render.h"
 #include "vis.h"
@@ -61,9 +63,14 @@ class CopyPool {
     cv_.notify_all();
     for (auto& t : workers_) t.join();
   }
-  // Copy every piece (dst, src, bytes) and return when all are done.
-  void copy(const std::vector<std::tuple<char*, const char*, size_t>>& pieces) {
-    if (pieces.empty()) return;
+  // fd >= 0: the pieces' sources are byte offsets into this file, read
+  // with pread (no page faults on a mapping the process has not touched)
+  void set_source_fd(int fd) { fd_ = fd; }
+  // Copy every piece (dst, src, bytes) and return when all are done; false
+  // if a read failed.
+  bool copy(const std::vector<std::tuple<char*, const char*, size_t>>& pieces) {
+    if (pieces.empty()) return true;
+    failed_ = false;
     {
       std::lock_guard<std::mutex> g(m_);
       job_ = &pieces;
@@ -75,6 +82,7 @@ class CopyPool {
     std::unique_lock<std::mutex> lk(m_);
     done_cv_.wait(lk, [this] { return pending_ == 0; });
     job_ = nullptr;
+    return !failed_;
   }
 
  private:
@@ -93,7 +101,23 @@ class CopyPool {
         const size_t i = next_.fetch_add(1);
         if (i >= job->size()) break;
         const auto& pc = (*job)[i];
-        std::memcpy(std::get<0>(pc), std::get<1>(pc), std::get<2>(pc));
+        if (fd_ >= 0) {
+          char* dst = std::get<0>(pc);
+          size_t left = std::get<2>(pc);
+          off_t off = (off_t)reinterpret_cast<uintptr_t>(std::get<1>(pc));
+          while (left) {
+            const ssize_t got = pread(fd_, dst, left, off);
+            if (got <= 0) {
+              failed_ = true;
+              break;
+            }
+            dst += got;
+            off += got;
+            left -= (size_t)got;
+          }
+        } else {
+          std::memcpy(std::get<0>(pc), std::get<1>(pc), std::get<2>(pc));
+        }
       }
       std::lock_guard<std::mutex> g(m_);
       if (--pending_ == 0) done_cv_.notify_one();
@@ -107,6 +131,8 @@ class CopyPool {
   int pending_ = 0;
   uint64_t gen_ = 0;
   bool stop_ = false;
+  int fd_ = -1;
+  std::atomic<bool> failed_{false};
 };
 }
 
@@ -470,6 +496,7 @@ vms_session* vms_session_create(const vms_session_desc* desc) {
   if (desc->upload_mode == 2) {
     const unsigned hw = std::thread::hardware_concurrency();
     s->pool = new CopyPool((int)std::max(1u, std::min(8u, hw ? hw / 2 : 4u)));
+    s->pool->set_source_fd(desc->host_fd);
   }
   s->plan_pid.resize(P + 1);
   s->plan_level.resize(P + 1);
@@ -610,7 +637,10 @@ int32_t vms_session_frame(vms_session* s, const vms_frame_args* a, vms_frame_sta
         s->bounce_bytes[par] = want;
       }
       s->pieces.clear();
-      const char* src = reinterpret_cast<const char*>(s->d.host_records);
+      // from the file (pread at the record section's offset) or the mapping
+      const char* src = s->d.host_fd >= 0
+                            ? reinterpret_cast<const char*>((uintptr_t)s->d.host_fd_offset)
+                            : reinterpret_cast<const char*>(s->d.host_records);
       constexpr size_t kPiece = 1u << 20;
       for (int64_t i = 0; i < n_plan; ++i) {
         const vms_copy& c = s->copies[par][i];
@@ -618,7 +648,14 @@ int32_t vms_session_frame(vms_session* s, const vms_frame_args* a, vms_frame_sta
           s->pieces.emplace_back(s->bounce[par] + c.dst_offset + o, src + c.src_offset + o,
                                  std::min<size_t>(kPiece, c.nbytes - o));
       }
-      s->pool->copy(s->pieces);
+      const auto g0 = std::chrono::steady_clock::now();
+      const bool read_ok = s->pool->copy(s->pieces);
+      out->ms_host_gather = (float)(std::chrono::duration<double, std::milli>(
+                                std::chrono::steady_clock::now() - g0).count());
+      if (!read_ok) {
+        set_error("session_frame: reading page rows from the scene file failed");
+        return VMS_ERR_CUDA;
+      }
       VMS_CUDA(cudaMemcpyAsync(s->staging, s->bounce[par], bytes, cudaMemcpyHostToDevice,
                                s->copy_stream));
     } else {

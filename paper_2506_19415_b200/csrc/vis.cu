@@ -325,41 +325,28 @@ struct VisBins {
   uint32_t pair_cap;
 };
 
-__global__ void __launch_bounds__(kVisThreads) vis_raster_k(
-    const VisTri* __restrict__ tris, const uint32_t* __restrict__ n_tris_dev, uint32_t n_host,
-    int w, int h, uint32_t* __restrict__ id_image, double* __restrict__ invz_image,
-    int init_from_images, uint32_t page_count, uint32_t* __restrict__ page_depth,
-    uint8_t* __restrict__ page_direct, uint32_t* __restrict__ err, VisBins bins) {
-  pdl_wait();
-  constexpr int kBoxes = 4;  // triangle boxes tested per thread per round
-  __shared__ VisTri stri[kVisThreads];
-  __shared__ uint32_t sidx[kBoxes * kVisThreads];
-  __shared__ uint32_t wsum[kVisThreads / 32];
+struct RasterSmem {
+  VisTri stri[kVisThreads];
+  uint32_t sidx[4 * kVisThreads];
+  uint32_t wsum[kVisThreads / 32];
+};
 
-  const int tx0 = blockIdx.x * kVisTile, ty0 = blockIdx.y * kVisTile;
+// The triangles [first, n) of `list` (or of the triangle array itself when
+// list == nullptr) against the CTA's 16x16 tile at (tx0, ty0): each pixel
+// keeps the nearest 1/z, the first triangle in order winning ties (strict >,
+// _core.pyx:150-159).  CTA-uniform arguments; every thread calls it.
+__device__ __forceinline__ void raster_range(const VisTri* __restrict__ tris,
+                                             const uint32_t* __restrict__ list, uint32_t first,
+                                             uint32_t n, int tx0, int ty0, int w, int h,
+                                             RasterSmem& sm, uint32_t& best_id,
+                                             double& best_z) {
+  constexpr int kBoxes = 4;  // triangle boxes tested per thread per round
   const int tx1 = min(tx0 + kVisTile, w) - 1, ty1 = min(ty0 + kVisTile, h) - 1;
   const int px = tx0 + (threadIdx.x & (kVisTile - 1));
   const int py = ty0 + (threadIdx.x / kVisTile);
   const bool inside_img = px < w && py < h;
   const double fx = (double)px + 0.5, fy = (double)py + 0.5;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-
-  uint32_t best_id = 0;
-  double best_z = 0.0;
-  if (init_from_images && inside_img) {
-    best_id = id_image[(int64_t)py * w + px];
-    best_z = invz_image[(int64_t)py * w + px];
-  }
-  // the triangles to test: all of them, or this tile's binned list (in
-  // triangle order) when the frame's pair list fit its buffer
-  uint32_t first = 0, n = n_tris_dev ? *n_tris_dev : n_host;
-  const uint32_t* list = nullptr;
-  if (bins.vals && *bins.n_pairs <= bins.pair_cap) {
-    const uint2 r = bins.ranges[blockIdx.y * gridDim.x + blockIdx.x];
-    list = bins.vals;
-    first = r.x;
-    n = r.y;
-  }
   for (uint32_t base = first; base < n; base += kBoxes * kVisThreads) {
     // test kBoxes 16-byte boxes per thread (loads in flight together) and
     // compact the indices of the triangles touching this tile, in order
@@ -381,16 +368,16 @@ __global__ void __launch_bounds__(kVisThreads) vis_raster_k(
 #pragma unroll
     for (int k = 0; k < kBoxes; ++k) {
       const uint32_t bal = __ballot_sync(0xffffffffu, hit[k]);
-      if (lane == 0) wsum[warp] = __popc(bal);
+      if (lane == 0) sm.wsum[warp] = __popc(bal);
       __syncthreads();
       uint32_t pre = 0, tot = 0;
 #pragma unroll
       for (int q = 0; q < kVisThreads / 32; ++q) {
-        const uint32_t c = wsum[q];
+        const uint32_t c = sm.wsum[q];
         pre += q < warp ? c : 0u;
         tot += c;
       }
-      if (hit[k]) sidx[cnt + pre + __popc(bal & lanemask_lt())] = tid[k];
+      if (hit[k]) sm.sidx[cnt + pre + __popc(bal & lanemask_lt())] = tid[k];
       cnt += tot;
       __syncthreads();
     }
@@ -398,11 +385,11 @@ __global__ void __launch_bounds__(kVisThreads) vis_raster_k(
     // walks them in index order (strict > keeps the first triangle on ties)
     for (uint32_t h0 = 0; h0 < cnt; h0 += kVisThreads) {
       const uint32_t m = min(cnt - h0, (uint32_t)kVisThreads);
-      if (threadIdx.x < m) stri[threadIdx.x] = tris[sidx[h0 + threadIdx.x]];
+      if (threadIdx.x < m) sm.stri[threadIdx.x] = tris[sm.sidx[h0 + threadIdx.x]];
       __syncthreads();
       if (inside_img) {
         for (uint32_t j = 0; j < m; ++j) {
-          const VisTri& q = stri[j];
+          const VisTri& q = sm.stri[j];
           if (px < q.x0 || px > q.x1 || py < q.y0 || py > q.y1) continue;
           const double e0 = dsub(dmul(dsub(q.cx, q.bx), dsub(fy, q.by)),
                                  dmul(dsub(q.cy, q.by), dsub(fx, q.bx)));
@@ -424,12 +411,28 @@ __global__ void __launch_bounds__(kVisThreads) vis_raster_k(
       __syncthreads();
     }
   }
+}
+
+// Per-pixel outputs of the raster: the images (when asked) and K3, the fused
+// depth encode + per-page max + direct flag (runtime.py:26-43,70-89,
+// render.py:305-307), warp-aggregated with match_any.
+__device__ __forceinline__ void raster_epilogue(int tx0, int ty0, int w, int h,
+                                                uint32_t best_id, double best_z,
+                                                uint32_t* __restrict__ id_image,
+                                                double* __restrict__ invz_image,
+                                                uint32_t page_count,
+                                                uint32_t* __restrict__ page_depth,
+                                                uint8_t* __restrict__ page_direct,
+                                                uint32_t* __restrict__ err) {
+  const int px = tx0 + (threadIdx.x & (kVisTile - 1));
+  const int py = ty0 + (threadIdx.x / kVisTile);
+  const bool inside_img = px < w && py < h;
+  const int lane = threadIdx.x & 31;
   if (inside_img) {
     if (id_image) id_image[(int64_t)py * w + px] = best_id;
     if (invz_image) invz_image[(int64_t)py * w + px] = best_z;
   }
   if (!page_depth) return;
-  // K3: depth = 1/invz -> float32 -> encoded (runtime.py:26-43, render.py:305-307)
   uint32_t pid = inside_img ? best_id : 0u;
   if (pid > page_count) {
     atomicMax(err, pid);
@@ -447,6 +450,145 @@ __global__ void __launch_bounds__(kVisThreads) vis_raster_k(
       atomicMax(&page_depth[pid], mx);
       page_direct[pid] = 1;
     }
+  }
+}
+
+// Whole-list raster: one CTA per 16x16 tile walks every triangle (small
+// meshes) and writes the outputs.
+__global__ void __launch_bounds__(kVisThreads) vis_raster_k(
+    const VisTri* __restrict__ tris, const uint32_t* __restrict__ n_tris_dev, uint32_t n_host,
+    int w, int h, uint32_t* __restrict__ id_image, double* __restrict__ invz_image,
+    int init_from_images, uint32_t page_count, uint32_t* __restrict__ page_depth,
+    uint8_t* __restrict__ page_direct, uint32_t* __restrict__ err) {
+  pdl_wait();
+  __shared__ RasterSmem sm;
+  const int tx0 = blockIdx.x * kVisTile, ty0 = blockIdx.y * kVisTile;
+  const int px = tx0 + (threadIdx.x & (kVisTile - 1));
+  const int py = ty0 + (threadIdx.x / kVisTile);
+  uint32_t best_id = 0;
+  double best_z = 0.0;
+  if (init_from_images && px < w && py < h) {
+    best_id = id_image[(int64_t)py * w + px];
+    best_z = invz_image[(int64_t)py * w + px];
+  }
+  const uint32_t n = n_tris_dev ? *n_tris_dev : n_host;
+  raster_range(tris, nullptr, 0, n, tx0, ty0, w, h, sm, best_id, best_z);
+  raster_epilogue(tx0, ty0, w, h, best_id, best_z, id_image, invz_image, page_count, page_depth,
+                  page_direct, err);
+}
+
+// Binned raster, work items = (tile, chunk of <= kVisChunk of the tile's
+// list entries).  The nearest-with-first-wins rule is a reduction: (z, i)
+// beats (z', i') iff z > z' or (z == z' and i < i'), so a long list (the
+// vanishing point of a street: 10^5 triangles in one tile) is split over many
+// CTAs; a tile of one chunk writes its outputs directly, the chunks of a
+// longer list write per-pixel partials that vis_merge_k folds in chunk order.
+constexpr uint32_t kVisChunk = 2048;
+
+struct VisPartial {
+  double z;
+  uint32_t id;
+  uint32_t pad_;
+};
+
+__global__ void vis_chunk_count_k(const uint2* __restrict__ ranges, uint32_t tiles,
+                                  const uint32_t* __restrict__ n_pairs, uint32_t pair_cap,
+                                  uint32_t* __restrict__ nchunk, uint32_t* __restrict__ slot,
+                                  uint32_t* __restrict__ slot_ctr, uint32_t slot_cap) {
+  pdl_wait();
+  const bool ok = *n_pairs <= pair_cap;
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < tiles;
+       t += gridDim.x * blockDim.x) {
+    uint32_t c = 1;
+    if (ok) {
+      const uint2 r = ranges[t];
+      const uint32_t len = r.y - r.x;
+      if (len > kVisChunk) {
+        c = (len + kVisChunk - 1) / kVisChunk;
+        const uint32_t b = atomicAdd(slot_ctr, c);
+        if (b + c > slot_cap) {
+          c = 1;  // out of partial slots: this tile walks its list in one CTA
+        } else {
+          slot[t] = b;
+        }
+      }
+    }
+    nchunk[t] = c;
+  }
+}
+
+__global__ void __launch_bounds__(kVisThreads) vis_raster_items_k(
+    const VisTri* __restrict__ tris, const uint32_t* __restrict__ n_tris_dev, int w, int h,
+    int tiles_x, uint32_t tiles, VisBins bins, const uint32_t* __restrict__ nchunk,
+    const uint32_t* __restrict__ chunk_off, const uint32_t* __restrict__ n_items,
+    const uint32_t* __restrict__ slot, VisPartial* __restrict__ partial,
+    uint32_t* __restrict__ id_image, double* __restrict__ invz_image, uint32_t page_count,
+    uint32_t* __restrict__ page_depth, uint8_t* __restrict__ page_direct,
+    uint32_t* __restrict__ err) {
+  pdl_wait();
+  __shared__ RasterSmem sm;
+  const bool binned = *bins.n_pairs <= bins.pair_cap;
+  const uint32_t items = binned ? *n_items : tiles;
+  for (uint32_t it = blockIdx.x; it < items; it += gridDim.x) {
+    uint32_t t = it, c = 0;
+    if (binned) {
+      // the tile whose chunk range holds item `it` (chunk_off is ascending)
+      uint32_t lo = 0, hi = tiles;
+      while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (chunk_off[mid] <= it) lo = mid; else hi = mid;
+      }
+      t = lo;
+      c = it - chunk_off[t];
+    }
+    const int tx0 = (int)(t % tiles_x) * kVisTile, ty0 = (int)(t / tiles_x) * kVisTile;
+    uint32_t best_id = 0;
+    double best_z = 0.0;
+    if (binned) {
+      const uint2 r = bins.ranges[t];
+      const uint32_t a = r.x + c * kVisChunk;
+      const uint32_t b = nchunk[t] > 1 ? min(r.y, a + kVisChunk) : r.y;
+      raster_range(tris, bins.vals, a, b, tx0, ty0, w, h, sm, best_id, best_z);
+    } else {  // the pair list overflowed: walk every triangle
+      raster_range(tris, nullptr, 0, *n_tris_dev, tx0, ty0, w, h, sm, best_id, best_z);
+    }
+    if (!binned || nchunk[t] == 1) {
+      raster_epilogue(tx0, ty0, w, h, best_id, best_z, id_image, invz_image, page_count,
+                      page_depth, page_direct, err);
+    } else {
+      VisPartial pt;
+      pt.z = best_z;
+      pt.id = best_id;
+      pt.pad_ = 0;
+      partial[(size_t)(slot[t] + c) * kVisThreads + threadIdx.x] = pt;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kVisThreads) vis_merge_k(
+    int w, int h, int tiles_x, uint32_t tiles, const uint32_t* __restrict__ n_pairs,
+    uint32_t pair_cap, const uint32_t* __restrict__ nchunk, const uint32_t* __restrict__ slot,
+    const VisPartial* __restrict__ partial, uint32_t* __restrict__ id_image,
+    double* __restrict__ invz_image, uint32_t page_count, uint32_t* __restrict__ page_depth,
+    uint8_t* __restrict__ page_direct, uint32_t* __restrict__ err) {
+  pdl_wait();
+  if (*n_pairs > pair_cap) return;
+  for (uint32_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+    const uint32_t c = nchunk[t];
+    if (c <= 1) continue;
+    uint32_t best_id = 0;
+    double best_z = 0.0;
+    const VisPartial* p = partial + (size_t)slot[t] * kVisThreads + threadIdx.x;
+    for (uint32_t k = 0; k < c; ++k) {  // chunk order: earlier chunks win ties
+      const VisPartial q = p[(size_t)k * kVisThreads];
+      if (q.z > best_z) {
+        best_z = q.z;
+        best_id = q.id;
+      }
+    }
+    const int tx0 = (int)(t % tiles_x) * kVisTile, ty0 = (int)(t / tiles_x) * kVisTile;
+    raster_epilogue(tx0, ty0, w, h, best_id, best_z, id_image, invz_image, page_count,
+                    page_depth, page_direct, err);
   }
 }
 
@@ -532,6 +674,10 @@ uint32_t vis_pair_cap(uint32_t n_faces) {
   return (uint32_t)(c < (1u << 20) ? (1u << 20) : (c > (1ull << 30) ? (1ull << 30) : c));
 }
 
+// Partial-result slots of the chunked raster: a tile of more than one chunk
+// uses one slot per chunk, so sum(slots) <= 2 * pairs / kVisChunk.
+uint32_t vis_slot_cap(uint32_t n_faces) { return 2 * (vis_pair_cap(n_faces) / kVisChunk) + 64; }
+
 size_t vis_bin_bytes(uint32_t n_faces) {
   if (!vis_binned(n_faces)) return 0;
   const uint32_t nt = 2 * n_faces + 1, cap = vis_pair_cap(n_faces);
@@ -540,7 +686,11 @@ size_t vis_bin_bytes(uint32_t n_faces) {
   b += sizeof(uint32_t) * (size_t)cap * 4;         // keys/vals ping-pong
   b += sizeof(uint2) * kVisMaxTiles;               // tile ranges
   b += radix_ws_bytes(cap) + scan_ws_bytes(nt);
-  return b + 8 * 256;
+  // chunked raster: per-tile chunk counts, offsets, partial slots; partials
+  b += sizeof(uint32_t) * (size_t)kVisMaxTiles * 3 + sizeof(uint32_t) * 4;
+  b += scan_ws_bytes(kVisMaxTiles);
+  b += sizeof(VisPartial) * kVisThreads * (size_t)vis_slot_cap(n_faces);
+  return b + 16 * 256;
 }
 
 size_t vis_ws_bytes(uint32_t n_faces, uint32_t page_count) {
@@ -567,6 +717,10 @@ struct VisWs {
   uint2* ranges;
   void *radix, *scan2;
   uint32_t pair_cap;
+  uint32_t *nchunk, *chunk_off, *slot, *ictr;  // ictr: [0] items, [1] slot counter
+  void* scan3;
+  VisPartial* partial;
+  uint32_t slot_cap;
 };
 
 template <typename T>
@@ -594,8 +748,10 @@ VisWs carve_ws(void* ws, uint32_t nf, uint32_t P) {
   w.fd = carve<VisFrameDev>(p, 1);
   w.bcnt = w.boff = w.n_pairs = w.k0 = w.v0 = w.k1 = w.v1 = nullptr;
   w.ranges = nullptr;
-  w.radix = w.scan2 = nullptr;
-  w.pair_cap = 0;
+  w.radix = w.scan2 = w.scan3 = nullptr;
+  w.pair_cap = w.slot_cap = 0;
+  w.nchunk = w.chunk_off = w.slot = w.ictr = nullptr;
+  w.partial = nullptr;
   if (vis_binned(nf)) {
     const uint32_t nt = 2 * nf + 1;
     w.pair_cap = vis_pair_cap(nf);
@@ -609,6 +765,13 @@ VisWs carve_ws(void* ws, uint32_t nf, uint32_t P) {
     w.ranges = carve<uint2>(p, kVisMaxTiles);
     w.radix = carve<char>(p, radix_ws_bytes(w.pair_cap));
     w.scan2 = carve<char>(p, scan_ws_bytes(nt));
+    w.nchunk = carve<uint32_t>(p, kVisMaxTiles);
+    w.chunk_off = carve<uint32_t>(p, kVisMaxTiles);
+    w.slot = carve<uint32_t>(p, kVisMaxTiles);
+    w.ictr = carve<uint32_t>(p, 4);
+    w.scan3 = carve<char>(p, scan_ws_bytes(kVisMaxTiles));
+    w.slot_cap = vis_slot_cap(nf);
+    w.partial = carve<VisPartial>(p, (size_t)kVisThreads * w.slot_cap);
   }
   return w;
 }
@@ -660,6 +823,8 @@ int32_t vis_launch(const VisArgs& a, cudaStream_t s) {
     VMS_CUDA(cudaMemsetAsync(w.scan2, 0, scan_ws_bytes(2 * a.n_faces + 1), s));
     VMS_CUDA(cudaMemsetAsync(w.radix, 0, radix_clear_bytes(), s));
     VMS_CUDA(cudaMemsetAsync(w.ranges, 0, sizeof(uint2) * kVisMaxTiles, s));
+    VMS_CUDA(cudaMemsetAsync(w.ictr, 0, sizeof(uint32_t) * 4, s));
+    VMS_CUDA(cudaMemsetAsync(w.scan3, 0, scan_ws_bytes(kVisMaxTiles), s));
   }
   if (a.n_faces) {
     VMS_CUDA(launch(vis_count_k, ceil_div<uint32_t>(a.n_faces, T), T, 0, s,
@@ -709,11 +874,33 @@ int32_t vis_launch(const VisArgs& a, cudaStream_t s) {
                     w.pair_cap, w.ranges));
     mark("vis_bin_ranges", s);
     bins = VisBins{vs, w.ranges, w.n_pairs, w.pair_cap};
+    // work items: (tile, chunk of <= kVisChunk list entries), then the
+    // merge of the multi-chunk tiles
+    VMS_CUDA(launch(vis_chunk_count_k, ceil_div<uint32_t>(tiles, T), T, 0, s,
+                    (const uint2*)w.ranges, tiles, (const uint32_t*)w.n_pairs, w.pair_cap,
+                    w.nchunk, w.slot, w.ictr + 1, w.slot_cap));
+    mark("vis_chunk_count", s);
+    st = scan_exclusive_u32(w.nchunk, w.chunk_off, nullptr, tiles, kVisMaxTiles, w.ictr, w.scan3,
+                            s, false);
+    if (st) return st;
+    VMS_CUDA(launch(vis_raster_items_k, 8 * kSMs, kVisThreads, 0, s, (const VisTri*)w.tris,
+                    (const uint32_t*)w.n_tris, a.cam.width, a.cam.height, (int)grid.x, tiles,
+                    bins, (const uint32_t*)w.nchunk, (const uint32_t*)w.chunk_off,
+                    (const uint32_t*)w.ictr, (const uint32_t*)w.slot, w.partial, a.id_image,
+                    a.invz_image, a.page_count, w.base, w.direct, w.err));
+    mark("vis_raster", s);
+    VMS_CUDA(launch(vis_merge_k, 2 * kSMs, kVisThreads, 0, s, a.cam.width, a.cam.height,
+                    (int)grid.x, tiles, (const uint32_t*)w.n_pairs, w.pair_cap,
+                    (const uint32_t*)w.nchunk, (const uint32_t*)w.slot,
+                    (const VisPartial*)w.partial, a.id_image, a.invz_image, a.page_count,
+                    w.base, w.direct, w.err));
+    mark("vis_merge", s);
+  } else {
+    VMS_CUDA(launch(vis_raster_k, grid, kVisThreads, 0, s, (const VisTri*)w.tris,
+                    (const uint32_t*)w.n_tris, 0u, a.cam.width, a.cam.height, a.id_image,
+                    a.invz_image, 0, a.page_count, w.base, w.direct, w.err));
+    mark("vis_raster", s);
   }
-  VMS_CUDA(launch(vis_raster_k, grid, kVisThreads, 0, s, (const VisTri*)w.tris,
-                  (const uint32_t*)w.n_tris, 0u, a.cam.width, a.cam.height, a.id_image,
-                  a.invz_image, 0, a.page_count, w.base, w.direct, w.err, bins));
-  mark("vis_raster", s);
   if (back) {
     VMS_CUDA(launch(vis_back_k, 1, kFrontThreads, sizeof(uint32_t) * (a.page_count + 1), s,
                     (const uint32_t*)w.base, (const uint8_t*)w.direct, a.link_off, a.link_tgt,
@@ -782,8 +969,7 @@ int32_t raster_triangles(const double* raw, const uint32_t* ids, uint32_t n, uin
   if (n) vis_setup_raw_k<<<ceil_div<uint32_t>(n, T), T, 0, s>>>(raw, ids, n, w, h, tris);
   dim3 grid(ceil_div(w, kVisTile), ceil_div(h, kVisTile));
   vis_raster_k<<<grid, kVisThreads, 0, s>>>(tris, nullptr, n, w, h, id_image, invz_image, 1, 0,
-                                            nullptr, nullptr, nullptr,
-                                            VisBins{nullptr, nullptr, nullptr, 0u});
+                                            nullptr, nullptr, nullptr);
   VMS_LAUNCH_CHECK("raster_triangles");
   return VMS_OK;
 }

@@ -426,12 +426,19 @@ class VmSession:
                     warnings.warn(f"scene not page-lockable ({exc}); streaming pages from "
                                   "the mapping (upload_mode 2)", RuntimeWarning)
                     self.upload_mode = 2
+            self._fd = None
             if self.upload_mode == 2:
                 # streaming source: the scene's own (memory-mapped) rows; the
                 # session gathers each frame's pages through a page-locked
-                # bounce buffer, so the scene need not fit in pinned memory
+                # bounce buffer, so the scene need not fit in pinned memory.
+                # A file-backed scene is read with pread (host threads, no
+                # page faults on the untouched mapping)
                 self.host = np.ascontiguousarray(scene.gaussians, dtype=np.float32)
                 host_ptr = self.host.ctypes.data
+                if isinstance(scene.gaussians, np.memmap) and getattr(scene, "path", None):
+                    import os
+
+                    self._fd = os.open(scene.path, os.O_RDONLY)
             else:
                 # page-locked, mapped into the device; shared by every
                 # session of the process (and, for a memory-mapped file, by
@@ -457,6 +464,8 @@ class VmSession:
             d.vis_ws = self.vis.ws.data_ptr()
             d.exact = int(self.exact)
             d.upload_mode = self.upload_mode
+            d.host_fd = -1 if self._fd is None else int(self._fd)
+            d.host_fd_offset = int(getattr(scene, "gaus_offset", 0)) if self._fd is not None else 0
             # tile-instance capacity; the session regrows it on overflow
             # (64 M instances, 1 GB: frames with the camera inside dense
             # geometry need tens of millions; past it they blend through the
@@ -479,6 +488,12 @@ class VmSession:
         if h is not None and h.value:
             self._lib.vms_session_destroy(h)
             self._h = None
+        fd = getattr(self, "_fd", None)
+        if fd is not None:
+            import os
+
+            os.close(fd)
+            self._fd = None
 
     # reference attribute: per-page link arrays
     @property
@@ -595,6 +610,7 @@ class VmSession:
             "time_tiles": st.ms_tiles / 1e3,
             "time_blend": st.ms_blend / 1e3,
             "time_device_frame": st.ms_frame / 1e3,
+            "time_host_gather": st.ms_host_gather / 1e3,
             "time_frame_wall": h1 - h0,
             "n_kept": int(st.n_kept),
             "n_instances": int(st.n_inst),

@@ -240,3 +240,43 @@ def test_sharded_sessions_match_per_shard_oracle(cuda, tmp_path):
     for pr, o in zip(procs, outs):
         assert pr.returncode == 0, o
     assert all("shard ok" in o for o in outs), outs
+
+
+def test_binned_visibility_raster_is_bit_exact(cuda):
+    """The binned, chunk-parallel visibility raster (per-tile triangle lists,
+    long lists split over CTAs and merged in chunk order; on by default from
+    65536 faces) forced on for the small meshes: the visibility goldens, the
+    session goldens and C1 still match bit for bit (a subprocess, since the
+    raster variant is fixed per process)."""
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, VMSPLAT_VIS_BIN="1", PYTHONPATH=root)
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-m", "gpu", "-p", "no:cacheprovider",
+                        os.path.join(root, "tests", "test_gpu_parity.py"), "-k",
+                        "visibility or session_matches or c1_session or rasterize or nothing"],
+                       env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+    assert " passed" in r.stdout
+
+
+def test_hot_tile_blend_is_exact(cuda):
+    """The hot-tile blend (blend_hot_k: one CTA per 8x4 block, producer warps
+    computing the FP64 weights of a long list, one consumer warp applying
+    them in list order; on by default for lists >= 32768 instances) forced
+    on for every list >= 256: the composite goldens, the session goldens and
+    C2's first 35 frames still match (a subprocess: the threshold is read
+    once per process)."""
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, VMSPLAT_HOT_LEN="256", PYTHONPATH=root)
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-m", "gpu", "-p", "no:cacheprovider",
+                        os.path.join(root, "tests", "test_gpu_parity.py"), "-k",
+                        "composite or session_matches or c1_session or output_modes or overflow "
+                        "or c2_whole"],
+                       env=env, capture_output=True, text=True, timeout=1500)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+    assert " passed" in r.stdout
