@@ -253,8 +253,8 @@ int32_t vms_reduce_visibility(const uint32_t* page_image, const double* depth_im
                               void* stream);
 
 /* execute_copies (runtime.py:362-374): subsystem [3] data movement.
- * mode 0: one cudaMemcpyBatchAsync of all copies on the copy engines (pinned
- * host source; copies in host memory);
+ * mode 0: copy engines, one cudaMemcpyAsync per run of copies adjacent in
+ * both source and destination (pinned host source; copies in host memory);
  * mode 1: one gather kernel reading mapped pinned host memory (copies in
  * [dev]-accessible memory; occupies SMs while it waits on PCIe). */
 int32_t vms_upload_pages(const vms_copy* copies, int64_t n, const void* host_base,

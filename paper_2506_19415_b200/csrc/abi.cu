@@ -382,31 +382,22 @@ int32_t vms_upload_pages(const vms_copy* copies, int64_t n, const void* host_bas
   if (n == 0) return VMS_OK;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (mode == 0) {
-    // copy engines: one batched call for all pages (no SM time - the pages
+    // copy engines: one cudaMemcpyAsync per run of copies that are adjacent
+    // in both the host scene and the destination (no SM time - the pages
     // stream in while the previous frame renders at full SM occupancy)
     const char* h = static_cast<const char*>(host_base);
     char* d = static_cast<char*>(dev_base);
-    thread_local std::vector<void*> dsts, srcs;
-    thread_local std::vector<size_t> sizes;
-    dsts.resize(n);
-    srcs.resize(n);
-    sizes.resize(n);
-    for (int64_t i = 0; i < n; ++i) {
-      dsts[i] = d + copies[i].dst_offset;
-      srcs[i] = const_cast<char*>(h + copies[i].src_offset);
-      sizes[i] = copies[i].nbytes;
+    int64_t i = 0;
+    while (i < n) {
+      uint64_t src = copies[i].src_offset, dst = copies[i].dst_offset, nb = copies[i].nbytes;
+      int64_t j = i + 1;
+      while (j < n && copies[j].src_offset == src + nb && copies[j].dst_offset == dst + nb) {
+        nb += copies[j].nbytes;
+        ++j;
+      }
+      VMS_CUDA(cudaMemcpyAsync(d + dst, h + src, nb, cudaMemcpyHostToDevice, s));
+      i = j;
     }
-    int dev = 0;
-    VMS_CUDA(cudaGetDevice(&dev));
-    cudaMemcpyAttributes at = {};
-    at.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-    at.srcLocHint.type = cudaMemLocationTypeHost;
-    at.dstLocHint.type = cudaMemLocationTypeDevice;
-    at.dstLocHint.id = dev;
-    at.flags = cudaMemcpyFlagPreferOverlapWithCompute;
-    size_t idx = 0, fail = 0;
-    VMS_CUDA(cudaMemcpyBatchAsync(dsts.data(), srcs.data(), sizes.data(), (size_t)n, &at, &idx,
-                                  1, &fail, s));
     return VMS_OK;
   }
   mark("begin", s);

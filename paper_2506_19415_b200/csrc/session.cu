@@ -203,6 +203,7 @@ struct vms_session {
   Graph vis_graph, render_graph[2][2];  // render: [timing][banded]
   std::vector<uint64_t> level_start;  // first row of each level block
   std::vector<uint32_t> plan_pid;
+  std::vector<int32_t> plan_order;
   std::vector<uint8_t> plan_level;
   std::vector<int32_t> plan_entry, plan_slot;
 };
@@ -597,15 +598,26 @@ int32_t vms_session_frame(vms_session* s, const vms_frame_args* a, vms_frame_sta
   rc = recycle(s, par);
   if (rc) return rc;
   // copy plan: scene rows -> packed staging, staging -> pool slot rows
+  // (packed into staging in scene order, so pages adjacent in the scene
+  // file become one copy)
   uint64_t bytes = 0;
   const uint64_t rb = (uint64_t)kRecordFloats * sizeof(float);
-  for (int64_t i = 0; i < n_plan; ++i) {
+  auto src_row = [&](int64_t i) {
+    const uint32_t lv = s->plan_level[i];
+    return s->level_start[lv] + (uint64_t)(s->plan_pid[i] - 1) * ((uint64_t)s->d.page_size >> lv);
+  };
+  s->plan_order.resize(n_plan);
+  for (int64_t i = 0; i < n_plan; ++i) s->plan_order[i] = (int32_t)i;
+  std::sort(s->plan_order.begin(), s->plan_order.end(),
+            [&](int32_t x, int32_t y) { return src_row(x) < src_row(y); });
+  for (int64_t k = 0; k < n_plan; ++k) {
+    const int64_t i = s->plan_order[k];
     const uint32_t lv = s->plan_level[i];
     const uint64_t per = (uint64_t)s->d.page_size >> lv;
-    const uint64_t src = s->level_start[lv] + (uint64_t)(s->plan_pid[i] - 1) * per;
+    const uint64_t src = src_row(i);
     const uint64_t dst = (uint64_t)s->plan_entry[i] * s->d.page_size + (uint64_t)s->plan_slot[i] * per;
-    s->copies[par][i] = vms_copy{src * rb, bytes, per * rb};
-    s->scatter_h[par][i] = vms_copy{bytes, dst * rb, per * rb};
+    s->copies[par][k] = vms_copy{src * rb, bytes, per * rb};
+    s->scatter_h[par][k] = vms_copy{bytes, dst * rb, per * rb};
     bytes += per * rb;
   }
   // chunk table of every resident page, ascending page id (gather order)
