@@ -382,6 +382,49 @@ int32_t vms_session_wait(vms_session* s, int32_t back);
 /* Wait for the last frame; out4 = its n_kept, n_inst, overflow, n_need. */
 int32_t vms_session_counters(vms_session* s, uint32_t* out4, void* stream);
 
+/* ---- weighted k-means LOD pyramid (lod.py) -------------- */
+
+/* NumPy's Philox bit-generator state (Generator(Philox(...)).bit_generator
+ * .state: counter, key, buffer, buffer_pos, has_uint32, uinteger). */
+typedef struct vms_philox {
+  uint64_t counter[4];
+  uint64_t key[2];
+  uint64_t buffer[4];
+  int32_t buffer_pos;
+  int32_t has_uint32;
+  uint32_t uinteger;
+  uint32_t _pad;
+} vms_philox;
+
+typedef struct vms_lod_params {
+  double weights[5];    /* AttributeWeights position, rotation, scale, opacity,
+                           sh_dc (lod.py:26-41) */
+  double scale_factor;  /* merge volume compensation (lod.py:22, :150) */
+  int32_t max_iters;    /* Lloyd iteration cap (lod.py:23, :106) */
+  int32_t k;            /* 0: one pyramid level (_page_pyramid, lod.py:157-176):
+                           all-zero rows are padding, k = ceil(live / 2), the
+                           clusters are merged into `out`; > 0: cluster_page
+                           (lod.py:83-131) of every row with this k, the
+                           cluster index per row into `assign_out`; -1:
+                           merge_cluster (lod.py:134-154) of all rows into
+                           the first row of `out` */
+} vms_lod_params;
+
+size_t vms_lod_workspace_bytes(uint32_t pages, uint32_t rows_in);
+
+/* One CTA per page, `pages` pages of `rows_in` records (59 f32) at `in`
+ * [dev]; rows_in <= 4096.  Pyramid mode writes each page's merged records
+ * to the front of its `rows_out` rows of `out` [dev] (the rest zero), in
+ * cluster order, exactly as _page_pyramid + merge_cluster (lod.py:134-176).
+ * `rng` [dev] holds one NumPy Philox state per page and is advanced exactly
+ * as the reference's draws advance it.  `status` [dev] per page: 0 ok,
+ * 1 k-means inertia increased (InvariantViolation, lod.py:113-114), 2 level
+ * overflow (lod.py:171-172).  Results are bit-identical to the reference. */
+int32_t vms_lod_level(const float* in, uint32_t pages, uint32_t rows_in, float* out,
+                      uint32_t rows_out, const vms_lod_params* params, vms_philox* rng,
+                      int32_t* assign_out, int32_t* status, void* workspace,
+                      size_t workspace_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -96,6 +96,17 @@ class FrameStats(ctypes.Structure):
                 ("ms_host_gather", ctypes.c_float), ("host_update_s", D)]
 
 
+class Philox(ctypes.Structure):
+    """NumPy Philox bit-generator state (include/vmsplat_b200.h vms_philox)."""
+    _fields_ = [("counter", ctypes.c_uint64 * 4), ("key", ctypes.c_uint64 * 2),
+                ("buffer", ctypes.c_uint64 * 4), ("buffer_pos", I32), ("has_uint32", I32),
+                ("uinteger", U32), ("_pad", U32)]
+
+
+class LodParams(ctypes.Structure):
+    _fields_ = [("weights", D * 5), ("scale_factor", D), ("max_iters", I32), ("k", I32)]
+
+
 # name -> (restype, argtypes); every symbol include/vmsplat_b200.h declares
 SIGNATURES = {
     "vms_last_error": (ctypes.c_char_p, []),
@@ -144,6 +155,8 @@ SIGNATURES = {
     "vms_debug_blend_trace": (I32, [P]),
     "vms_debug_exp": (I32, [P, I64, P, P]),
     "vms_bvh_nearest_points": (I32, [P, I64, P, P, P, I64, P, P, I64, P, P, P, P]),
+    "vms_lod_workspace_bytes": (SZ, [U32, U32]),
+    "vms_lod_level": (I32, [P, U32, U32, P, U32, ctypes.POINTER(LodParams), P, P, P, P, SZ, P]),
 }
 
 _lib = None

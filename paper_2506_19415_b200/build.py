@@ -29,6 +29,7 @@ UNITS = {
     "abi.cu": [],
     "session.cu": [],
     "bvh.cu": ["-fmad=false"],
+    "lod.cu": ["-fmad=false"],
 }
 HOST_UNITS = {"pagetable.cpp": ["-O2", "-std=c++17", "-fPIC"]}
 HEADERS = ["common.cuh", "prims.h", "render.h", "vis.h"]

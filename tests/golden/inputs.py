@@ -254,3 +254,37 @@ def c1_path(cp_module=None):
     cps = (cp_module.Checkpoint((0.0, 0.0, -2.0), (1.0, 0.0, 0.0, 0.0)),
            cp_module.Checkpoint((0.0, 0.0, -16.0), (1.0, 0.0, 0.0, 0.0)))
     return cp_module.CameraPath(cps, speed=2.0, fps=1.0, fov_deg=90.0, width=256, height=256)
+
+
+def wall_scene(seed=2, count=12000, extent=8.0, z=10.0, thickness=0.3, scale=0.28):
+    """Restates pkg/src/vmsplat/synthetic.py:36-50,110-113."""
+    rng = np.random.default_rng(seed)
+    pos = np.column_stack([rng.uniform(-extent, extent, count),
+                           rng.uniform(-extent, extent, count),
+                           rng.normal(z, thickness, count)])
+    s = np.exp(rng.normal(np.log(scale), 0.25, size=(count, 3))).astype(np.float32)
+    s[:, 2] *= 0.6
+    return _synthetic_records(rng, pos, s)
+
+
+def padded_pages(counts, page_size, seed0=10, dup=1):
+    """Level-0 pages (lod tests): page i holds counts[i] box-scene records
+    (each repeated `dup` times, so k-means sees coincident points), padded
+    with zero rows to page_size."""
+    rows = []
+    for i, c in enumerate(counts):
+        base = box_scene(seed=seed0 + i, count=-(-c // dup), extent=3.0, depth=8.0)
+        r = np.repeat(base, dup, axis=0)[:c]
+        pad = np.zeros((page_size - c, RECORD_SIZE), np.float32)
+        rows.append(np.concatenate([r, pad]))
+    return np.concatenate(rows)
+
+
+# (name, counts, page_size, level_count, max_iters, seed, dup)
+LOD_PYRAMIDS = [
+    ("reftest", (64, 50, 7), 64, 3, 10, 7, 1),
+    ("mixed", (256, 201, 130, 33, 1, 0, 255, 96), 256, 4, 50, 7, 1),
+    ("dups", (120, 64), 128, 3, 50, 11, 3),
+]
+# the C2-size page (one page of 2048 records, 2 levels): hash only
+LOD_BIG = ("big", (2048,), 2048, 2, 50, 7, 1)

@@ -23,8 +23,8 @@ SCENES = os.path.join(HERE, "golden", "ref_scenes")
 def install():
     if "vmsplat" in sys.modules and getattr(sys.modules["vmsplat"], "IS_ALIAS", False):
         return sys.modules["vmsplat"]
-    from paper_2506_19415_b200 import (camera_path, errors, gaussians, harness, kernels, render,
-                                       runtime, scene_io)
+    from paper_2506_19415_b200 import (camera_path, errors, gaussians, harness, kernels, lod,
+                                       render, runtime, scene_io)
 
     pkg = types.ModuleType("vmsplat")
     pkg.__path__ = []
@@ -38,7 +38,7 @@ def install():
     metrics.ssim = _metrics_restatement.ssim
     mods = {"render": render, "runtime": runtime, "kernels": kernels, "scene_io": scene_io,
             "errors": errors, "gaussians": gaussians, "camera_path": camera_path,
-            "harness": harness, "mesh": mesh, "metrics": metrics}
+            "harness": harness, "mesh": mesh, "metrics": metrics, "lod": lod}
     sys.modules["vmsplat"] = pkg
     for name, mod in mods.items():
         setattr(pkg, name, mod)
