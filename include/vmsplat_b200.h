@@ -382,6 +382,48 @@ int32_t vms_session_wait(vms_session* s, int32_t back);
 /* Wait for the last frame; out4 = its n_kept, n_inst, overflow, n_need. */
 int32_t vms_session_counters(vms_session* s, uint32_t* out4, void* stream);
 
+/* ---- device-resident page table ------------------------- */
+
+/* Opaque device page table (csrc/dpt.cu): the state of runtime.PageTable
+ * (runtime.py:161-291) in device memory; capacity <= 8192 entries, levels
+ * <= 6.  Not thread-safe; one stream at a time. */
+typedef struct vms_dpt vms_dpt;
+
+typedef struct vms_dpt_frame {  /* [dev] per-frame inputs of the update */
+  int64_t frame;
+  double budget;                /* staging budget in level-0 pages */
+} vms_dpt_frame;
+
+typedef struct vms_dpt_stats {  /* [dev or mapped host] per-frame outputs */
+  uint32_t n_req, n_plan, missing, resident, occupied, bad, plan_overflow;
+  uint32_t n_chunks, n_records, pad_;
+  uint32_t resident_per_level[16];
+} vms_dpt_stats;
+
+vms_dpt* vms_dpt_create(int32_t capacity, int32_t page_count, int32_t levels);
+void vms_dpt_destroy(vms_dpt* d);
+size_t vms_dpt_smem_bytes(const vms_dpt* d);
+/* update_page_table (runtime.py:294-346) on the device: the required list
+ * (ascending page id, [dev] arrays as reduce_visibility + select_lod produce
+ * them, *n_req [dev]) -> the copy plan (pid, level, entry, slot) in the
+ * reference's order, stats.  Bit-identical plans, residency, LRU stamps and
+ * missing counts to the reference (and to vms_pt_update).  Graph-capturable. */
+int32_t vms_dpt_update(vms_dpt* d, const uint32_t* pid, const uint32_t* enc,
+                       const uint8_t* direct, const uint8_t* level, const uint32_t* n_req,
+                       const vms_dpt_frame* frame, uint32_t* plan_pid, uint8_t* plan_level,
+                       int32_t* plan_entry, int32_t* plan_slot, int64_t plan_cap,
+                       vms_dpt_stats* stats, void* stream);
+/* gather_resident's order (runtime.py:377-390) as <= 128-record chunks
+ * {pool row, gather index, count} of every resident page, ascending page id,
+ * into out [dev]; stats->n_chunks / n_records.  Graph-capturable. */
+int32_t vms_dpt_chunks(vms_dpt* d, uint32_t page_size, vms_chunk* out, int64_t cap,
+                       vms_dpt_stats* stats, void* stream);
+/* Snapshot (synchronises `stream`): per entry level (-1 empty), LRU stamp and
+ * max_slots slot page ids [host]; res [host] (page_count + 1) entry << 8 | slot
+ * or 0xFFFFFFFF. */
+int32_t vms_dpt_state(const vms_dpt* d, int32_t* level, int64_t* last_used, uint32_t* slots,
+                      int32_t max_slots, uint32_t* res, void* stream);
+
 /* ---- weighted k-means LOD pyramid (lod.py) -------------- */
 
 /* NumPy's Philox bit-generator state (Generator(Philox(...)).bit_generator

@@ -103,6 +103,16 @@ class Philox(ctypes.Structure):
                 ("uinteger", U32), ("_pad", U32)]
 
 
+class DptFrame(ctypes.Structure):
+    _fields_ = [("frame", I64), ("budget", D)]
+
+
+class DptStats(ctypes.Structure):
+    _fields_ = [("n_req", U32), ("n_plan", U32), ("missing", U32), ("resident", U32),
+                ("occupied", U32), ("bad", U32), ("plan_overflow", U32), ("n_chunks", U32),
+                ("n_records", U32), ("pad_", U32), ("resident_per_level", U32 * 16)]
+
+
 class LodParams(ctypes.Structure):
     _fields_ = [("weights", D * 5), ("scale_factor", D), ("max_iters", I32), ("k", I32)]
 
@@ -156,6 +166,12 @@ SIGNATURES = {
     "vms_debug_exp": (I32, [P, I64, P, P]),
     "vms_bvh_nearest_points": (I32, [P, I64, P, P, P, I64, P, P, I64, P, P, P, P]),
     "vms_lod_workspace_bytes": (SZ, [U32, U32]),
+    "vms_dpt_create": (P, [I32, I32, I32]),
+    "vms_dpt_destroy": (None, [P]),
+    "vms_dpt_smem_bytes": (SZ, [P]),
+    "vms_dpt_update": (I32, [P, P, P, P, P, P, P, P, P, P, P, I64, P, P]),
+    "vms_dpt_chunks": (I32, [P, U32, P, I64, P, P]),
+    "vms_dpt_state": (I32, [P, P, P, P, I32, P, P]),
     "vms_lod_level": (I32, [P, U32, U32, P, U32, ctypes.POINTER(LodParams), P, P, P, P, SZ, P]),
 }
 

@@ -30,6 +30,7 @@ UNITS = {
     "session.cu": [],
     "bvh.cu": ["-fmad=false"],
     "lod.cu": ["-fmad=false"],
+    "dpt.cu": [],
 }
 HOST_UNITS = {"pagetable.cpp": ["-O2", "-std=c++17", "-fPIC"]}
 HEADERS = ["common.cuh", "prims.h", "render.h", "vis.h"]

@@ -308,6 +308,142 @@ class PageTable:
         return pp[:k].copy(), pl[:k].copy(), pe[:k].copy(), ps[:k].copy(), int(missing.value)
 
 
+class DevicePageTable:
+    """The same table resident in device memory (SURVEY §8(f) F2,
+    csrc/dpt.cu): ``update`` runs update_page_table's two passes on the GPU
+    (one CTA; bit-identical plans, LRU stamps and residency to PageTable and
+    the reference).  Queries take a device snapshot.  capacity <= 8192,
+    levels <= 6; ``page_count`` bounds the page ids."""
+
+    def __init__(self, capacity: int, page_count: int, levels: int = 1):
+        if capacity < 1:
+            raise InvariantViolation("page table needs at least one entry")
+        self._lib = _lib.load()
+        t = _device.require_cuda()
+        h = self._lib.vms_dpt_create(int(capacity), int(page_count), int(levels))
+        if not h:
+            raise InvariantViolation(self._lib.vms_last_error().decode())
+        self._h = ctypes.c_void_p(h)
+        self._cap, self._pages, self._levels = int(capacity), int(page_count), int(levels)
+        self._t = t
+        dev = t.device("cuda", t.cuda.current_device())
+        self._frame = t.zeros(16, dtype=t.uint8, device=dev)
+        self._stats = t.zeros(ctypes.sizeof(_lib.DptStats), dtype=t.uint8, device=dev)
+        self._n = t.zeros(1, dtype=t.int32, device=dev)
+        self._last_stats = _lib.DptStats()
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            self._lib.vms_dpt_destroy(h)
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    @property
+    def capacity(self) -> int:
+        return self._cap
+
+    def _state(self):
+        ms = 1 << (self._levels - 1)
+        level = np.zeros(self._cap, np.int32)
+        last = np.zeros(self._cap, np.int64)
+        slots = np.zeros((self._cap, ms), np.uint32)
+        res = np.zeros(self._pages + 1, np.uint32)
+        _lib.check(self._lib.vms_dpt_state(self._h, level.ctypes.data, last.ctypes.data,
+                                           slots.ctypes.data, ms, res.ctypes.data,
+                                           _device.sptr()), "dpt_state")
+        return level, last, slots, res
+
+    @property
+    def entries(self) -> list:
+        level, last, slots, _ = self._state()
+        return [PageTableEntry(int(lv), int(la), [int(x) for x in sl[:(1 << lv)]] if lv >= 0 else [])
+                for lv, la, sl in zip(level, last, slots)]
+
+    @property
+    def resident(self) -> dict:
+        _, _, _, res = self._state()
+        ids = np.flatnonzero(res != 0xFFFFFFFF)
+        return {int(p): (int(res[p] >> 8), int(res[p] & 0xFF)) for p in ids}
+
+    def resident_count(self) -> int:
+        return len(self.resident)
+
+    def occupied_entries(self) -> int:
+        level, _, _, _ = self._state()
+        return int((level >= 0).sum())
+
+    def usage_ratio(self) -> float:
+        return self.occupied_entries() / self.capacity
+
+    def resident_level(self, page_id: int):
+        loc = self.resident.get(page_id)
+        return None if loc is None else self.entries[loc[0]].lod_level
+
+    def resident_counts(self, level_count: int) -> tuple:
+        counts = [0] * level_count
+        level, _, _, res = self._state()
+        for p in np.flatnonzero(res != 0xFFFFFFFF):
+            counts[int(level[res[p] >> 8])] += 1
+        return tuple(counts)
+
+    def check(self) -> None:
+        """Cross-check the residency map against the entries (runtime.py:218-234)."""
+        level, _, slots, res = self._state()
+        seen = {}
+        for ei in range(self._cap):
+            if level[ei] < 0:
+                continue
+            for si, pid in enumerate(slots[ei, :(1 << int(level[ei]))]):
+                if pid:
+                    if int(pid) in seen:
+                        raise InvariantViolation(f"page {pid} resident twice")
+                    seen[int(pid)] = (ei, si)
+        mapped = {int(p): (int(res[p] >> 8), int(res[p] & 0xFF))
+                  for p in np.flatnonzero(res != 0xFFFFFFFF)}
+        if seen != mapped:
+            raise InvariantViolation("residency map out of sync with entries")
+
+    def update(self, pid, enc, direct, level, frame: int, budget: float):
+        """update_page_table's two passes on the device (compacted required
+        arrays, ascending page id); returns (plan_pid, plan_level,
+        plan_entry, plan_slot, missing)."""
+        t = self._t
+        n = len(pid)
+        dev = self._frame.device
+        def arr(x, dt):  # at least one element (an empty list passes a dummy)
+            x = np.ascontiguousarray(x, dt)
+            return _device.to_dev(x if len(x) else np.zeros(1, dt), dt)
+
+        pid_d, enc_d = arr(pid, np.uint32), arr(enc, np.uint32)
+        dir_d, lvl_d = arr(direct, np.uint8), arr(level, np.uint8)
+        fr = _lib.DptFrame(int(frame), float(budget))
+        self._frame.copy_(t.frombuffer(bytearray(bytes(fr)), dtype=t.uint8))
+        self._n.fill_(n)
+        cap = max(n, 1)
+        pp = t.zeros(cap, dtype=t.int32, device=dev)
+        pl = t.zeros(cap, dtype=t.uint8, device=dev)
+        pe = t.zeros(cap, dtype=t.int32, device=dev)
+        ps = t.zeros(cap, dtype=t.int32, device=dev)
+        _lib.check(self._lib.vms_dpt_update(self._h, _lib.ptr(pid_d), _lib.ptr(enc_d),
+                                            _lib.ptr(dir_d), _lib.ptr(lvl_d), self._n.data_ptr(),
+                                            self._frame.data_ptr(), pp.data_ptr(), pl.data_ptr(),
+                                            pe.data_ptr(), ps.data_ptr(), cap,
+                                            self._stats.data_ptr(), _device.sptr()),
+                   "update_page_table (device)")
+        raw = self._stats.cpu().numpy().tobytes()
+        st = _lib.DptStats.from_buffer_copy(raw)
+        self._last_stats = st
+        if st.bad:
+            raise InvariantViolation("required page id or LOD level out of range")
+        k = int(st.n_plan)
+        return (pp[:k].cpu().numpy().astype(np.uint32), pl[:k].cpu().numpy(),
+                pe[:k].cpu().numpy(), ps[:k].cpu().numpy(), int(st.missing))
+
+
 def update_page_table(table: PageTable, required: RequiredList, controller: LodController,
                       frame: int, staging_budget_pages: float):
     """Two-pass table update (runtime.py:294-346).  Returns (plan, missing)."""

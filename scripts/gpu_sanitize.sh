@@ -1,6 +1,9 @@
 # compute-sanitizer memcheck / racecheck / synccheck on smoke() and on three
 # C2 frames (1080p, bench scene), logs under gpurun_out/sanitize/
 mkdir -p gpurun_out/sanitize
+cat > gpurun_out/sanitize/README <<X
+compute-sanitizer on smoke() and on 3 C2 frames (bench scene)
+X
 CS="compute-sanitizer --print-limit 50 --error-exitcode 9"
 SMOKE='import __graft_entry__ as g; g.smoke()'
 for tool in memcheck racecheck synccheck; do
