@@ -299,7 +299,9 @@ def bench_config(args, lay, world=1):
             "blend": "fp32" if args.fast else "fp64-exact",
             "l2": f"inputs larger than L2 (resident page pool up to {pool_mb:.0f} MB, "
                   f"126 MB L2; the frame's records stream from it every step)",
-            "upload_mode": upload_mode_of(args)}
+            "upload_mode": upload_mode_of(args),
+            "page_table": "device" if os.environ.get("VMSPLAT_DEVICE_TABLE", "0") == "1"
+            else "host"}
 
 
 def measure_pcie(torch, nbytes=256 << 20, reps=10):

@@ -326,6 +326,11 @@ typedef struct vms_session_desc {
                                    of being copied out of host_records (no page faults on a
                                    fresh mapping); -1 -> copy from host_records */
   uint64_t host_fd_offset;      /* byte offset of the record section in host_fd */
+  int32_t device_table;         /* 1: the page table lives on the device (vms_dpt, SURVEY
+                                   8(f) F2) - updated by a kernel right after the visibility
+                                   pass, the host only issues the planned copies; needs
+                                   capacity <= 8192 and lod_levels <= 6 */
+  int32_t pad_;
 } vms_session_desc;
 
 typedef struct vms_frame_args {
@@ -401,6 +406,8 @@ typedef struct vms_dpt_stats {  /* [dev or mapped host] per-frame outputs */
 } vms_dpt_stats;
 
 vms_dpt* vms_dpt_create(int32_t capacity, int32_t page_count, int32_t levels);
+/* The device table of a session created with device_table = 1 (else NULL). */
+vms_dpt* vms_session_dpt(vms_session* s);
 void vms_dpt_destroy(vms_dpt* d);
 size_t vms_dpt_smem_bytes(const vms_dpt* d);
 /* update_page_table (runtime.py:294-346) on the device: the required list
@@ -420,7 +427,7 @@ int32_t vms_dpt_chunks(vms_dpt* d, uint32_t page_size, vms_chunk* out, int64_t c
                        vms_dpt_stats* stats, void* stream);
 /* Snapshot (synchronises `stream`): per entry level (-1 empty), LRU stamp and
  * max_slots slot page ids [host]; res [host] (page_count + 1) entry << 8 | slot
- * or 0xFFFFFFFF. */
+ * or 0xFFFFFFFF.  Synchronises the device. */
 int32_t vms_dpt_state(const vms_dpt* d, int32_t* level, int64_t* last_used, uint32_t* slots,
                       int32_t max_slots, uint32_t* res, void* stream);
 

@@ -75,7 +75,7 @@ class SessionDesc(ctypes.Structure):
                 ("m_cap", U32), ("vis_ws", P), ("render_ws", P),
                 ("render_ws_bytes", ctypes.c_uint64), ("width", I32), ("height", I32),
                 ("exact", I32), ("upload_mode", I32), ("host_fd", I32),
-                ("host_fd_offset", ctypes.c_uint64)]
+                ("host_fd_offset", ctypes.c_uint64), ("device_table", I32), ("pad_", I32)]
 
 
 class FrameArgs(ctypes.Structure):
@@ -155,6 +155,7 @@ SIGNATURES = {
     "vms_session_create": (P, [ctypes.POINTER(SessionDesc)]),
     "vms_session_destroy": (None, [P]),
     "vms_session_table": (P, [P]),
+    "vms_session_dpt": (P, [P]),
     "vms_session_set_render_ws": (I32, [P, P, ctypes.c_uint64, U32, I32, I32]),
     "vms_session_frame": (I32, [P, ctypes.POINTER(FrameArgs), ctypes.POINTER(FrameStats), P]),
     "vms_session_counters": (I32, [P, P, P]),

@@ -576,8 +576,8 @@ int32_t vms_dpt_state(const vms_dpt* d, int32_t* level, int64_t* last_used, uint
     set_error("dpt_state: invalid arguments");
     return VMS_ERR_INVALID;
   }
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  VMS_CUDA(cudaStreamSynchronize(s));
+  (void)stream;  // the table may be updated on a session's own streams
+  VMS_CUDA(cudaDeviceSynchronize());
   const size_t C = d->C;
   std::vector<int8_t> lv(C);
   std::vector<int32_t> last(C);

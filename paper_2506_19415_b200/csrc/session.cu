@@ -200,7 +200,20 @@ struct vms_session {
   int64_t max_chunks = 0;
   int parity = 0;
   bool use_graphs = true;
-  Graph vis_graph, render_graph[2][2];  // render: [timing][banded]
+  Graph vis_graph[2], render_graph[2][2];  // vis: [parity] (device table); render: [timing][banded]
+  // device page table (desc.device_table): its outputs land in mapped memory
+  // (plan, stats) and per-parity device chunk tables; the next frame of the
+  // same parity waits for ev_chunks before its update overwrites them
+  vms_dpt* dpt = nullptr;
+  uint32_t* dplan_pid = nullptr;
+  uint8_t* dplan_level = nullptr;
+  int32_t* dplan_entry = nullptr;
+  int32_t* dplan_slot = nullptr;
+  vms_dpt_stats* dstats = nullptr;
+  vms_dpt_frame* dframe = nullptr;
+  vms_chunk* chunks_dev[2] = {nullptr, nullptr};
+  cudaEvent_t ev_chunks[2] = {nullptr, nullptr};
+  bool chunks_pending[2] = {false, false};
   std::vector<uint64_t> level_start;  // first row of each level block
   std::vector<uint32_t> plan_pid;
   std::vector<int32_t> plan_order;
@@ -213,7 +226,15 @@ namespace {
 
 void free_session(vms_session* s) {
   if (!s) return;
-  s->vis_graph.reset();
+  for (auto& g : s->vis_graph) g.reset();
+  if (s->dpt) vms_dpt_destroy(s->dpt);
+  for (cudaEvent_t e : s->ev_chunks)
+    if (e) cudaEventDestroy(e);
+  for (void* p : {(void*)s->dplan_pid, (void*)s->dplan_level, (void*)s->dplan_entry,
+                  (void*)s->dplan_slot, (void*)s->dstats, (void*)s->dframe})
+    if (p) cudaFreeHost(p);
+  for (vms_chunk* p : s->chunks_dev)
+    if (p) cudaFree(p);
   for (auto& gt : s->render_graph)
     for (auto& g : gt) g.reset();
   if (s->pt) vms_pt_destroy(s->pt);
@@ -479,6 +500,23 @@ vms_session* vms_session_create(const vms_session_desc* desc) {
   }
   ok = ok && cudaMalloc(&s->scatter_d, sizeof(vms_copy) * (P + 1)) == cudaSuccess;
   ok = ok && cudaMalloc(&s->chunks_d, sizeof(vms_chunk) * s->max_chunks) == cudaSuccess;
+  if (ok && desc->device_table) {
+    s->dpt = vms_dpt_create((int32_t)desc->capacity, (int32_t)P, (int32_t)desc->lod_levels);
+    if (!s->dpt) {
+      free_session(s);
+      return nullptr;  // vms_dpt_create set the error
+    }
+    ok = ok && host_alloc(&s->dplan_pid, P + 1) == cudaSuccess;
+    ok = ok && host_alloc(&s->dplan_level, P + 1) == cudaSuccess;
+    ok = ok && host_alloc(&s->dplan_entry, P + 1) == cudaSuccess;
+    ok = ok && host_alloc(&s->dplan_slot, P + 1) == cudaSuccess;
+    ok = ok && host_alloc(&s->dstats, 1) == cudaSuccess;
+    ok = ok && host_alloc(&s->dframe, 1) == cudaSuccess;
+    for (int k = 0; k < 2; ++k) {
+      ok = ok && cudaMalloc(&s->chunks_dev[k], sizeof(vms_chunk) * s->max_chunks) == cudaSuccess;
+      ok = ok && cudaEventCreateWithFlags(&s->ev_chunks[k], cudaEventDisableTiming) == cudaSuccess;
+    }
+  }
   if (!ok) {
     set_error("session_create: %s", cudaGetErrorString(cudaGetLastError()));
     free_session(s);
@@ -512,6 +550,8 @@ void vms_session_destroy(vms_session* s) {
 }
 
 vms_pagetable* vms_session_table(vms_session* s) { return s ? s->pt : nullptr; }
+
+vms_dpt* vms_session_dpt(vms_session* s) { return s ? s->dpt : nullptr; }
 
 int32_t vms_session_set_render_ws(vms_session* s, void* ws, uint64_t bytes, uint32_t m_cap,
                                   int32_t width, int32_t height) {
@@ -551,6 +591,12 @@ int32_t vms_session_frame(vms_session* s, const vms_frame_args* a, vms_frame_sta
   // (same parity) is recycled: that frame's image copy to the host and the
   // visibility pass, which queues behind the render in flight for SM slots,
   // then overlap instead of adding up.
+  if (s->dpt) {
+    // this parity's device chunk table is free once the frame two back copied it
+    if (s->chunks_pending[par]) VMS_CUDA(cudaStreamWaitEvent(s->vis_stream, s->ev_chunks[par], 0));
+    s->dframe->frame = a->frame;
+    s->dframe->budget = a->budget;
+  }
   if (timing) VMS_CUDA(cudaEventRecord(s->tev[0], s->vis_stream));
   if (tl >= 0) VMS_CUDA(cudaEventRecord(s->tl_ev[tl][0], s->vis_stream));
   s->vis_fd_h->cam = a->vis_cam;
@@ -573,8 +619,20 @@ int32_t vms_session_frame(vms_session* s, const vms_frame_args* a, vms_frame_sta
   v.out.level = s->req_level;
   v.out.meta = s->req_meta;
   v.workspace = s->d.vis_ws;
-  rc = run_captured(s, s->vis_graph, v.cam.width, v.cam.height, 0,
-                    [&](cudaStream_t q, bool) { return vis_launch(v, q); }, s->vis_stream);
+  rc = run_captured(s, s->vis_graph[s->dpt ? par : 0], v.cam.width, v.cam.height, 0,
+                    [&](cudaStream_t q, bool) {
+                      int32_t r = vis_launch(v, q);
+                      if (r || !s->dpt) return r;
+                      // [3] on the device: update_page_table, then the chunk table
+                      r = vms_dpt_update(s->dpt, s->req_pid, s->req_enc, s->req_direct,
+                                         s->req_level, s->req_meta + 1, s->dframe, s->dplan_pid,
+                                         s->dplan_level, s->dplan_entry, s->dplan_slot,
+                                         (int64_t)P + 1, s->dstats, q);
+                      if (r) return r;
+                      return vms_dpt_chunks(s->dpt, s->d.page_size, s->chunks_dev[par],
+                                            s->max_chunks, s->dstats, q);
+                    },
+                    s->vis_stream);
   if (rc) return rc;
   if (timing) VMS_CUDA(cudaEventRecord(s->tev[1], s->vis_stream));
   if (tl >= 0) VMS_CUDA(cudaEventRecord(s->tl_ev[tl][1], s->vis_stream));
@@ -588,12 +646,31 @@ int32_t vms_session_frame(vms_session* s, const vms_frame_args* a, vms_frame_sta
     return VMS_ERR_INVARIANT;
   }
   const auto h0 = std::chrono::steady_clock::now();
-  // [3] page table (exact update_page_table)
+  // [3] page table (exact update_page_table): on the host, or already done
+  // on the device (read its plan and stats)
   int64_t n_plan = 0, missing = 0;
-  rc = vms_pt_update(s->pt, s->req_pid, s->req_enc, s->req_direct, s->req_level, n_req, a->frame,
-                     a->budget, s->plan_pid.data(), s->plan_level.data(), s->plan_entry.data(),
-                     s->plan_slot.data(), (int64_t)s->plan_pid.size(), &n_plan, &missing);
-  if (rc) return rc;
+  const uint32_t* plan_pid = s->plan_pid.data();
+  const uint8_t* plan_level = s->plan_level.data();
+  const int32_t* plan_entry = s->plan_entry.data();
+  const int32_t* plan_slot = s->plan_slot.data();
+  if (s->dpt) {
+    if (s->dstats->bad || s->dstats->plan_overflow) {
+      set_error("device page table: required page id / level out of range or plan overflow");
+      return VMS_ERR_INVARIANT;
+    }
+    n_plan = s->dstats->n_plan;
+    missing = s->dstats->missing;
+    plan_pid = s->dplan_pid;
+    plan_level = s->dplan_level;
+    plan_entry = s->dplan_entry;
+    plan_slot = s->dplan_slot;
+  } else {
+    rc = vms_pt_update(s->pt, s->req_pid, s->req_enc, s->req_direct, s->req_level, n_req,
+                       a->frame, a->budget, s->plan_pid.data(), s->plan_level.data(),
+                       s->plan_entry.data(), s->plan_slot.data(), (int64_t)s->plan_pid.size(),
+                       &n_plan, &missing);
+    if (rc) return rc;
+  }
   // the frame two back (this parity): its host copies, counters, image
   rc = recycle(s, par);
   if (rc) return rc;
@@ -603,8 +680,8 @@ int32_t vms_session_frame(vms_session* s, const vms_frame_args* a, vms_frame_sta
   uint64_t bytes = 0;
   const uint64_t rb = (uint64_t)kRecordFloats * sizeof(float);
   auto src_row = [&](int64_t i) {
-    const uint32_t lv = s->plan_level[i];
-    return s->level_start[lv] + (uint64_t)(s->plan_pid[i] - 1) * ((uint64_t)s->d.page_size >> lv);
+    const uint32_t lv = plan_level[i];
+    return s->level_start[lv] + (uint64_t)(plan_pid[i] - 1) * ((uint64_t)s->d.page_size >> lv);
   };
   s->plan_order.resize(n_plan);
   for (int64_t i = 0; i < n_plan; ++i) s->plan_order[i] = (int32_t)i;
@@ -612,10 +689,10 @@ int32_t vms_session_frame(vms_session* s, const vms_frame_args* a, vms_frame_sta
             [&](int32_t x, int32_t y) { return src_row(x) < src_row(y); });
   for (int64_t k = 0; k < n_plan; ++k) {
     const int64_t i = s->plan_order[k];
-    const uint32_t lv = s->plan_level[i];
+    const uint32_t lv = plan_level[i];
     const uint64_t per = (uint64_t)s->d.page_size >> lv;
     const uint64_t src = src_row(i);
-    const uint64_t dst = (uint64_t)s->plan_entry[i] * s->d.page_size + (uint64_t)s->plan_slot[i] * per;
+    const uint64_t dst = (uint64_t)plan_entry[i] * s->d.page_size + (uint64_t)plan_slot[i] * per;
     s->copies[par][k] = vms_copy{src * rb, bytes, per * rb};
     s->scatter_h[par][k] = vms_copy{bytes, dst * rb, per * rb};
     bytes += per * rb;
@@ -623,7 +700,8 @@ int32_t vms_session_frame(vms_session* s, const vms_frame_args* a, vms_frame_sta
   // chunk table of every resident page, ascending page id (gather order)
   int64_t n_res = 0;
   const int64_t n_chunks =
-      vms_pt_chunks(s->pt, s->d.page_size, s->chunks_h[par], s->max_chunks, &n_res);
+      s->dpt ? (n_res = s->dstats->n_records, (int64_t)s->dstats->n_chunks)
+             : vms_pt_chunks(s->pt, s->d.page_size, s->chunks_h[par], s->max_chunks, &n_res);
   if (n_chunks < 0 || n_chunks > s->max_chunks) {
     set_error("session_frame: chunk table overflow");
     return VMS_ERR_INVARIANT;
@@ -706,9 +784,19 @@ int32_t vms_session_frame(vms_session* s, const vms_frame_args* a, vms_frame_sta
   f->n_splats = (uint32_t)n_res;
   f->counters_host = s->counters_h[par];  // mapped: written by tile_prep_k
   VMS_CUDA(cudaMemcpyAsync(ws.fd, f, sizeof(FrameDev), cudaMemcpyHostToDevice, st));
-  if (n_chunks)
-    VMS_CUDA(cudaMemcpyAsync(s->chunks_d, s->chunks_h[par], sizeof(vms_chunk) * n_chunks,
-                             cudaMemcpyHostToDevice, st));
+  if (n_chunks) {
+    if (s->dpt) {
+      VMS_CUDA(cudaMemcpyAsync(s->chunks_d, s->chunks_dev[par], sizeof(vms_chunk) * n_chunks,
+                               cudaMemcpyDeviceToDevice, st));
+    } else {
+      VMS_CUDA(cudaMemcpyAsync(s->chunks_d, s->chunks_h[par], sizeof(vms_chunk) * n_chunks,
+                               cudaMemcpyHostToDevice, st));
+    }
+  }
+  if (s->dpt) {
+    VMS_CUDA(cudaEventRecord(s->ev_chunks[par], st));
+    s->chunks_pending[par] = true;
+  }
   // host output: the blend runs as kBands launches over bands of tile rows
   // and each band's rows go to the host as soon as that band is blended
   // host output, synchronous call: the blend runs as kBands launches and each
@@ -769,16 +857,21 @@ int32_t vms_session_frame(vms_session* s, const vms_frame_args* a, vms_frame_sta
   if (timing) VMS_CUDA(cudaEventRecord(s->tev[9], st));
   // stats (runtime.py:471-481)
   out->required = n_req;
-  out->resident = (uint32_t)vms_pt_resident_count(s->pt);
+  out->resident = s->dpt ? s->dstats->resident : (uint32_t)vms_pt_resident_count(s->pt);
   out->planned = (uint32_t)n_plan;
   out->missing = (uint32_t)missing;
   out->bytes_copied = bytes;
-  out->occupied_entries = (uint32_t)vms_pt_occupied(s->pt);
+  out->occupied_entries = s->dpt ? s->dstats->occupied : (uint32_t)vms_pt_occupied(s->pt);
   out->capacity = s->d.capacity;
   out->n_chunks = (uint32_t)n_chunks;
   out->n_res = (uint32_t)n_res;
-  rc = vms_pt_resident_counts(s->pt, out->resident_per_level, (int32_t)s->d.lod_levels);
-  if (rc) return rc;
+  if (s->dpt) {
+    for (uint32_t k = 0; k < s->d.lod_levels && k < 16; ++k)
+      out->resident_per_level[k] = s->dstats->resident_per_level[k];
+  } else {
+    rc = vms_pt_resident_counts(s->pt, out->resident_per_level, (int32_t)s->d.lod_levels);
+    if (rc) return rc;
+  }
   if (timing || a->sync || (a->host_image && !async_out)) {
     VMS_CUDA(cudaStreamSynchronize(st));
     const uint32_t* c = s->counters_h[par];

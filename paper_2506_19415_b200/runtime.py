@@ -331,10 +331,21 @@ class DevicePageTable:
         self._stats = t.zeros(ctypes.sizeof(_lib.DptStats), dtype=t.uint8, device=dev)
         self._n = t.zeros(1, dtype=t.int32, device=dev)
         self._last_stats = _lib.DptStats()
+        self._owner = None
+
+    @classmethod
+    def borrowed(cls, handle, capacity: int, page_count: int, levels: int, owner):
+        """A view of the device table owned by a session (kept alive by owner)."""
+        self = cls.__new__(cls)
+        self._lib = _lib.load()
+        self._h = ctypes.c_void_p(handle)
+        self._cap, self._pages, self._levels = int(capacity), int(page_count), int(levels)
+        self._owner = owner
+        return self
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h is not None and h.value:
+        if h is not None and h.value and getattr(self, "_owner", None) is None:
             self._lib.vms_dpt_destroy(h)
             self._h = None
 
@@ -502,7 +513,7 @@ class VmSession:
                  vis_scale: float = 0.25, band=(0.5, 0.8), step: float = 0.05,
                  lod_enabled: bool = True, links_enabled: bool = True, exact: bool = True,
                  upload_mode: int | None = None, timing: bool = True, device=None,
-                 instance_capacity: int | None = None):
+                 instance_capacity: int | None = None, device_table: bool | None = None):
         from paper_2506_19415_b200.render import VisibilityBuffers
 
         t = _device.require_cuda()
@@ -607,14 +618,27 @@ class VmSession:
             # geometry need tens of millions; past it they blend through the
             # exact but slower spill path)
             d.m_cap = int(instance_capacity) if instance_capacity else 1 << 26
+            # the page table on the device: the visibility
+            # graph runs update_page_table too; the host only issues copies
+            if device_table is None:  # default: VMSPLAT_DEVICE_TABLE=1 selects it
+                import os
+
+                device_table = os.environ.get("VMSPLAT_DEVICE_TABLE", "0") == "1"
+            d.device_table = int(bool(device_table))
+            self.device_table = bool(device_table)
             self._desc = d
             self._h = None
             h = self._lib.vms_session_create(ctypes.byref(d))
             if not h:
                 raise InvariantViolation(self._lib.vms_last_error().decode())
             self._h = ctypes.c_void_p(h)
-            self.table = PageTable.borrowed(self._lib.vms_session_table(self._h),
-                                            self.capacity, self)
+            if self.device_table:
+                self.table = DevicePageTable.borrowed(self._lib.vms_session_dpt(self._h),
+                                                      self.capacity, scene.page_count,
+                                                      scene.lod_levels, self)
+            else:
+                self.table = PageTable.borrowed(self._lib.vms_session_table(self._h),
+                                                self.capacity, self)
         self._args = _lib.FrameArgs()
         self._stats = _lib.FrameStats()
         self._pinned_out = None

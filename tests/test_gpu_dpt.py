@@ -125,3 +125,73 @@ def test_device_table_reference_unit_cases(cuda):
     _both(2, 4, [({p: (60.0, True) for p in (1, 2, 3, 4)}, 0, 10)])     # same-level packing
     a = _both(4, 4, [({1: (60.0, True)}, 0, 10), ({1: (1.0, True)}, 1, 10)])  # transition
     assert a.resident_counts(4) == (1, 0, 0, 0)
+
+
+# -- the device table inside a session ----------------------------------------------
+
+STAT_KEYS = ("required_pages", "resident_pages", "resident_per_level", "planned_copies",
+             "missing_pages", "bytes_copied", "usage", "lod_step", "thresholds")
+
+
+@pytest.fixture(scope="module")
+def c2_scene(tmp_path_factory):
+    from paper_2506_19415_b200 import scenegen
+    from paper_2506_19415_b200.scene_io import read_scene
+
+    p = tmp_path_factory.mktemp("c2dpt") / "c2.vms"
+    scenegen.write_city(p, scenegen.C2)
+    return read_scene(p, mmap_gaussians=True)
+
+
+def test_session_device_table_matches_host_table_c2(cuda, c2_scene):
+    """C2 (1000 pages, 3 LOD levels, buffer 500, staging 40) over all 120
+    frames: a session whose page table runs on the device gives the host-table
+    session's stats on every frame, the same residency, and identical images
+    (the host table is pinned to the oracle, tests/test_gpu_parity.py)."""
+    from paper_2506_19415_b200 import scenegen
+    from paper_2506_19415_b200.runtime import VmSession
+
+    traj = scenegen.street_path(scenegen.C2, frames=120)
+    d = VmSession(c2_scene, device_table=True)
+    h = VmSession(c2_scene)
+    for f in range(traj.frame_count):
+        cam = traj.frame_camera(f)
+        a, sa = d.render_frame(cam, f)
+        b, sb = h.render_frame(cam, f)
+        for k in STAT_KEYS:
+            assert sa[k] == sb[k], (f, k)
+        assert np.array_equal(a, b), f
+        if f % 10 == 0:
+            assert d.table.resident == h.table.resident, f
+    d.table.check()
+    ea, eb = d.table.entries, h.table.entries
+    assert [(e.lod_level, e.last_used_frame, e.slots) for e in ea] == \
+        [(e.lod_level, e.last_used_frame, e.slots) for e in eb]
+
+
+def test_session_device_table_pipelined(cuda):
+    """Two frames in flight (the bench's asynchronous device output): every
+    frame rendered into its own device tensor, compared after a flush."""
+    import torch
+
+    from paper_2506_19415_b200.runtime import VmSession
+
+    from paper_2506_19415_b200 import scenegen
+
+    sc = scenegen.city_scene(inputs.CITY_SMALL)
+    path = inputs.city_path(inputs.CITY_SMALL)
+    d = VmSession(sc, buffer_pages=16, staging_pages=6.0, vis_scale=0.5, device_table=True)
+    h = VmSession(sc, buffer_pages=16, staging_pages=6.0, vis_scale=0.5)
+    cam0 = path.frame_camera(0)
+    outs = [torch.empty((cam0.height, cam0.width, 3), dtype=torch.float32, device="cuda")
+            for _ in range(path.frame_count)]
+    stats = []
+    for f in range(path.frame_count):
+        _, st = d.render_frame(path.frame_camera(f), f, out=outs[f])
+        stats.append(st)
+    d.flush()
+    for f in range(path.frame_count):
+        ref, st = h.render_frame(path.frame_camera(f), f)
+        for k in STAT_KEYS:
+            assert stats[f][k] == st[k], (f, k)
+        assert np.array_equal(outs[f].cpu().numpy(), ref), f
