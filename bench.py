@@ -300,8 +300,8 @@ def bench_config(args, lay, world=1):
             "l2": f"inputs larger than L2 (resident page pool up to {pool_mb:.0f} MB, "
                   f"126 MB L2; the frame's records stream from it every step)",
             "upload_mode": upload_mode_of(args),
-            "page_table": "device" if os.environ.get("VMSPLAT_DEVICE_TABLE", "0") == "1"
-            else "host"}
+            "page_table": "host" if os.environ.get("VMSPLAT_DEVICE_TABLE") == "0"
+            else "device (dpt_update_k) when capacity <= 8192, else host C++"}
 
 
 def measure_pcie(torch, nbytes=256 << 20, reps=10):

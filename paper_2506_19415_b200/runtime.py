@@ -308,6 +308,10 @@ class PageTable:
         return pp[:k].copy(), pl[:k].copy(), pe[:k].copy(), ps[:k].copy(), int(missing.value)
 
 
+DEVICE_TABLE_MAX_CAPACITY = 8192  # csrc/dpt.cu kMaxCap (entry metadata in shared memory)
+DEVICE_TABLE_MAX_LEVELS = 6        # <= 32 slots per entry
+
+
 class DevicePageTable:
     """The same table resident in device memory (SURVEY §8(f) F2,
     csrc/dpt.cu): ``update`` runs update_page_table's two passes on the GPU
@@ -620,10 +624,17 @@ class VmSession:
             d.m_cap = int(instance_capacity) if instance_capacity else 1 << 26
             # the page table on the device: the visibility
             # graph runs update_page_table too; the host only issues copies
-            if device_table is None:  # default: VMSPLAT_DEVICE_TABLE=1 selects it
+            if device_table is None:
+                # default: on the device whenever it fits its limits (measured
+                # faster: +3 % device fps, +5 % e2e on C2); VMSPLAT_DEVICE_TABLE
+                # = 0 / 1 forces the host C++ table / the device table
                 import os
 
-                device_table = os.environ.get("VMSPLAT_DEVICE_TABLE", "0") == "1"
+                env = os.environ.get("VMSPLAT_DEVICE_TABLE", "")
+                device_table = env == "1" if env in ("0", "1") else (
+                    self.capacity <= DEVICE_TABLE_MAX_CAPACITY and
+                    int(scene.lod_levels) <= DEVICE_TABLE_MAX_LEVELS and
+                    int(scene.page_count) < (1 << 30))
             d.device_table = int(bool(device_table))
             self.device_table = bool(device_table)
             self._desc = d
