@@ -25,11 +25,11 @@
  *  - Results are bit-exact with the reference for every integer/index output
  *    (page-ID images, required lists, plans, sort orders).  Images: exact
  *    mode (the default; FP64 blend arithmetic like the reference) is within
- *    1e-5 max-abs of the reference; fast mode (opt-in FP32 blend) is within
- *    PSNR >= 50 dB and 1e-2 max-abs - an FP32 exponent can move a pixel's
- *    transmittance across the 1/255 stop threshold one splat earlier or
- *    later, which changes that pixel by up to ~4e-3 (tests/test_gpu_parity.py
- *    checks both bounds).
+ *    1e-5 max-abs of the reference; fast mode (opt-in, certified FP32 blend)
+ *    is within 1e-3 max-abs: each pixel carries a running bound on its FP32
+ *    transmittance and colour error, and every pixel whose 1/255 stop
+ *    decision or colour (> 4e-4) the bound cannot certify is re-blended with
+ *    the exact FP64 arithmetic (tests/test_gpu_parity.py checks both).
  */
 #ifndef VMSPLAT_B200_H
 #define VMSPLAT_B200_H
@@ -172,6 +172,10 @@ int32_t vms_debug_blend_trace(void* dev_ptr);
 /* The exact blend's table-driven FP64 exp(x), x in [-700, 0], evaluated on
  * [dev] x -> [dev] out (accuracy test against libm; not on the hot path). */
 int32_t vms_debug_exp(const double* x, int64_t n, double* out, void* stream);
+/* Certified fast blend (exact = 0): on != 0 flags every pixel, so the whole
+ * image is re-blended by the FP64 repair kernel (tests: must equal exact
+ * mode). */
+int32_t vms_debug_cert_all(int32_t on);
 
 /* ---- kernel-level drop-ins (pkg/src/vmsplat/kernels/__init__.py) ------ */
 
@@ -408,6 +412,9 @@ typedef struct vms_dpt_stats {  /* [dev or mapped host] per-frame outputs */
 vms_dpt* vms_dpt_create(int32_t capacity, int32_t page_count, int32_t levels);
 /* The device table of a session created with device_table = 1 (else NULL). */
 vms_dpt* vms_session_dpt(vms_session* s);
+/* Pixels the last frame's certified fast blend re-blended in FP64
+ * (synchronises the device; exact = 0 sessions). */
+int32_t vms_session_cert_count(vms_session* s, uint32_t* out);
 void vms_dpt_destroy(vms_dpt* d);
 size_t vms_dpt_smem_bytes(const vms_dpt* d);
 /* update_page_table (runtime.py:294-346) on the device: the required list

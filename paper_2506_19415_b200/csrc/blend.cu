@@ -351,6 +351,12 @@ __constant__ double2 kExp2Tab[64];
 // take them as c[][] operands, where literals that do not fit an immediate
 // would be rematerialised with uniform moves on every pixel-splat.
 constexpr float kStopF = 0x1.010102p-8f;  // RN32(1/255) = smallest float >= 1/255
+// certified fast blend: the colour error an unflagged pixel may carry (the
+// contract is 1e-3 max-abs against the reference)
+constexpr float kCertTol = 4e-4f;
+// VMSPLAT_CERT_ALL=1: flag every pixel (tests re-blend the whole image in
+// FP64 through the repair kernel)
+__device__ int g_cert_all = 0;
 constexpr int kPairStep = 2;  // splats whose box tests and sigmas are evaluated together
 
 __constant__ double kBlendC[10] = {
@@ -424,7 +430,9 @@ __global__ void __launch_bounds__(kBlendThreads, kSparse ? 3 : 4) blend_k(const 
                                                          float* image_arg,
                                                          const FrameDev* __restrict__ fd,
                                                          int accumulate,
-                                                         const uint32_t* __restrict__ tile_hot) {
+                                                         const uint32_t* __restrict__ tile_hot,
+                                                         uint32_t* __restrict__ cert_cnt,
+                                                         uint4* __restrict__ cert_list) {
   pdl_wait();
   constexpr int SUB = TS / 16;  // sub-tiles per tile edge
   using Staged = typename std::conditional<kExact, SplatF64, BlendRec>::type;
@@ -460,6 +468,14 @@ __global__ void __launch_bounds__(kBlendThreads, kSparse ? 3 : 4) blend_k(const 
     cg = p[1];
     cb = p[2];
   }
+  // certified fast blend (kExact == false, cert_cnt set): E bounds the
+  // relative error of T against the reference's FP64 arithmetic, C the
+  // colour error; a pixel whose stop decision (T < 1/255) or colour the
+  // bounds cannot certify is re-blended in FP64 by blend_repair_k
+  const float cr0 = cr, cg0 = cg, cb0 = cb;
+  float certE = 0.f, certC = 0.f;
+  uint32_t certN = 0;
+  bool certFlag = false;
   const double fx = (double)px + 0.5, fy = (double)py + 0.5;
   for (uint32_t base = start; base < end; base += kBlendThreads) {
     if (__syncthreads_and(T < kStopF)) break;
@@ -682,17 +698,46 @@ __global__ void __launch_bounds__(kBlendThreads, kSparse ? 3 : 4) blend_k(const 
           const int x0 = s.bx & 0xFFFF, x1 = s.bx >> 16, y0 = s.by & 0xFFFF, y1 = s.by >> 16;
           if (px < x0 || px >= x1 || py < y0 || py >= y1) continue;
           const float dx = ((float)px + 0.5f) - s.cx, dy = ((float)py + 0.5f) - s.cy;
-          const float sig = -0.5f * (s.ca * dx * dx + 2.0f * s.cb * dy * dx + s.cc * dy * dy);
+          const float adx = s.ca * dx, bdy = s.cb * dy, cdy = s.cc * dy;
+          const float sig = -0.5f * __fmaf_rn(adx, dx, __fmaf_rn(2.0f * bdy, dx, cdy * dy));
           const float wgt = fminf(s.alpha * __expf(sig), 0.99f);
           const float wt = wgt * T;
-          cr += wt * s.r;
-          cg += wt * s.g;
-          cb += wt * s.b;
-          T = T * (1.0f - wgt);
+          cr = __fmaf_rn(wt, s.r, cr);
+          cg = __fmaf_rn(wt, s.g, cg);
+          cb = __fmaf_rn(wt, s.b, cb);
+          const float om = 1.0f - wgt;
+          T = T * om;
+          if (cert_cnt) {
+            // S = 0.5 (|a dx dx| + 2 |b dx dy| + |c dy dy|) bounds the terms of
+            // sigma: |sigma' - sigma| <= 16u S (dx, dy and the three roundings),
+            // __expf adds (4 + 2.4 |sigma'|) u, alpha * e and the 0.99f clamp
+            // (vs 0.99) 2u -> w is within epsw = (19 S + 6) u relative; T's
+            // relative error grows by epsw w / (1 - w) + 4u per step
+            const float S = 0.5f * __fmaf_rn(fabsf(adx), fabsf(dx),
+                                             __fmaf_rn(2.0f * fabsf(bdy), fabsf(dx),
+                                                       fabsf(cdy * dy)));
+            const float epsw = __fmaf_rn(S, 19.0f * 0x1p-24f, 6.0f * 0x1p-24f);
+            certC = __fmaf_rn(wt * fmaxf(s.r, fmaxf(s.g, s.b)), epsw + certE + 0x1p-22f, certC);
+            certE = __fdividef(epsw * wgt * 1.02f, om) + (certE + 4.0f * 0x1p-24f);
+            ++certN;
+            // the next stop test could go the other way
+            certFlag |= fabsf(T - kStopF) <= 1.02f * certE * T + 0x1p-40f;
+          }
         }
       }
     }
     __syncthreads();
+  }
+  if (cert_cnt && inside) {
+    // colour: the accumulated bound plus one f32 ulp per step of the final
+    // value (colours are >= 0, so every partial sum is below it)
+    const float cm = fmaxf(cr, fmaxf(cg, cb));
+    certFlag |= __fmaf_rn((float)certN * 0x1p-23f, cm, certC) > kCertTol;
+    if (certFlag || g_cert_all) {
+      const uint32_t k = atomicAdd(cert_cnt, 1u);
+      cert_list[k] = make_uint4((uint32_t)(py * w + px), __float_as_uint(cr0),
+                                __float_as_uint(cg0), __float_as_uint(cb0));
+    }
   }
   // output: the 16x16 block goes through shared memory and out as whole
   // rows of 16-byte stores (coalesced; with a zero-copy host image these are
@@ -729,6 +774,91 @@ __global__ void __launch_bounds__(kBlendThreads, kSparse ? 3 : 4) blend_k(const 
       o[2] = smid;
       o[3] = ((unsigned long long)(end - start) << 32) | (uint32_t)tile;
       o[4] = o[5] = o[6] = o[7] = 0;
+    }
+  }
+}
+
+// Certified fast blend, second half: every pixel the FP32 blend could not
+// certify is re-blended from its initial colour with the exact kernel's
+// FP64 arithmetic (the same staged values, sigma order, exp, skip and stop
+// rules, in list order - so the pixel equals the exact blend's).  One warp
+// per flagged pixel: the lanes take 32 list entries at a time (box test,
+// sigma and weight in parallel), then every lane applies the live ones in
+// list order to its own copy of the pixel state (broadcast by shuffles),
+// until T < 1/255.
+template <int TS>
+__global__ void __launch_bounds__(kBlendThreads) blend_repair_k(
+    const uint32_t* __restrict__ ranges, const uint32_t* __restrict__ tv_tiles,
+    const uint32_t* __restrict__ vals, const RenderCounters* __restrict__ ctr,
+    const BlendRec* __restrict__ rec, int w, int tiles_x, float* image_arg,
+    const FrameDev* __restrict__ fd, const uint32_t* __restrict__ cert_cnt,
+    const uint4* __restrict__ cert_list) {
+  pdl_wait();
+  __shared__ double2 tab[64];
+  if (threadIdx.x < 64) tab[threadIdx.x] = kExp2Tab[threadIdx.x];
+  __syncthreads();
+  const uint32_t n = *cert_cnt;
+  const int lane = threadIdx.x & 31;
+  const uint32_t warps = gridDim.x * (kBlendThreads / 32);
+  float* __restrict__ image = image_arg ? image_arg : fd->image;
+  const bool spill = ctr->overflow != 0u;
+  for (uint32_t k = blockIdx.x * (kBlendThreads / 32) + (threadIdx.x >> 5); k < n; k += warps) {
+    const uint4 e = cert_list[k];
+    const int px = (int)(e.x % (uint32_t)w), py = (int)(e.x / (uint32_t)w);
+    const int tile = (py / TS) * tiles_x + px / TS;
+    const uint32_t start = spill ? 0u : ranges[2 * tile];
+    const uint32_t end = spill ? ctr->n_kept : ranges[2 * tile + 1];
+    const uint32_t* __restrict__ tv = spill ? vals : tv_tiles;
+    float cr = __uint_as_float(e.y), cg = __uint_as_float(e.z), cb = __uint_as_float(e.w);
+    float T = 1.f;
+    const double fx = (double)px + 0.5, fy = (double)py + 0.5;
+    for (uint32_t base = start; base < end && T >= kStopF; base += 32) {
+      const uint32_t i = base + lane;
+      bool live = false;
+      double wk = 0.0;
+      float r = 0.f, g = 0.f, b = 0.f;
+      if (i < end) {
+        const BlendRec q = rec[tv[i]];
+        const int x0 = q.bx & 0xFFFF, x1 = q.bx >> 16, y0 = q.by & 0xFFFF, y1 = q.by >> 16;
+        if (px >= x0 && px < x1 && py >= y0 && py < y1) {
+          // blend_k<exact>'s staging (-0.5 folded into the conic) and sigma
+          const double ca = -0.5 * (double)q.ca, cb2 = -(double)q.cb, cc = -0.5 * (double)q.cc;
+          const double dx = __dsub_rn(fx, (double)q.cx);
+          const double dy = __dsub_rn(fy, (double)q.cy);
+          const double sg = __dadd_rn(__dadd_rn(__dmul_rn(__dmul_rn(ca, dx), dx),
+                                                __dmul_rn(__dmul_rn(cb2, dy), dx)),
+                                      __dmul_rn(__dmul_rn(cc, dy), dy));
+          if (sg >= (double)q.skip) {
+            live = true;
+            wk = __dmul_rn((double)q.alpha, exp_tab(sg, tab));
+            if (wk > kBlendC[8]) wk = kBlendC[8];
+            r = q.r;
+            g = q.g;
+            b = q.b;
+          }
+        }
+      }
+      uint32_t m = __ballot_sync(0xffffffffu, live);
+      while (m && T >= kStopF) {
+        const int j = __ffs(m) - 1;
+        m &= m - 1;
+        const double wgt = __shfl_sync(0xffffffffu, wk, j);
+        const double rr = (double)__shfl_sync(0xffffffffu, r, j);
+        const double gg = (double)__shfl_sync(0xffffffffu, g, j);
+        const double bb = (double)__shfl_sync(0xffffffffu, b, j);
+        const double t = (double)T;
+        const double wt = __dmul_rn(wgt, t);
+        cr = __double2float_rn(__dadd_rn((double)cr, __dmul_rn(wt, rr)));
+        cg = __double2float_rn(__dadd_rn((double)cg, __dmul_rn(wt, gg)));
+        cb = __double2float_rn(__dadd_rn((double)cb, __dmul_rn(wt, bb)));
+        T = __double2float_rn(__dmul_rn(t, __dsub_rn(1.0, wgt)));
+      }
+    }
+    if (lane == 0) {
+      float* p = image + ((size_t)py * w + px) * 3;
+      p[0] = cr;
+      p[1] = cg;
+      p[2] = cb;
     }
   }
 }
@@ -1086,14 +1216,26 @@ int32_t launch_band(int width, int height, const uint32_t* vals, const RenderWs&
         accumulate);
     VMS_CUDA(cudaEventRecord(hs.join, hs.side));
   }
+  // fast (FP32) blend: certified, with the FP64 re-blend of the pixels it
+  // flags; each band's flags go to the band's own segment of the list
+  uint32_t* cert_cnt = exact ? nullptr : w.cert + band;
+  uint4* cert_list = exact ? nullptr : w.cert_list + (size_t)r0 * ts * width;
   if (count)
     VMS_CUDA(launch(kern, count * subs, kBlendThreads, dsmem, s, (const uint32_t*)w.ranges,
                     (const uint32_t*)w.order, sorted_tiles(w, n_tiles), vals,
                     (const RenderCounters*)w.ctr, (const BlendRec*)w.rec, width, height, tiles_x,
                     first, image, (const FrameDev*)w.fd, accumulate,
-                    (const uint32_t*)(hot ? w.tile_hot : nullptr)));
+                    (const uint32_t*)(hot ? w.tile_hot : nullptr), cert_cnt, cert_list));
   mark("blend", s);
   if (hot) VMS_CUDA(cudaStreamWaitEvent(s, hs.join, 0));
+  if (!exact && count) {
+    auto* rk = ts == 16 ? blend_repair_k<16> : blend_repair_k<32>;
+    VMS_CUDA(launch(rk, 2 * kSMs, kBlendThreads, 0, s, (const uint32_t*)w.ranges,
+                    sorted_tiles(w, n_tiles), vals, (const RenderCounters*)w.ctr,
+                    (const BlendRec*)w.rec, width, tiles_x, image, (const FrameDev*)w.fd,
+                    (const uint32_t*)cert_cnt, (const uint4*)cert_list));
+    mark("blend_repair", s);
+  }
   VMS_LAUNCH_CHECK("blend");
   return VMS_OK;
 }
@@ -1186,6 +1328,11 @@ int32_t blend_init() {
     t[j].y = (double)(v - (long double)t[j].x);
   }
   VMS_CUDA(cudaMemcpyToSymbol(kExp2Tab, t, sizeof(t)));
+  {
+    const char* e = getenv("VMSPLAT_CERT_ALL");
+    const int all = e && e[0] == '1' ? 1 : 0;
+    VMS_CUDA(cudaMemcpyToSymbol(g_cert_all, &all, sizeof(int)));
+  }
   for (const void* f : {(const void*)blend_k<true, 16, true>, (const void*)blend_k<true, 32, true>})
     VMS_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)kSparseSmem));
@@ -1206,6 +1353,23 @@ int32_t debug_exp(const double* x, uint64_t n, double* out, cudaStream_t s) {
   return VMS_OK;
 }
 
+int32_t debug_cert_all(int on) {
+  if (const int32_t rc = blend_init()) return rc;
+  const int v = on ? 1 : 0;
+  VMS_CUDA(cudaMemcpyToSymbol(g_cert_all, &v, sizeof(int)));
+  return VMS_OK;
+}
+
+int32_t debug_cert_count(const RenderWs& w, uint32_t* out) {
+  uint32_t c[16];
+  VMS_CUDA(cudaDeviceSynchronize());
+  VMS_CUDA(cudaMemcpy(c, w.cert, sizeof(c), cudaMemcpyDeviceToHost));
+  uint32_t t = 0;
+  for (int b = 0; b < kMaxBands; ++b) t += c[b];
+  *out = t;
+  return VMS_OK;
+}
+
 int32_t debug_blend_trace(void* dev_ptr) {
   unsigned long long* p = static_cast<unsigned long long*>(dev_ptr);
   VMS_CUDA(cudaMemcpyToSymbol(g_blend_trace, &p, sizeof(p)));
@@ -1223,6 +1387,7 @@ size_t render_ws_bytes(uint32_t n_cap, uint32_t m_cap, uint32_t n_tiles) {
   b += sizeof(uint32_t) * 3 * (size_t)n_tiles; // ranges + order
   b += sizeof(uint32_t) * (kMaxHot + 1 + (size_t)n_tiles);  // hot list + flags
   b += sizeof(RenderCounters) + sizeof(FrameDev);
+  b += sizeof(uint32_t) * 16 + sizeof(uint4) * (size_t)n_tiles * tile_size() * tile_size();
   b += 2 * scan_ws_bytes(n_cap) + radix_ws_bytes(n_cap > m_cap ? n_cap : m_cap);
   return b + 256 * 26;
 }
@@ -1255,6 +1420,8 @@ RenderWs render_carve(void* ws, uint32_t n_cap, uint32_t m_cap, uint32_t n_tiles
   w.tile_hot = carve<uint32_t>(p, (size_t)n_tiles);
   w.ctr = carve<RenderCounters>(p, 1);
   w.fd = carve<FrameDev>(p, 1);
+  w.cert = carve<uint32_t>(p, 16);
+  w.cert_list = carve<uint4>(p, (size_t)n_tiles * tile_size() * tile_size());
   w.scan_ws = carve<char>(p, scan_ws_bytes(n_cap));
   w.scan_ws2 = carve<char>(p, scan_ws_bytes(n_cap));
   w.radix_ws = carve<char>(p, radix_ws_bytes(n_cap > m_cap ? n_cap : m_cap));
@@ -1275,6 +1442,7 @@ int32_t render_clear(int width, int height, const RenderWs& w, cudaStream_t s) {
   const int ts = tile_size();
   const size_t cells = (size_t)(ceil_div(width, ts) + 1) * (ceil_div(height, ts) + 1);
   VMS_CUDA(cudaMemsetAsync(w.ctr, 0, sizeof(RenderCounters), s));
+  VMS_CUDA(cudaMemsetAsync(w.cert, 0, sizeof(uint32_t) * 16, s));
   VMS_CUDA(cudaMemsetAsync(w.scan_ws, 0, scan_ws_bytes(w.n_cap), s));
   VMS_CUDA(cudaMemsetAsync(w.scan_ws2, 0, scan_ws_bytes(w.n_cap), s));
   VMS_CUDA(cudaMemsetAsync(w.radix_ws, 0, radix_clear_bytes(), s));
@@ -1312,6 +1480,7 @@ int32_t composite_ordered(const float* centers, const float* conics, const float
                           int h, int w, int exact, const RenderWs& ws, cudaStream_t s) {
   const int T = 256;
   VMS_CUDA(cudaMemsetAsync(ws.ctr, 0, sizeof(RenderCounters), s));
+  VMS_CUDA(cudaMemsetAsync(ws.cert, 0, sizeof(uint32_t) * 16, s));
   if (n) {
     // splats with an empty clamped box are dropped; the rest keep their order
     pack_ordered_k<<<ceil_div<uint32_t>(n, T), T, 0, s>>>(centers, conics, colors, alphas, bounds,

@@ -75,6 +75,8 @@ struct RenderWs {
   uint32_t* order;   // blend schedule: tiles, longest list first
   uint32_t* hot;     // [0] hot tiles this frame, [1..] their ids (blend_hot_k)
   uint32_t* tile_hot;  // per tile: 1 if blend_hot_k owns it
+  uint32_t* cert;      // certified fast blend: flagged-pixel count per band
+  uint4* cert_list;    // {pixel, initial r, g, b bits} per flagged pixel, by band
   RenderCounters* ctr;
   FrameDev* fd;
   void* scan_ws;
@@ -115,6 +117,10 @@ int32_t preprocess_init();
 // Per-CTA blend timing trace (profiling only; nullptr disables).
 int32_t debug_blend_trace(void* dev_ptr);
 int32_t debug_exp(const double* x, uint64_t n, double* out, cudaStream_t s);
+// Certified fast blend: flag every pixel (tests); pixels flagged by the
+// last blend (synchronises the device).
+int32_t debug_cert_all(int on);
+int32_t debug_cert_count(const RenderWs& w, uint32_t* out);
 
 // Zero the frame's counters and primitive workspaces (all memsets of a
 // frame, ahead of its first kernel); render_finish assumes it ran.

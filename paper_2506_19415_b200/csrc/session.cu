@@ -553,6 +553,16 @@ vms_pagetable* vms_session_table(vms_session* s) { return s ? s->pt : nullptr; }
 
 vms_dpt* vms_session_dpt(vms_session* s) { return s ? s->dpt : nullptr; }
 
+int32_t vms_session_cert_count(vms_session* s, uint32_t* out) {
+  if (!s || !out || !s->ws) {
+    set_error("session_cert_count: invalid arguments");
+    return VMS_ERR_INVALID;
+  }
+  RenderWs ws = render_carve(s->ws, s->d.capacity * s->d.page_size, s->m_cap,
+                             tile_count(s->ws_w, s->ws_h));
+  return debug_cert_count(ws, out);
+}
+
 int32_t vms_session_set_render_ws(vms_session* s, void* ws, uint64_t bytes, uint32_t m_cap,
                                   int32_t width, int32_t height) {
   // the session owns its scratch; this only raises the instance capacity

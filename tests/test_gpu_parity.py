@@ -4,10 +4,9 @@ the reference's golden vectors.
 Tolerances (north star): integer/index outputs — page-ID images, depths,
 required lists, plans, residency, sort orders, stats.csv — bit-exact;
 images max-abs <= 1e-5 in exact (FP64 blend, the default) mode.  The opt-in
-fast (FP32 blend) mode is held to <= 1e-3 on the kernel-level cases and to
-PSNR >= 50 dB with max-abs <= 1e-2 on whole sessions (an FP32 exponent can
-move a pixel across the 1/255 stop threshold one splat earlier or later;
-include/vmsplat_b200.h states the same bound).
+fast mode (certified FP32 blend: pixels whose stop decision or colour its
+error bound cannot certify are re-blended in FP64) is held to the north
+star's max-abs <= 1e-3 (PSNR >= 50 dB) everywhere.
 """
 
 import hashlib
@@ -277,9 +276,8 @@ def test_session_matches_reference(cuda, golden, variant, exact):
         ref = g[f"{variant}_image_{f}"]
         if exact:  # the default, reference-faithful blend
             assert _maxabs(img, ref) <= EXACT_TOL, f
-        else:  # opt-in FP32 blend: an early-termination flip may exceed 1e-3 in
-            # isolated pixels
-            assert core.psnr(img, ref) >= 50.0 and _maxabs(img, ref) <= 1e-2, f
+        else:  # opt-in certified FP32 blend
+            assert core.psnr(img, ref) >= 50.0 and _maxabs(img, ref) <= FAST_TOL, f
         s.table.check()
     assert core.stats_csv(stats).encode() == g[f"{variant}_stats"].tobytes()
 
@@ -631,3 +629,69 @@ def test_session_frame_with_nothing_visible(cuda):
     ref, rst = cpu.render_frame(away, 4)
     assert st["required_pages"] == 0 and st["bytes_copied"] == 0
     assert _maxabs(img, ref) <= EXACT_TOL
+
+
+# -- certified fast blend ---------------------------------------------------------
+
+def test_certified_repair_reproduces_exact_blend(cuda):
+    """With every pixel flagged (vms_debug_cert_all), the fast blend's FP64
+    repair re-blends the whole image: it must equal the exact blend bit for
+    bit - sessions (initial colour 0) and composite_splats (in-place blend
+    onto the caller's image)."""
+    from paper_2506_19415_b200 import _lib, kernels
+    from paper_2506_19415_b200.runtime import VmSession
+
+    lib = _lib.load()
+    sc = _city()
+    path = inputs.city_path(inputs.CITY_SMALL)
+    _lib.check(lib.vms_debug_cert_all(1), "cert_all")
+    try:
+        fast = VmSession(sc, buffer_pages=16, staging_pages=6.0, vis_scale=0.5, exact=False)
+        ex = VmSession(sc, buffer_pages=16, staging_pages=6.0, vis_scale=0.5, exact=True)
+        for f in range(path.frame_count):
+            a, _ = fast.render_frame(path.frame_camera(f), f)
+            n = np.zeros(1, np.uint32)
+            _lib.check(lib.vms_session_cert_count(fast._h, n.ctypes.data), "cert_count")
+            assert int(n[0]) == a.shape[0] * a.shape[1], f
+            b, _ = ex.render_frame(path.frame_camera(f), f)
+            assert np.array_equal(a, b), f
+        for seed in (0, 1, 2):
+            args = inputs.random_splats(seed, 400, 64, 48)
+            base = np.random.default_rng(seed).random((48, 64, 3)).astype(np.float32)
+            x, y = base.copy(), base.copy()
+            kernels.composite_splats(*args, x, exact=False)
+            kernels.composite_splats(*args, y, exact=True)
+            assert np.array_equal(x, y), seed
+    finally:
+        _lib.check(lib.vms_debug_cert_all(0), "cert_all")
+
+
+def test_certified_fast_blend_c2_within_contract(cuda, c2_scene):
+    """The certified fast blend on the C2 benchmark frames (5-34, including
+    the vanishing-point frames) and every 8th frame: max-abs <= 1e-3 against
+    the oracle, and the repair really runs (some pixels flagged)."""
+    from paper_2506_19415_b200 import _lib, scenegen
+    from paper_2506_19415_b200.runtime import VmSession
+
+    lib = _lib.load()
+    traj = scenegen.street_path(scenegen.C2, frames=120)
+    s = VmSession(c2_scene, exact=False)
+    o = core.OSession(c2_scene)
+    frames = sorted(set(range(0, 35)) | set(range(0, 120, 8)))
+    worst, flagged = 0.0, []
+    for f in range(max(frames) + 1):
+        cam = traj.frame_camera(f)
+        want = f in frames
+        img, st = s.render_frame(cam, f, out=None if want else "device")
+        ref, rst = o.render_frame(cam, f, want_image=want)
+        assert st["required_pages"] == rst["required_pages"], f
+        if want:
+            n = np.zeros(1, np.uint32)
+            _lib.check(lib.vms_session_cert_count(s._h, n.ctypes.data), "cert_count")
+            flagged.append(int(n[0]))
+            err = _maxabs(img, ref)
+            assert err <= FAST_TOL, (f, err)
+            worst = max(worst, err)
+    print(f"certified fast blend: worst max-abs {worst:.2e}; flagged pixels per frame "
+          f"min {min(flagged)} median {int(np.median(flagged))} max {max(flagged)}")
+    assert max(flagged) > 0
