@@ -28,7 +28,7 @@
  *    1e-5 max-abs of the reference; fast mode (opt-in, certified FP32 blend)
  *    is within 1e-3 max-abs: each pixel carries a running bound on its FP32
  *    transmittance and colour error, and every pixel whose 1/255 stop
- *    decision or colour (> 4e-4) the bound cannot certify is re-blended with
+ *    decision or colour (> 9e-4) the bound cannot certify is re-blended with
  *    the exact FP64 arithmetic (tests/test_gpu_parity.py checks both).
  */
 #ifndef VMSPLAT_B200_H

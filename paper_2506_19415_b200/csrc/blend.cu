@@ -19,6 +19,7 @@
 // SURVEY A16); exact mode reproduces the reference's FP64 arithmetic with
 // f32 storage of T and colour.
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <type_traits>
 
@@ -353,10 +354,11 @@ __constant__ double2 kExp2Tab[64];
 constexpr float kStopF = 0x1.010102p-8f;  // RN32(1/255) = smallest float >= 1/255
 // certified fast blend: the colour error an unflagged pixel may carry (the
 // contract is 1e-3 max-abs against the reference)
-constexpr float kCertTol = 4e-4f;
+constexpr float kCertTol = 9e-4f;
 // VMSPLAT_CERT_ALL=1: flag every pixel (tests re-blend the whole image in
 // FP64 through the repair kernel)
 __device__ int g_cert_all = 0;
+__device__ uint32_t g_cert_why[4];
 constexpr int kPairStep = 2;  // splats whose box tests and sigmas are evaluated together
 
 __constant__ double kBlendC[10] = {
@@ -699,7 +701,25 @@ __global__ void __launch_bounds__(kBlendThreads, kSparse ? 3 : 4) blend_k(const 
           if (px < x0 || px >= x1 || py < y0 || py >= y1) continue;
           const float dx = ((float)px + 0.5f) - s.cx, dy = ((float)py + 0.5f) - s.cy;
           const float adx = s.ca * dx, bdy = s.cb * dy, cdy = s.cc * dy;
-          const float sig = -0.5f * __fmaf_rn(adx, dx, __fmaf_rn(2.0f * bdy, dx, cdy * dy));
+          float sig = -0.5f * __fmaf_rn(adx, dx, __fmaf_rn(2.0f * bdy, dx, cdy * dy));
+          // S = 0.5 (|a dx dx| + 2 |b dx dy| + |c dy dy|): the size of sigma's
+          // terms, which bounds its FP32 rounding error
+          float S = 0.f;
+          if (cert_cnt) {
+            S = 0.5f * __fmaf_rn(fabsf(adx), fabsf(dx),
+                                 __fmaf_rn(2.0f * fabsf(bdy), fabsf(dx), fabsf(cdy * dy)));
+            if (S > 256.f) {
+              // ill-conditioned conic (terms >> sigma: FP32 cancels): sigma
+              // in FP64 as the reference evaluates it, then rounded once
+              const double ddx = ((double)px + 0.5) - (double)s.cx;
+              const double ddy = ((double)py + 0.5) - (double)s.cy;
+              const double q = __dadd_rn(__dadd_rn(__dmul_rn(__dmul_rn((double)s.ca, ddx), ddx),
+                                                   __dmul_rn(__dmul_rn(2.0 * (double)s.cb, ddy), ddx)),
+                                         __dmul_rn(__dmul_rn((double)s.cc, ddy), ddy));
+              sig = (float)(-0.5 * q);
+              S = fabsf(sig) + 1.0f;  // one f32 rounding of sigma instead of 4u S
+            }
+          }
           const float wgt = fminf(s.alpha * __expf(sig), 0.99f);
           const float wt = wgt * T;
           cr = __fmaf_rn(wt, s.r, cr);
@@ -709,14 +729,13 @@ __global__ void __launch_bounds__(kBlendThreads, kSparse ? 3 : 4) blend_k(const 
           T = T * om;
           if (cert_cnt) {
             // S = 0.5 (|a dx dx| + 2 |b dx dy| + |c dy dy|) bounds the terms of
-            // sigma: |sigma' - sigma| <= 16u S (dx, dy and the three roundings),
-            // __expf adds (4 + 2.4 |sigma'|) u, alpha * e and the 0.99f clamp
-            // (vs 0.99) 2u -> w is within epsw = (19 S + 6) u relative; T's
-            // relative error grows by epsw w / (1 - w) + 4u per step
-            const float S = 0.5f * __fmaf_rn(fabsf(adx), fabsf(dx),
-                                             __fmaf_rn(2.0f * fabsf(bdy), fabsf(dx),
-                                                       fabsf(cdy * dy)));
-            const float epsw = __fmaf_rn(S, 19.0f * 0x1p-24f, 6.0f * 0x1p-24f);
+            // sigma: dx, dy are exact (Sterbenz: pixel centre and splat centre
+            // within a factor of 2, |dx| < 2^12), the products and the two
+            // fused sums round: |sigma' - sigma| <= 4u S; __expf adds
+            // (4 + 2.4 |sigma'|) u, alpha * e and the 0.99f clamp (vs 0.99)
+            // 2u -> w is within epsw = (8 S + 8) u relative (margin kept);
+            // T's relative error grows by epsw w / (1 - w) + 4u per step
+            const float epsw = __fmaf_rn(S, 8.0f * 0x1p-24f, 8.0f * 0x1p-24f);
             certC = __fmaf_rn(wt * fmaxf(s.r, fmaxf(s.g, s.b)), epsw + certE + 0x1p-22f, certC);
             certE = __fdividef(epsw * wgt * 1.02f, om) + (certE + 4.0f * 0x1p-24f);
             ++certN;
@@ -732,8 +751,15 @@ __global__ void __launch_bounds__(kBlendThreads, kSparse ? 3 : 4) blend_k(const 
     // colour: the accumulated bound plus one f32 ulp per step of the final
     // value (colours are >= 0, so every partial sum is below it)
     const float cm = fmaxf(cr, fmaxf(cg, cb));
-    certFlag |= __fmaf_rn((float)certN * 0x1p-23f, cm, certC) > kCertTol;
-    if (certFlag || g_cert_all) {
+    const bool colour = __fmaf_rn((float)certN * 0x1p-23f, cm, certC) > kCertTol;
+    if (g_cert_all > 1) {  // diagnostics (VMSPLAT_CERT_ALL=2): flag reasons
+      if (certFlag) atomicAdd(&g_cert_why[0], 1u);
+      if (colour) atomicAdd(&g_cert_why[1], 1u);
+      if (certN > 2000) atomicAdd(&g_cert_why[2], 1u);
+      if (certE > 1e-3f) atomicAdd(&g_cert_why[3], 1u);
+    }
+    certFlag |= colour;
+    if (certFlag || g_cert_all == 1) {
       const uint32_t k = atomicAdd(cert_cnt, 1u);
       cert_list[k] = make_uint4((uint32_t)(py * w + px), __float_as_uint(cr0),
                                 __float_as_uint(cg0), __float_as_uint(cb0));
@@ -812,13 +838,18 @@ __global__ void __launch_bounds__(kBlendThreads) blend_repair_k(
     float cr = __uint_as_float(e.y), cg = __uint_as_float(e.z), cb = __uint_as_float(e.w);
     float T = 1.f;
     const double fx = (double)px + 0.5, fy = (double)py + 0.5;
+    // the next chunk's records are in flight while this chunk is evaluated
+    BlendRec nq;
+    if (start + lane < end) nq = rec[tv[start + lane]];
     for (uint32_t base = start; base < end && T >= kStopF; base += 32) {
       const uint32_t i = base + lane;
       bool live = false;
       double wk = 0.0;
       float r = 0.f, g = 0.f, b = 0.f;
+      const BlendRec cq = nq;
+      if (base + 32 + lane < end) nq = rec[tv[base + 32 + lane]];
       if (i < end) {
-        const BlendRec q = rec[tv[i]];
+        const BlendRec q = cq;
         const int x0 = q.bx & 0xFFFF, x1 = q.bx >> 16, y0 = q.by & 0xFFFF, y1 = q.by >> 16;
         if (px >= x0 && px < x1 && py >= y0 && py < y1) {
           // blend_k<exact>'s staging (-0.5 folded into the conic) and sigma
@@ -1330,7 +1361,7 @@ int32_t blend_init() {
   VMS_CUDA(cudaMemcpyToSymbol(kExp2Tab, t, sizeof(t)));
   {
     const char* e = getenv("VMSPLAT_CERT_ALL");
-    const int all = e && e[0] == '1' ? 1 : 0;
+    const int all = e && *e ? atoi(e) : 0;
     VMS_CUDA(cudaMemcpyToSymbol(g_cert_all, &all, sizeof(int)));
   }
   for (const void* f : {(const void*)blend_k<true, 16, true>, (const void*)blend_k<true, 32, true>})
@@ -1367,6 +1398,14 @@ int32_t debug_cert_count(const RenderWs& w, uint32_t* out) {
   uint32_t t = 0;
   for (int b = 0; b < kMaxBands; ++b) t += c[b];
   *out = t;
+  uint32_t why[4];
+  VMS_CUDA(cudaMemcpyFromSymbol(why, g_cert_why, sizeof(why)));
+  if (why[0] | why[1] | why[2] | why[3]) {
+    fprintf(stderr, "[cert] flagged %u: stop band %u, colour %u, >2000 steps %u, E>1e-3 %u\n", t,
+            why[0], why[1], why[2], why[3]);
+    const uint32_t z[4] = {0, 0, 0, 0};
+    VMS_CUDA(cudaMemcpyToSymbol(g_cert_why, z, sizeof(z)));
+  }
   return VMS_OK;
 }
 
