@@ -267,8 +267,8 @@ def launches_per_frame(stats, n_faces, upload_mode, n_pages=1000, device_table=F
                          chunk count, scan, merge)                       +10
       page copies       scatter_k (the uploads are copy-engine DMA;
                         upload_mode 1 adds the upload_k gather kernel)   1
-                        (the device page table: dpt_update_k and
-                         dpt_chunks_k in the same graph)                 +2
+                        (the device page table: dpt_update_k and the
+                         chunk-table sums / scan / emit kernels)         +4
       render graph      preprocess, scan, compact, radix hist + 4 passes,
                         dup_count, scan, dup_emit, tile_prep, 2 radix
                         passes, blend                                    16
@@ -282,7 +282,7 @@ def launches_per_frame(stats, n_faces, upload_mode, n_pages=1000, device_table=F
     if stats["planned_copies"]:
         up = 2 if upload_mode == 1 else 1
     if device_table:
-        vis += 2
+        vis += 4
     render = 16 + (2 if exact else 1)
     return vis + up + render
 

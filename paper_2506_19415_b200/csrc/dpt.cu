@@ -23,9 +23,10 @@
 //                          (untouched entries keep their order, the entries
 //                          touched this frame follow in index order - they
 //                          all carry this frame's stamp), state write-back
-// A second CTA-wide kernel (dpt_chunks_k) builds the chunk table of every
-// resident page in ascending page id (the reference's gather order,
-// runtime.py:377-390) for the render.
+// Three small kernels (dpt_chunk_sums_k, dpt_chunk_scan_k,
+// dpt_chunk_emit_k: block sums, their scan, the emit) build the chunk table
+// of every resident page in ascending page id (the reference's gather
+// order, runtime.py:377-390) for the render.
 //
 // The entry metadata (level, occupancy, free-slot mask) and the bitmaps live
 // in shared memory during the update: capacity <= 8192 entries and <= 6 LOD
@@ -47,9 +48,10 @@ struct vms_dpt {
   uint32_t* bm;      // [(L + 1) * W]: open bitmaps per level, then the empty bitmap
   int32_t* lru[2];   // entries in (last used, index) order; [cur] is current
   int32_t* cur;      // [1] device: which lru buffer is current
-  uint64_t* skeys;   // [P + 1] sort spill (more than kSortSmem required pages)
+  uint64_t* skeys;   // [P + 1] sort spill (more required pages than fit in shared memory)
   uint32_t* svals;
   int32_t* counts;   // [2 + 16]: occupied entries, resident pages, resident per level
+  uint2* csums;      // chunk table: per 2048-page block (records, chunks), then their bases
   void* base;
 };
 
@@ -58,7 +60,6 @@ namespace {
 
 constexpr uint32_t kNone = 0xFFFFFFFFu;
 constexpr int kThreads = 1024;
-constexpr int kSortSmem = 8192;  // required pages sorted in shared memory
 constexpr int kMaxCap = 8192;
 constexpr int kMaxLevels = 6;
 constexpr uint64_t kNoKey = ~0ull;
@@ -92,6 +93,7 @@ struct DptArgs {
   int32_t* plan_slot;
   int64_t plan_cap;
   vms_dpt_stats* stats;
+  int sort_cap;  // work items sorted in shared memory (a power of two)
 };
 
 struct Bits {
@@ -150,8 +152,8 @@ __global__ void __launch_bounds__(kThreads, 1) dpt_update_k(DptArgs a) {
   __shared__ int s_per[16];
   const int C = a.C, L = a.L, W = a.W, WS = a.WS, tid = threadIdx.x, NT = blockDim.x;
   uint64_t* keys = reinterpret_cast<uint64_t*>(smem);
-  uint32_t* vals = reinterpret_cast<uint32_t*>(keys + kSortSmem);
-  uint32_t* freem = vals + kSortSmem;
+  uint32_t* vals = reinterpret_cast<uint32_t*>(keys + a.sort_cap);
+  uint32_t* freem = vals + a.sort_cap;
   uint32_t* bw = freem + C;               // (L + 2) * W: open[L], empty, prot
   uint32_t* bs = bw + (L + 2) * W;        // (L + 2) * WS summaries
   int8_t* level = reinterpret_cast<int8_t*>(bs + (L + 2) * WS);
@@ -183,11 +185,11 @@ __global__ void __launch_bounds__(kThreads, 1) dpt_update_k(DptArgs a) {
   __syncthreads();
   Bits open[kMaxLevels], empty{bw + L * W, bs + L * WS}, prot{bw + (L + 1) * W, bs + (L + 1) * WS};
   for (int k = 0; k < L; ++k) open[k] = Bits{bw + k * W, bs + k * WS};
-  // pass 1 (runtime.py:312-327): keys in shared memory up to kSortSmem pages
+  // pass 1 (runtime.py:312-327): keys in shared memory up to sort_cap pages
   int N = 1;
   while (N < n) N <<= 1;
-  uint64_t* K = N <= kSortSmem ? keys : a.skeys;
-  uint32_t* V = N <= kSortSmem ? vals : a.svals;
+  uint64_t* K = N <= a.sort_cap ? keys : a.skeys;
+  uint32_t* V = N <= a.sort_cap ? vals : a.svals;
   for (int i = tid; i < N; i += NT) {
     uint64_t key = kNoKey;
     if (i < n) {
@@ -371,46 +373,95 @@ __global__ void __launch_bounds__(kThreads, 1) dpt_update_k(DptArgs a) {
   }
 }
 
-// chunk table of the resident pages, ascending page id (runtime.py:377-390)
-__global__ void __launch_bounds__(kThreads, 1) dpt_chunks_k(const uint32_t* __restrict__ res,
-                                                         const int8_t* __restrict__ level,
-                                                         int32_t P, uint32_t page_size,
-                                                         vms_chunk* __restrict__ out,
-                                                         int64_t cap, vms_dpt_stats* st) {
+// chunk table of the resident pages, ascending page id (runtime.py:377-390):
+// per-block sums of records and chunks over 2048-page blocks, a scan of the
+// block sums, then every block emits its pages' chunks from its base
+constexpr int kChunkThreads = 256;
+constexpr int kChunkPages = 8;  // pages per thread
+constexpr int kChunkBlock = kChunkThreads * kChunkPages;
+constexpr uint32_t kChunkRecs = 128;
+
+__device__ __forceinline__ void page_chunks(const uint32_t* res, const int8_t* level, int p,
+                                            uint32_t page_size, uint32_t& r, uint32_t& c) {
+  const uint32_t loc = res[p];
+  r = loc == kNone ? 0u : page_size >> level[loc >> 8];
+  c = (r + kChunkRecs - 1) / kChunkRecs;
+}
+
+__global__ void __launch_bounds__(kChunkThreads) dpt_chunk_sums_k(
+    const uint32_t* __restrict__ res, const int8_t* __restrict__ level, int32_t P,
+    uint32_t page_size, uint2* __restrict__ sums) {
   pdl_wait();
   __shared__ int warp_tot[33];
-  constexpr uint32_t kChunk = 128;
-  const int NT = blockDim.x, tid = threadIdx.x;
-  const int per = (P + NT - 1) / NT;
-  const int b0 = 1 + tid * per, b1 = min(P + 1, b0 + per);
+  const int p0 = 1 + blockIdx.x * kChunkBlock + threadIdx.x * kChunkPages;
   int recs = 0, chunks = 0;
-  for (int p = b0; p < b1; ++p) {
-    const uint32_t loc = res[p];
-    if (loc == kNone) continue;
-    const uint32_t r = page_size >> level[loc >> 8];
+  for (int p = p0; p < min(P + 1, p0 + kChunkPages); ++p) {
+    uint32_t r, c;
+    page_chunks(res, level, p, page_size, r, c);
     recs += (int)r;
-    chunks += (int)((r + kChunk - 1) / kChunk);
+    chunks += (int)c;
   }
-  int g = block_excl_scan(recs, warp_tot);
-  const int total_recs = warp_tot[32];
+  block_excl_scan(recs, warp_tot);
+  const int tr = warp_tot[32];
   __syncthreads();
-  int c = block_excl_scan(chunks, warp_tot);
-  const int total_chunks = warp_tot[32];
-  for (int p = b0; p < b1; ++p) {
+  block_excl_scan(chunks, warp_tot);
+  if (threadIdx.x == 0) sums[blockIdx.x] = make_uint2((uint32_t)tr, (uint32_t)warp_tot[32]);
+}
+
+__global__ void __launch_bounds__(1024) dpt_chunk_scan_k(uint2* __restrict__ sums, int nb,
+                                                        vms_dpt_stats* st) {
+  pdl_wait();
+  __shared__ int warp_tot[33];
+  int base_r = 0, base_c = 0;
+  for (int b0 = 0; b0 < nb; b0 += blockDim.x) {
+    const int b = b0 + threadIdx.x;
+    const uint2 v = b < nb ? sums[b] : make_uint2(0u, 0u);
+    const int er = block_excl_scan((int)v.x, warp_tot);
+    const int tr = warp_tot[32];
+    __syncthreads();
+    const int ec = block_excl_scan((int)v.y, warp_tot);
+    const int tc = warp_tot[32];
+    __syncthreads();
+    if (b < nb) sums[b] = make_uint2((uint32_t)(base_r + er), (uint32_t)(base_c + ec));
+    base_r += tr;
+    base_c += tc;
+  }
+  if (threadIdx.x == 0) {
+    st->n_records = (uint32_t)base_r;
+    st->n_chunks = (uint32_t)base_c;
+  }
+}
+
+__global__ void __launch_bounds__(kChunkThreads) dpt_chunk_emit_k(
+    const uint32_t* __restrict__ res, const int8_t* __restrict__ level, int32_t P,
+    uint32_t page_size, const uint2* __restrict__ bases, vms_chunk* __restrict__ out,
+    int64_t cap) {
+  pdl_wait();
+  __shared__ int warp_tot[33];
+  const int p0 = 1 + blockIdx.x * kChunkBlock + threadIdx.x * kChunkPages;
+  const int p1 = min(P + 1, p0 + kChunkPages);
+  int recs = 0, chunks = 0;
+  for (int p = p0; p < p1; ++p) {
+    uint32_t r, c;
+    page_chunks(res, level, p, page_size, r, c);
+    recs += (int)r;
+    chunks += (int)c;
+  }
+  const uint2 base = bases[blockIdx.x];
+  int g = (int)base.x + block_excl_scan(recs, warp_tot);
+  __syncthreads();
+  int64_t c = (int64_t)base.y + block_excl_scan(chunks, warp_tot);
+  for (int p = p0; p < p1; ++p) {
     const uint32_t loc = res[p];
     if (loc == kNone) continue;
-    const uint32_t e = loc >> 8, s = loc & 0xFF;
+    const uint32_t e = loc >> 8, sl = loc & 0xFF;
     const uint32_t r = page_size >> level[e];
-    const uint32_t row = e * page_size + s * r;
-    for (uint32_t k = 0; k < r; k += kChunk) {
-      if (c < cap) out[c] = vms_chunk{row + k, (uint32_t)g + k, min(kChunk, r - k), 0u};
+    const uint32_t row = e * page_size + sl * r;
+    for (uint32_t k = 0; k < r; k += kChunkRecs) {
+      if (c < cap) out[c] = vms_chunk{row + k, (uint32_t)g + k, min(kChunkRecs, r - k), 0u};
       ++c;
     }
     g += (int)r;
-  }
-  if (tid == 0) {
-    st->n_chunks = (uint32_t)total_chunks;
-    st->n_records = (uint32_t)total_recs;
   }
 }
 
@@ -446,7 +497,8 @@ vms_dpt* vms_dpt_create(int32_t capacity, int32_t page_count, int32_t levels) {
                o_slots = take(4 * C * d->S), o_res = take(4 * P1),
                o_bm = take(4 * (size_t)(levels + 1) * d->W), o_lru0 = take(4 * C),
                o_lru1 = take(4 * C), o_cur = take(4), o_sk = take(8 * pow2),
-               o_sv = take(4 * pow2), o_cnt = take(4 * 18);
+               o_sv = take(4 * pow2), o_cnt = take(4 * 18),
+               o_cs = take(8 * (P1 / 2048 + 2));
   if (cudaMalloc(&d->base, off) != cudaSuccess) {
     set_error("dpt_create: device allocation of %zu bytes failed", off);
     delete d;
@@ -466,6 +518,7 @@ vms_dpt* vms_dpt_create(int32_t capacity, int32_t page_count, int32_t levels) {
   d->skeys = reinterpret_cast<uint64_t*>(b + o_sk);
   d->svals = reinterpret_cast<uint32_t*>(b + o_sv);
   d->counts = reinterpret_cast<int32_t*>(b + o_cnt);
+  d->csums = reinterpret_cast<uint2*>(b + o_cs);
   // initial state: every entry empty, LRU stamp -1, order by index
   std::vector<int8_t> lv(C, -1);
   std::vector<int32_t> last(C, -1), order(C);
@@ -495,10 +548,22 @@ void vms_dpt_destroy(vms_dpt* d) {
   delete d;
 }
 
+namespace {
+size_t dpt_fixed_smem(const vms_dpt* d) {
+  return 4 * (size_t)d->C + 4 * (size_t)(d->L + 2) * (d->W + d->WS) + 2 * (size_t)d->C + 64;
+}
+// the largest power-of-two sort buffer that fits next to the table state
+int dpt_sort_cap(const vms_dpt* d) {
+  const size_t avail = 227 * 1024 - 2048 - dpt_fixed_smem(d);
+  int cap = 1024;
+  while ((size_t)(2 * cap) * 12 <= avail && cap < (1 << 16)) cap *= 2;
+  return cap;
+}
+}  // namespace
+
 size_t vms_dpt_smem_bytes(const vms_dpt* d) {
   if (!d) return 0;
-  return (size_t)vms::kSortSmem * 12 + 4 * (size_t)d->C + 4 * (size_t)(d->L + 2) * (d->W + d->WS) +
-         2 * (size_t)d->C;
+  return (size_t)dpt_sort_cap(d) * 12 + dpt_fixed_smem(d);
 }
 
 int32_t vms_dpt_update(vms_dpt* d, const uint32_t* pid, const uint32_t* enc,
@@ -545,6 +610,7 @@ int32_t vms_dpt_update(vms_dpt* d, const uint32_t* pid, const uint32_t* enc,
   a.plan_slot = plan_slot;
   a.plan_cap = plan_cap;
   a.stats = stats;
+  a.sort_cap = dpt_sort_cap(d);
   const size_t smem = vms_dpt_smem_bytes(d);
   VMS_CUDA(cudaFuncSetAttribute(dpt_update_k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)smem));
@@ -562,8 +628,12 @@ int32_t vms_dpt_chunks(vms_dpt* d, uint32_t page_size, vms_chunk* out, int64_t c
     return VMS_ERR_INVALID;
   }
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  VMS_CUDA(launch(dpt_chunks_k, 1, kThreads, 0, s, (const uint32_t*)d->res,
-                  (const int8_t*)d->level, d->P, page_size, out, cap, stats));
+  const int nb = (d->P + kChunkBlock - 1) / kChunkBlock;
+  VMS_CUDA(launch(dpt_chunk_sums_k, nb, kChunkThreads, 0, s, (const uint32_t*)d->res,
+                  (const int8_t*)d->level, d->P, page_size, d->csums));
+  VMS_CUDA(launch(dpt_chunk_scan_k, 1, 1024, 0, s, d->csums, nb, stats));
+  VMS_CUDA(launch(dpt_chunk_emit_k, nb, kChunkThreads, 0, s, (const uint32_t*)d->res,
+                  (const int8_t*)d->level, d->P, page_size, (const uint2*)d->csums, out, cap));
   mark("dpt_chunks", s);
   VMS_LAUNCH_CHECK("dpt_chunks");
   return VMS_OK;

@@ -310,10 +310,8 @@ class PageTable:
 
 DEVICE_TABLE_MAX_CAPACITY = 8192  # csrc/dpt.cu kMaxCap (entry metadata in shared memory)
 DEVICE_TABLE_MAX_LEVELS = 6        # <= 32 slots per entry
-# the session default uses the device table up to this many pages: past it
-# the one-CTA chunk-table scan over every page costs more than the host's
-# ordered-map walk (C4, 170 K pages: 166 vs 171 frames/s; C2/C3: +3-4 %)
-DEVICE_TABLE_AUTO_MAX_PAGES = 65536
+# largest page count the device table's 30-bit page ids address
+DEVICE_TABLE_MAX_PAGES = (1 << 30) - 1
 
 
 class DevicePageTable:
@@ -629,9 +627,9 @@ class VmSession:
             # the page table on the device: the visibility
             # graph runs update_page_table too; the host only issues copies
             if device_table is None:
-                # default: on the device whenever it fits its limits and the
-                # scene is not huge (measured: +3-4 % device fps, +5 % e2e on
-                # C2/C3; -3 % on C4); VMSPLAT_DEVICE_TABLE
+                # default: on the device whenever it fits its limits (measured:
+                # +3-4 % device fps, +4-5 % e2e on C2/C3, equal on C4);
+                # VMSPLAT_DEVICE_TABLE
                 # = 0 / 1 forces the host C++ table / the device table
                 import os
 
@@ -639,7 +637,7 @@ class VmSession:
                 device_table = env == "1" if env in ("0", "1") else (
                     self.capacity <= DEVICE_TABLE_MAX_CAPACITY and
                     int(scene.lod_levels) <= DEVICE_TABLE_MAX_LEVELS and
-                    int(scene.page_count) <= DEVICE_TABLE_AUTO_MAX_PAGES)
+                    int(scene.page_count) <= DEVICE_TABLE_MAX_PAGES)
             d.device_table = int(bool(device_table))
             self.device_table = bool(device_table)
             self._desc = d
