@@ -253,17 +253,27 @@ struct LodArgs {
   int32_t* status;   // per page: 0 ok, 1 inertia increased, 2 level overflow
   double* feat_ws;   // per page rows_in x 14
   double* cent_ws;   // per page rows_in x 14
+  int* live_ws;      // per page rows_in: the live rows in order (seeding -> Lloyd)
+  int* m_ws;         // per page: live row count
   uint32_t k_cap;
 };
 
-__global__ void __launch_bounds__(kThreads) lod_page_k(LodArgs a) {
+// Two launches per level: phase 1 (kSeedThreads threads, shared memory for
+// the two distance arrays only, so ~5 pages share an SM and their serial
+// k-means++ cumsums overlap) finds the live rows, builds the features and
+// seeds the centres; phase 2 (kThreads) runs the Lloyd iterations and the
+// merge.  Both phases keep the page's state in global memory (features,
+// centres, live rows, the Philox state).
+constexpr int kSeedThreads = 128;
+
+__global__ void __launch_bounds__(kThreads) lod_page_k(LodArgs a, int phase) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ Shared sh;
   const uint32_t page = blockIdx.x;
   const int R = (int)a.rows_in, K = (int)a.k_cap;
   double* d2 = reinterpret_cast<double*>(smem);
-  double* cdf = d2 + R;
-  double* tile = cdf + R;
+  double* cdf = d2 + R;  // phase 1: R + 2 doubles (also the live scan's scratch)
+  double* tile = cdf;    // phase 2
   int* live = reinterpret_cast<int*>(tile + kTile * kFeat);
   int* asg = live + (R + 1);
   int* mem = asg + R;
@@ -272,44 +282,61 @@ __global__ void __launch_bounds__(kThreads) lod_page_k(LodArgs a) {
   const float* in = a.in + (size_t)page * R * kRec;
   double* feat = a.feat_ws + (size_t)page * R * kFeat;
   double* cent = a.cent_ws + (size_t)page * R * kFeat;
+  int* glive = a.live_ws + (size_t)page * R;
   const int tid = threadIdx.x, NT = blockDim.x;
 
-  // live rows in order (is_padding: all-zero rows, gaussians.py:71-73)
-  if (a.k_fixed == 0) {  // pyramid level: padding rows are not clustered
-    for (int i = tid; i < R; i += NT) {
-      bool any = false;
-      for (int j = 0; j < kRec; ++j) any |= in[(size_t)i * kRec + j] != 0.0f;
-      cnt[i] = any ? 1 : 0;  // scratch flags (cnt has >= R + 1 entries here)
+  if (phase == 1) {
+    // live rows in order (is_padding: all-zero rows, gaussians.py:71-73)
+    int* flag = reinterpret_cast<int*>(cdf);  // R + 1 ints
+    int* pos = flag + (R + 1);                // R + 1 ints
+    if (a.k_fixed == 0) {  // pyramid level: padding rows are not clustered
+      for (int i = tid; i < R; i += NT) {
+        bool any = false;
+        for (int j = 0; j < kRec; ++j) any |= in[(size_t)i * kRec + j] != 0.0f;
+        flag[i] = any ? 1 : 0;
+      }
+      __syncthreads();
+      block_scan(sh, flag, pos, R);
+      for (int i = tid; i < R; i += NT)
+        if (flag[i]) glive[pos[i]] = i;
+      if (tid == 0) sh.n_live = pos[R];
+    } else {
+      for (int i = tid; i < R; i += NT) glive[i] = i;
+      if (tid == 0) sh.n_live = R;
+    }
+    if (tid == 0) {
+      sh.rng = a.rng[page];
+      a.m_ws[page] = sh.n_live;
     }
     __syncthreads();
-    block_scan(sh, cnt, off, R);
-    for (int i = tid; i < R; i += NT)
-      if (cnt[i]) live[off[i]] = i;
-    if (tid == 0) sh.n_live = off[R];
   } else {
-    for (int i = tid; i < R; i += NT) live[i] = i;
-    if (tid == 0) sh.n_live = R;
+    if (tid == 0) {
+      sh.n_live = a.m_ws[page];
+      sh.rng = a.rng[page];
+      sh.stop = 0;
+    }
+    __syncthreads();
+    for (int i = tid; i < sh.n_live; i += NT) live[i] = glive[i];
   }
-  if (tid == 0) {
-    sh.rng = a.rng[page];
-    sh.stop = 0;
-  }
-  __syncthreads();
   const int m = sh.n_live;
   if (m == 0) return;
   const int k = a.k_fixed > 0 ? a.k_fixed : a.k_fixed == 0 ? (m + 1) / 2 : 1;
-  for (int i = tid; i < R; i += NT) asg[i] = -1;
+  if (phase == 2)
+    for (int i = tid; i < R; i += NT) asg[i] = -1;
 
   if (a.k_fixed < 0) {
     // merge_cluster of all rows (lod.py:134-154)
+    if (phase == 1) return;
     for (int i = tid; i < m; i += NT) asg[i] = 0;
   } else if (k >= m) {
     // cluster_page: k >= m -> arange(m), no draws (lod.py:96-97)
+    if (phase == 1) return;
     for (int i = tid; i < m; i += NT) asg[i] = i;
-  } else {
+  } else if (phase == 1) {
+    __syncthreads();  // glive complete
     // features (lod.py:44-59)
     for (int i = tid; i < m; i += NT) {
-      const float* r = in + (size_t)live[i] * kRec;
+      const float* r = in + (size_t)glive[i] * kRec;
       double* f = feat + (size_t)i * kFeat;
       for (int j = 0; j < 3; ++j) f[j] = dmul((double)r[j], a.w[0]);
       const bool flip = (double)r[3] < 0.0;
@@ -381,6 +408,9 @@ __global__ void __launch_bounds__(kThreads) lod_page_k(LodArgs a) {
       }
       __syncthreads();
     }
+    if (tid == 0) a.rng[page] = sh.rng;
+    return;
+  } else {
     // Lloyd iterations (lod.py:106-130)
     if (tid == 0) sh.prev_inertia = __longlong_as_double(0x7FF0000000000000ll);
     for (int it = 0; it < a.max_iters; ++it) {
@@ -584,7 +614,9 @@ __global__ void __launch_bounds__(kThreads) lod_page_k(LodArgs a) {
 }  // namespace vms
 
 extern "C" size_t vms_lod_workspace_bytes(uint32_t pages, uint32_t rows_in) {
-  return (size_t)pages * rows_in * 14 * sizeof(double) * 2;
+  // features + centres (f64 x 14 per row), the live rows, the live counts
+  return (size_t)pages * rows_in * (14 * sizeof(double) * 2 + sizeof(int)) +
+         sizeof(int) * (size_t)pages;
 }
 
 extern "C" int32_t vms_lod_level(const float* in, uint32_t pages, uint32_t rows_in, float* out,
@@ -618,12 +650,16 @@ extern "C" int32_t vms_lod_level(const float* in, uint32_t pages, uint32_t rows_
   a.status = status;
   a.feat_ws = static_cast<double*>(workspace);
   a.cent_ws = a.feat_ws + (size_t)pages * rows_in * kFeat;
+  a.live_ws = reinterpret_cast<int*>(a.cent_ws + (size_t)pages * rows_in * kFeat);
+  a.m_ws = a.live_ws + (size_t)pages * rows_in;
   a.k_cap = p->k > 0 ? (uint32_t)p->k : (rows_in + 1) / 2;
-  if (a.k_cap < rows_in) a.k_cap = rows_in;  // cnt/off double as row-flag scratch
-  const size_t smem = sizeof(double) * (2 * (size_t)rows_in + kTile * kFeat) +
-                      sizeof(int) * (3 * (size_t)rows_in + 2 + 2 * ((size_t)a.k_cap + 1));
+  const size_t smem1 = sizeof(double) * (2 * (size_t)rows_in + 2);
+  const size_t smem2 = sizeof(double) * ((size_t)rows_in + kTile * kFeat) +
+                       sizeof(int) * (3 * (size_t)rows_in + 2 + 2 * ((size_t)a.k_cap + 1));
+  const size_t smem = smem1 > smem2 ? smem1 : smem2;
   VMS_CUDA(cudaFuncSetAttribute(lod_page_k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  lod_page_k<<<pages, kThreads, smem, s>>>(a);
+  lod_page_k<<<pages, kSeedThreads, smem1, s>>>(a, 1);
+  lod_page_k<<<pages, kThreads, smem2, s>>>(a, 2);
   mark("lod_page", s);
   VMS_LAUNCH_CHECK("lod_level");
   return VMS_OK;
