@@ -24,6 +24,8 @@
 // and the 53-bit double - the state is handed in and written back, so a
 // caller's numpy Generator continues exactly where the reference would.
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -145,25 +147,25 @@ __device__ double pw_sum(F at, int off, int n) {
   return dadd(a, pw_sum(at, off + n2, n - n2));
 }
 
-__device__ void pw_enum(int off, int n, int* lo, int* ln, int& cnt) {
+// The pairwise recursion's shape for a given n, built once: the leaves (in
+// order) and the internal nodes in post-order, each adding its two children
+// (a child < kNodeBase is a leaf, else node child - kNodeBase).
+constexpr int kNodeBase = 1 << 12;
+
+__device__ int pw_build(int off, int n, int* lo, int* ln, int& nl, int* nleft, int* nright,
+                        int& nn) {
   if (n <= 128) {
-    lo[cnt] = off;
-    ln[cnt] = n;
-    ++cnt;
-    return;
+    lo[nl] = off;
+    ln[nl] = n;
+    return nl++;
   }
   int n2 = n / 2;
   n2 -= n2 % 8;
-  pw_enum(off, n2, lo, ln, cnt);
-  pw_enum(off + n2, n - n2, lo, ln, cnt);
-}
-
-__device__ double pw_combine(int n, const double* leaf, int& li) {
-  if (n <= 128) return leaf[li++];
-  int n2 = n / 2;
-  n2 -= n2 % 8;
-  const double a = pw_combine(n2, leaf, li);
-  return dadd(a, pw_combine(n - n2, leaf, li));
+  const int l = pw_build(off, n2, lo, ln, nl, nleft, nright, nn);
+  const int r = pw_build(off + n2, n - n2, lo, ln, nl, nleft, nright, nn);
+  nleft[nn] = l;
+  nright[nn] = r;
+  return kNodeBase + nn++;
 }
 
 // sum of the 14 squared feature differences, NumPy's pairwise order for n=14
@@ -187,20 +189,24 @@ VMS_DEV double dot4(const double* q, const double* r) {
 struct Shared {
   Philox rng;
   double total, u, prev_inertia;
-  int idx, changed, any_empty, n_live, k, stop, leaves;
-  int leaf_off[kMaxLeaves], leaf_n[kMaxLeaves];
-  double leaf_sum[kMaxLeaves];
+  int idx, changed, any_empty, n_live, k, stop, leaves, nodes, plan_n;
+  int leaf_off[kMaxLeaves], leaf_n[kMaxLeaves], node_l[kMaxLeaves], node_r[kMaxLeaves];
+  double leaf_sum[kMaxLeaves], node_sum[kMaxLeaves];
   double ctr[kFeat];
   int warp_tot[kThreads / 32];
 };
 
-// block-wide pairwise sum of a[0..n) in shared memory (leaves on warp 0's
-// lanes, combined in the recursion's order by thread 0); result in sh.total
+// block-wide pairwise sum of a[0..n) in shared memory: the leaves on
+// separate threads, then thread 0 adds the internal nodes in post-order
+// (the recursion's order); result in sh.total.  The shape is built once
+// per n (sh.plan_n, reset to -1 at kernel start).
 __device__ void block_pw(Shared& sh, const double* a, int n) {
-  if (threadIdx.x == 0) {
-    int cnt = 0;
-    pw_enum(0, n, sh.leaf_off, sh.leaf_n, cnt);
-    sh.leaves = cnt;
+  if (threadIdx.x == 0 && sh.plan_n != n) {
+    int nl = 0, nn = 0;
+    pw_build(0, n, sh.leaf_off, sh.leaf_n, nl, sh.node_l, sh.node_r, nn);
+    sh.leaves = nl;
+    sh.nodes = nn;
+    sh.plan_n = n;
   }
   __syncthreads();
   auto at = [a](int i) { return a[i]; };
@@ -208,8 +214,9 @@ __device__ void block_pw(Shared& sh, const double* a, int n) {
     sh.leaf_sum[l] = pw_leaf(at, sh.leaf_off[l], sh.leaf_n[l]);
   __syncthreads();
   if (threadIdx.x == 0) {
-    int li = 0;
-    sh.total = pw_combine(n, sh.leaf_sum, li);
+    auto val = [&](int c) { return c < kNodeBase ? sh.leaf_sum[c] : sh.node_sum[c - kNodeBase]; };
+    for (int j = 0; j < sh.nodes; ++j) sh.node_sum[j] = dadd(val(sh.node_l[j]), val(sh.node_r[j]));
+    sh.total = sh.nodes ? sh.node_sum[sh.nodes - 1] : sh.leaf_sum[0];
   }
   __syncthreads();
 }
@@ -265,10 +272,12 @@ struct LodArgs {
 // merge.  Both phases keep the page's state in global memory (features,
 // centres, live rows, the Philox state).
 constexpr int kSeedThreads = 128;
+__device__ int g_lod_prof = 0;  // VMSPLAT_LOD_PROF=1: per-section clocks of page 0's seeding
 
-__global__ void __launch_bounds__(kThreads) lod_page_k(LodArgs a, int phase) {
+template <int phase>
+__device__ __forceinline__ void lod_page(const LodArgs& a, Shared& sh) {
   extern __shared__ __align__(16) unsigned char smem[];
-  __shared__ Shared sh;
+  if (threadIdx.x == 0) sh.plan_n = -1;
   const uint32_t page = blockIdx.x;
   const int R = (int)a.rows_in, K = (int)a.k_cap;
   double* d2 = reinterpret_cast<double*>(smem);
@@ -352,15 +361,27 @@ __global__ void __launch_bounds__(kThreads) lod_page_k(LodArgs a, int phase) {
     // k-means++ seeding (lod.py:62-80)
     if (tid == 0) sh.idx = (int)bounded(sh.rng, (uint32_t)m);
     __syncthreads();
+    long long tp[6] = {0, 0, 0, 0, 0, 0};  // VMSPLAT_LOD_PROF: clock per section
+    const bool prof = g_lod_prof && blockIdx.x == 0 && tid == 0;
+    long long t0 = prof ? clock64() : 0;
+    auto tick = [&](int k) {
+      if (prof) {
+        const long long t = clock64();
+        tp[k] += t - t0;
+        t0 = t;
+      }
+    };
     for (int c = 0; c < k; ++c) {
       if (c > 0) {
         block_pw(sh, d2, m);
+        tick(0);
         const double total = sh.total;
         if (!(total > 0.0)) {
           if (tid == 0) sh.idx = (int)bounded(sh.rng, (uint32_t)m);
         } else {
           for (int i = tid; i < m; i += NT) cdf[i] = ddiv(d2[i], total);
           __syncthreads();
+          tick(1);
           if (tid == 0) {
             double run = 0.0;
             int i = 0;
@@ -379,15 +400,17 @@ __global__ void __launch_bounds__(kThreads) lod_page_k(LodArgs a, int phase) {
               run = (i == 0) ? cdf[0] : dadd(run, cdf[i]);
               cdf[i] = run;
             }
-            sh.u = next_double(sh.rng);
-            sh.idx = m - 1;
-          }
-          __syncthreads();
-          const double last = cdf[m - 1], u = sh.u;
-          __syncthreads();
-          for (int i = tid; i < m; i += NT) {
-            const double v = ddiv(cdf[i], last);
-            if (v > u) atomicMin(&sh.idx, i);
+            tick(2);
+            // searchsorted(cdf / cdf[-1], u, 'right'): RN(x / last) is
+            // monotone in x, so the first index past u is found by bisection
+            const double u = next_double(sh.rng), last = run;
+            int lo = 0, hi = m - 1;  // cdf[m - 1] / last == 1 > u
+            while (lo < hi) {
+              const int mid = (lo + hi) >> 1;
+              if (ddiv(cdf[mid], last) > u) hi = mid; else lo = mid + 1;
+            }
+            sh.idx = lo;
+            tick(3);
           }
         }
         __syncthreads();
@@ -407,7 +430,11 @@ __global__ void __launch_bounds__(kThreads) lod_page_k(LodArgs a, int phase) {
         d2[i] = (c == 0) ? d : fmin(d2[i], d);
       }
       __syncthreads();
+      tick(4);
     }
+    if (prof)
+      printf("[lod seed] m %d k %d cycles: pairwise %lld, divide %lld, cumsum %lld, search %lld, "
+             "distances %lld\n", m, k, tp[0], tp[1], tp[2], tp[3], tp[4]);
     if (tid == 0) a.rng[page] = sh.rng;
     return;
   } else {
@@ -610,6 +637,16 @@ __global__ void __launch_bounds__(kThreads) lod_page_k(LodArgs a, int phase) {
   }
 }
 
+__global__ void __launch_bounds__(kSeedThreads) lod_seed_k(LodArgs a) {
+  __shared__ Shared sh;
+  lod_page<1>(a, sh);
+}
+
+__global__ void __launch_bounds__(kThreads) lod_lloyd_k(LodArgs a) {
+  __shared__ Shared sh;
+  lod_page<2>(a, sh);
+}
+
 }  // namespace
 }  // namespace vms
 
@@ -656,10 +693,16 @@ extern "C" int32_t vms_lod_level(const float* in, uint32_t pages, uint32_t rows_
   const size_t smem1 = sizeof(double) * (2 * (size_t)rows_in + 2);
   const size_t smem2 = sizeof(double) * ((size_t)rows_in + kTile * kFeat) +
                        sizeof(int) * (3 * (size_t)rows_in + 2 + 2 * ((size_t)a.k_cap + 1));
-  const size_t smem = smem1 > smem2 ? smem1 : smem2;
-  VMS_CUDA(cudaFuncSetAttribute(lod_page_k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  lod_page_k<<<pages, kSeedThreads, smem1, s>>>(a, 1);
-  lod_page_k<<<pages, kThreads, smem2, s>>>(a, 2);
+  VMS_CUDA(cudaFuncSetAttribute(lod_seed_k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1));
+  VMS_CUDA(cudaFuncSetAttribute(lod_lloyd_k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
+  static const int prof = [] {
+    const char* e = getenv("VMSPLAT_LOD_PROF");
+    return e && e[0] == '1' ? 1 : 0;
+  }();
+  if (prof) VMS_CUDA(cudaMemcpyToSymbolAsync(g_lod_prof, &prof, sizeof(int), 0,
+                                             cudaMemcpyHostToDevice, s));
+  lod_seed_k<<<pages, kSeedThreads, smem1, s>>>(a);
+  lod_lloyd_k<<<pages, kThreads, smem2, s>>>(a);
   mark("lod_page", s);
   VMS_LAUNCH_CHECK("lod_level");
   return VMS_OK;
