@@ -530,7 +530,8 @@ def run_ours(args, rank, world, local_rank):
             ent = json.load(open(tf)).get(dominant + "_k")
             if ent:
                 traffic = int(ent["bytes_per_launch"])
-                limits = {k: ent[k] for k in ("fp64_pct", "xu_pct", "ipc", "dur_us", "frame",
+                limits = {k: ent[k] for k in ("fp64_pct", "xu_pct", "ipc", "issue_frac",
+                                              "sm_pct", "top_stalls", "dur_us", "frame",
                                               "source") if k in ent}
         except (ValueError, KeyError, TypeError):
             traffic = None

@@ -69,9 +69,19 @@ def main():
         print(" | ".join([name] + [f"{v:.3g}" for v in vals] + [st]))
         base = name.split("<")[0]
         rd, wr = vals[1], vals[2]
-        traffic.setdefault(base, []).append((rd + wr) * 1e6)
+        m = dict(zip([x[1] for x in METRICS], vals))
+        traffic.setdefault(base, []).append(
+            ((rd + wr) * 1e6, m["dur_us"], m["fp64_%"], m["xu_%"], m["ipc"], m["sm_%"], st))
     if traffic_out:
-        summary = {k: {"bytes_per_launch": sum(v) / len(v), "launches": len(v),
+        def mean(v, i):
+            return round(sum(x[i] for x in v) / len(v), 3)
+
+        frame = next((tok[1:] for tok in path.replace(".", "_").split("_")
+                      if tok.startswith("f") and tok[1:].isdigit()), None)
+        summary = {k: {"bytes_per_launch": mean(v, 0), "launches": len(v), "dur_us": mean(v, 1),
+                       "fp64_pct": mean(v, 2), "xu_pct": mean(v, 3), "ipc": mean(v, 4),
+                       "issue_frac": round(mean(v, 4) / 4.0, 3), "sm_pct": mean(v, 5),
+                       "top_stalls": v[0][6], "frame": frame,
                        "source": path.split("/")[-1]} for k, v in traffic.items()}
         with open(traffic_out, "w") as fh:
             json.dump(summary, fh, indent=1)
