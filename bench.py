@@ -309,7 +309,7 @@ def bench_config(args, lay, world=1):
                   f"126 MB L2; the frame's records stream from it every step)",
             "upload_mode": upload_mode_of(args),
             "page_table": "host" if os.environ.get("VMSPLAT_DEVICE_TABLE") == "0"
-            else "device (dpt_update_k) when capacity <= 8192 and pages <= 65536, else host"}
+            else "device (dpt_update_k) when capacity <= 8192 and levels <= 6, else host"}
 
 
 def measure_pcie(torch, nbytes=256 << 20, reps=10):
@@ -358,12 +358,21 @@ def run_ours(args, rank, world, local_rank):
     from paper_2506_19415_b200.runtime import VmSession
     from paper_2506_19415_b200.scene_io import read_scene
 
-    torch.cuda.set_device(local_rank)
+    # one GPU per rank; VMSPLAT_DIST_BACKEND=gloo (with ranks sharing the
+    # visible GPUs round-robin) only exercises the multi-rank code path on a
+    # box with fewer GPUs than ranks - its numbers are not a scaling result
+    backend = os.environ.get("VMSPLAT_DIST_BACKEND", "nccl")
+    dev_index = local_rank % max(torch.cuda.device_count(), 1)
+    torch.cuda.set_device(dev_index)
+    coll = "cuda" if backend == "nccl" else "cpu"
     dist = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev_index))
+        else:
+            dist.init_process_group(backend)
     cfg = config_of(args)
     lay, path = ensure_scene(args, rank)
     if dist:
@@ -408,7 +417,7 @@ def run_ours(args, rank, world, local_rank):
     fresh_session()
     stream = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    sampler = ClockSampler(local_rank)
+    sampler = ClockSampler(dev_index)
     # N > 1: each timed frame is rendered into its own slot of a
     # device-resident frame stack, gathered to rank 0 after the timed region
     # (N = 1 leaves each frame in the session's two alternating device
@@ -429,7 +438,7 @@ def run_ours(args, rank, world, local_rank):
         holder["s"].flush()
         ms = e0.elapsed_time(e1)
         if dist:
-            t = torch.tensor([ms], device="cuda")
+            t = torch.tensor([ms], device=coll)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms = float(t.item())
             dist.barrier()
@@ -444,9 +453,10 @@ def run_ours(args, rank, world, local_rank):
 
     gathered = None
     if dist:
-        sharding.gather_rows(sharding.stats_rows(stats), dist, device="cuda")
-        frames_all = [torch.empty_like(stack) for _ in range(world)] if rank == 0 else None
-        dist.gather(stack, frames_all, dst=0)
+        sharding.gather_rows(sharding.stats_rows(stats), dist, device=coll)
+        src = stack if coll == "cuda" else stack.cpu()
+        frames_all = [torch.empty_like(src) for _ in range(world)] if rank == 0 else None
+        dist.gather(src, frames_all, dst=0)
         if rank == 0:
             gathered = {"frames": world * args.steps,
                         "bytes": world * stack.numel() * 4,
