@@ -552,11 +552,14 @@ namespace {
 size_t dpt_fixed_smem(const vms_dpt* d) {
   return 4 * (size_t)d->C + 4 * (size_t)(d->L + 2) * (d->W + d->WS) + 2 * (size_t)d->C + 64;
 }
-// the largest power-of-two sort buffer that fits next to the table state
+// the sort buffer: a power of two covering every page when that fits next
+// to the table state (no larger - a big shared-memory footprint would make
+// the update wait for an SM the render in flight has to give up), else the
+// largest that fits (more required pages spill to global memory)
 int dpt_sort_cap(const vms_dpt* d) {
   const size_t avail = 227 * 1024 - 2048 - dpt_fixed_smem(d);
-  int cap = 1024;
-  while ((size_t)(2 * cap) * 12 <= avail && cap < (1 << 16)) cap *= 2;
+  int cap = 256;
+  while (cap < d->P + 1 && (size_t)(2 * cap) * 12 <= avail && cap < (1 << 16)) cap *= 2;
   return cap;
 }
 }  // namespace

@@ -534,7 +534,12 @@ vms_session* vms_session_create(const vms_session_desc* desc) {
   }
   if (desc->upload_mode == 2) {
     const unsigned hw = std::thread::hardware_concurrency();
-    s->pool = new CopyPool((int)std::max(1u, std::min(8u, hw ? hw / 2 : 4u)));
+    unsigned nt = std::max(1u, std::min(8u, hw ? hw / 2 : 4u));
+    if (const char* e = std::getenv("VMSPLAT_COPY_THREADS")) {  // mode-2 gather threads
+      const int v = std::atoi(e);
+      if (v > 0 && v <= 64) nt = (unsigned)v;
+    }
+    s->pool = new CopyPool((int)nt);
     s->pool->set_source_fd(desc->host_fd);
   }
   s->plan_pid.resize(P + 1);
