@@ -74,7 +74,7 @@ constexpr int kMaxBands = 8;           // blend launches per frame (host-output 
 // per-tile instance counts come for free as a 2D difference array over the
 // tile grid (4 updates per splat, gx = tiles_x + 1 columns) accumulated in
 // shared memory and flushed once per CTA; tile_prep_k integrates it.
-__global__ void dup_count_k(const uint32_t* __restrict__ vals, const BlendRec* __restrict__ rec,
+__global__ void dup_count_k(const uint32_t* __restrict__ vals, const uint2* __restrict__ box,
                             const RenderCounters* __restrict__ ctr, int shift, int gx, int gy,
                             uint32_t* __restrict__ cnt, uint32_t* __restrict__ rects,
                             uint32_t* __restrict__ tdiff) {
@@ -100,20 +100,19 @@ __global__ void dup_count_k(const uint32_t* __restrict__ vals, const BlendRec* _
     atomicAdd(&d[(ty1 + 1) * gx + tx0], 0xFFFFFFFFu);
     atomicAdd(&d[(ty1 + 1) * gx + tx1 + 1], 1u);
   };
-  // two splats per thread per step: both gathers in flight together (only
-  // the packed box words of the 48-byte record are read)
+  // two splats per thread per step: both gathers in flight together, each an
+  // 8-byte box word pair (the preprocess writes them beside the 48-byte
+  // records, so this gather touches a sixth of the bytes)
   const uint32_t stride = gridDim.x * blockDim.x;
   uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
   for (; s + stride < n; s += 2 * stride) {
-    const BlendRec* r0 = rec + vals[s];
-    const BlendRec* r1 = rec + vals[s + stride];
-    const uint32_t bx0 = r0->bx, by0 = r0->by, bx1 = r1->bx, by1 = r1->by;
-    one(s, bx0, by0);
-    one(s + stride, bx1, by1);
+    const uint2 b0 = box[vals[s]], b1 = box[vals[s + stride]];
+    one(s, b0.x, b0.y);
+    one(s + stride, b1.x, b1.y);
   }
   if (s < n) {
-    const BlendRec* r0 = rec + vals[s];
-    one(s, r0->bx, r0->by);
+    const uint2 b0 = box[vals[s]];
+    one(s, b0.x, b0.y);
   }
   if (local) {
     __syncthreads();
@@ -1131,8 +1130,8 @@ __global__ void __launch_bounds__(kBlendThreads, 2) blend_hot_k(
 __global__ void pack_ordered_k(const float* __restrict__ centers, const float* __restrict__ conics,
                                const float* __restrict__ colors, const float* __restrict__ alphas,
                                const int32_t* __restrict__ bounds, uint32_t n, int w, int h,
-                               BlendRec* __restrict__ rec, uint32_t* __restrict__ vals,
-                               uint32_t* __restrict__ cnt) {
+                               BlendRec* __restrict__ rec, uint2* __restrict__ box,
+                               uint32_t* __restrict__ vals, uint32_t* __restrict__ cnt) {
   uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   int x0 = max(bounds[4 * i + 0], 0), x1 = min(bounds[4 * i + 1], w);
@@ -1155,6 +1154,7 @@ __global__ void pack_ordered_k(const float* __restrict__ centers, const float* _
   o.bx = (uint32_t)x0 | ((uint32_t)x1 << 16);
   o.by = (uint32_t)y0 | ((uint32_t)y1 << 16);
   rec[i] = o;
+  box[i] = make_uint2(o.bx, o.by);
   vals[i] = i;
   cnt[i] = empty ? 0u : 1u;
 }
@@ -1290,7 +1290,7 @@ int32_t tiles_and_blend(int width, int height, const uint32_t* vals, const Rende
   const int gx = tiles_x + 1, gy = tiles_y + 1;
   if (!cleared) VMS_CUDA(cudaMemsetAsync(w.tdiff, 0, sizeof(uint32_t) * gx * gy, s));
   const size_t dsm = gx * gy <= kDiffSmemWords ? sizeof(uint32_t) * gx * gy : 0;
-  VMS_CUDA(launch(dup_count_k, 2 * kSMs, T, dsm, s, vals, (const BlendRec*)w.rec,
+  VMS_CUDA(launch(dup_count_k, 2 * kSMs, T, dsm, s, vals, (const uint2*)w.box,
                   (const RenderCounters*)w.ctr, shift, gx, gy, w.cnt, w.rects, w.tdiff));
   mark("dup_count", s);
   int32_t st = scan_exclusive_u32(w.cnt, w.off, &w.ctr->n_kept, 0, w.n_cap, &w.ctr->n_inst,
@@ -1419,6 +1419,7 @@ size_t render_ws_bytes(uint32_t n_cap, uint32_t m_cap, uint32_t n_tiles) {
   size_t b = 0;
   b += sizeof(uint32_t) * (size_t)n_cap * 3;   // key_g, flag, pos
   b += sizeof(BlendRec) * (size_t)n_cap;       // rec
+  b += sizeof(uint2) * (size_t)n_cap;          // box
   b += sizeof(uint32_t) * (size_t)n_cap * 6;   // k0 v0 k1 v1 cnt off
   b += sizeof(uint32_t) * (size_t)m_cap * 4;   // tk0 tv0 tk1 tv1
   b += sizeof(uint32_t) * (size_t)n_cap;      // rects
@@ -1440,6 +1441,7 @@ RenderWs render_carve(void* ws, uint32_t n_cap, uint32_t m_cap, uint32_t n_tiles
   w.flag = carve<uint32_t>(p, n_cap);
   w.pos = carve<uint32_t>(p, n_cap);
   w.rec = carve<BlendRec>(p, n_cap);
+  w.box = carve<uint2>(p, n_cap);
   w.k0 = carve<uint32_t>(p, n_cap);
   w.v0 = carve<uint32_t>(p, n_cap);
   w.k1 = carve<uint32_t>(p, n_cap);
@@ -1523,7 +1525,8 @@ int32_t composite_ordered(const float* centers, const float* conics, const float
   if (n) {
     // splats with an empty clamped box are dropped; the rest keep their order
     pack_ordered_k<<<ceil_div<uint32_t>(n, T), T, 0, s>>>(centers, conics, colors, alphas, bounds,
-                                                          n, w, h, ws.rec, ws.v1, ws.flag);
+                                                          n, w, h, ws.rec, ws.box, ws.v1,
+                                                          ws.flag);
     int32_t st = scan_exclusive_u32(ws.flag, ws.pos, nullptr, n, n, &ws.ctr->n_kept, ws.scan_ws,
                                     s);
     if (st) return st;

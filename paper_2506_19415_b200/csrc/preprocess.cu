@@ -212,7 +212,7 @@ constexpr uint32_t kChunkFloats = kChunkRecords * kRecordFloats;
 __global__ void __launch_bounds__(kChunkRecords) preprocess_k(
     const float* __restrict__ pool, const Chunk* __restrict__ chunks,
     const FrameDev* __restrict__ fd, uint32_t* __restrict__ key_g, uint32_t* __restrict__ flag,
-    BlendRec* __restrict__ rec) {
+    BlendRec* __restrict__ rec, uint2* __restrict__ box) {
   extern __shared__ __align__(128) float sbuf[];  // kPreStages x kChunkFloats
   __shared__ __align__(8) uint64_t bar[kPreStages];
   __shared__ Chunk s_chunk[kPreStages];
@@ -288,6 +288,7 @@ __global__ void __launch_bounds__(kChunkRecords) preprocess_k(
         o.by = (uint32_t)p.y0 | ((uint32_t)p.y1 << 16);
         o.skip = blend_skip(o.alpha);
         rec[g] = o;
+        box[g] = make_uint2(o.bx, o.by);
         flag[g] = 1u;
         key_g[g] = __float_as_uint(__double2float_rn(p.tz));
       }
@@ -360,7 +361,7 @@ int32_t render_preprocess(const float* pool, const Chunk* chunks, uint32_t max_c
   }
   const uint32_t g = std::min<uint32_t>(max_chunks, (uint32_t)g_pre_grid);
   VMS_CUDA(launch(preprocess_k, g, kChunkRecords, kPreSmem, s, pool, chunks,
-                  (const FrameDev*)w.fd, w.key_g, w.flag, w.rec));
+                  (const FrameDev*)w.fd, w.key_g, w.flag, w.rec, w.box));
   mark("preprocess", s);
   VMS_LAUNCH_CHECK("render_preprocess");
   return VMS_OK;

@@ -65,6 +65,7 @@ struct RenderWs {
   uint32_t m_cap;  // tile-instance capacity
   uint32_t *key_g, *flag, *pos;
   BlendRec* rec;
+  uint2* box;      // the records' packed (bx, by) box words, for dup_count_k
   uint32_t *k0, *v0, *k1, *v1;
   uint32_t *cnt, *off;
   uint32_t *tk0, *tv0, *tk1, *tv1;
