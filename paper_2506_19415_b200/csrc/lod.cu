@@ -335,12 +335,18 @@ __device__ __forceinline__ void lod_page(const LodArgs& a, Shared& sh) {
 
   if (a.k_fixed < 0) {
     // merge_cluster of all rows (lod.py:134-154)
-    if (phase == 1) return;
-    for (int i = tid; i < m; i += NT) asg[i] = 0;
+    if constexpr (phase == 1) {
+      return;
+    } else {
+      for (int i = tid; i < m; i += NT) asg[i] = 0;
+    }
   } else if (k >= m) {
     // cluster_page: k >= m -> arange(m), no draws (lod.py:96-97)
-    if (phase == 1) return;
-    for (int i = tid; i < m; i += NT) asg[i] = i;
+    if constexpr (phase == 1) {
+      return;
+    } else {
+      for (int i = tid; i < m; i += NT) asg[i] = i;
+    }
   } else if (phase == 1) {
     __syncthreads();  // glive complete
     // features (lod.py:44-59)
