@@ -62,6 +62,11 @@ constexpr int kRBlock = 256;  // threads; one per digit bin
 constexpr int kRWarps = kRBlock / 32;
 constexpr int kRItems = 12;
 constexpr int kRTile = kRBlock * kRItems;  // 3072 pairs per tile
+// sorts of up to kRSmallMax pairs (the per-frame depth sort) use half-size
+// tiles: twice the CTAs on a grid that would otherwise leave SMs idle
+constexpr int kRItemsSmall = 6;
+constexpr int kRTileSmall = kRBlock * kRItemsSmall;
+constexpr uint32_t kRSmallMax = 1u << 21;
 
 // ------------------------------------------------ single-pass primitives
 // Decoupled look-back (Merrill & Garland): tiles are claimed in order through
@@ -190,14 +195,14 @@ __global__ void __launch_bounds__(kRBlock) radix_hist_k(const uint32_t* __restri
                                                         int begin_bit, int end_bit,
                                                         uint32_t* __restrict__ ghist,
                                                         uint32_t* __restrict__ status,
-                                                        size_t pass_stride) {
+                                                        size_t pass_stride, uint32_t tile_items) {
   pdl_wait();
   __shared__ uint32_t h[4][256];
   for (int i = threadIdx.x; i < 4 * 256; i += kRBlock) (&h[0][0])[i] = 0;
   __syncthreads();
   const uint32_t n = load_n(n_dev, n_host);
   const int passes = (end_bit - begin_bit + 7) / 8;
-  const size_t used = (size_t)((n + kRTile - 1) / kRTile) * 256;
+  const size_t used = (size_t)((n + tile_items - 1) / tile_items) * 256;
   for (int p = 0; p < passes; ++p)
     for (size_t i = blockIdx.x * (size_t)kRBlock + threadIdx.x; i < used;
          i += (size_t)gridDim.x * kRBlock)
@@ -217,6 +222,7 @@ __global__ void __launch_bounds__(kRBlock) radix_hist_k(const uint32_t* __restri
   }
 }
 
+template <int kItems>
 __global__ void __launch_bounds__(kRBlock) radix_onesweep_k(
     const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin,
     uint32_t* __restrict__ kout, uint32_t* __restrict__ vout, const uint32_t* n_dev,
@@ -224,8 +230,8 @@ __global__ void __launch_bounds__(kRBlock) radix_onesweep_k(
     uint32_t* status, uint32_t* counter) {
   pdl_wait();
   __shared__ uint32_t wcnt[kRWarps][257];
-  __shared__ uint32_t skey[kRTile];
-  __shared__ uint32_t sval[kRTile];
+  __shared__ uint32_t skey[kRBlock * kItems];
+  __shared__ uint32_t sval[kRBlock * kItems];
   __shared__ uint32_t dbase[256];
   __shared__ uint32_t run[256];
   __shared__ uint32_t tpre[256];
@@ -233,7 +239,7 @@ __global__ void __launch_bounds__(kRBlock) radix_onesweep_k(
   __shared__ uint32_t s_tile;
 
   const uint32_t n = load_n(n_dev, n_host);
-  const uint32_t n_tiles = (n + kRTile - 1) / kRTile;
+  const uint32_t n_tiles = (n + (kRBlock * kItems) - 1) / (kRBlock * kItems);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   {
     uint32_t all;
@@ -245,12 +251,12 @@ __global__ void __launch_bounds__(kRBlock) radix_onesweep_k(
     __syncthreads();
     const uint32_t t = s_tile;
     if (t >= n_tiles) break;
-    const uint32_t base = t * kRTile;
-    const uint32_t hi = min(n, base + kRTile);
-    uint32_t k[kRItems], v[kRItems], d[kRItems], rk[kRItems];
-    const uint32_t wbase = base + warp * 32 * kRItems;
+    const uint32_t base = t * (kRBlock * kItems);
+    const uint32_t hi = min(n, base + (kRBlock * kItems));
+    uint32_t k[kItems], v[kItems], d[kItems], rk[kItems];
+    const uint32_t wbase = base + warp * 32 * kItems;
 #pragma unroll
-    for (int it = 0; it < kRItems; ++it) {
+    for (int it = 0; it < kItems; ++it) {
       const uint32_t idx = wbase + it * 32 + lane;
       const bool ok = idx < hi;
       k[it] = ok ? kin[idx] : 0u;
@@ -258,7 +264,7 @@ __global__ void __launch_bounds__(kRBlock) radix_onesweep_k(
       d[it] = ok ? ((k[it] >> shift) & mask) : 256u;
     }
 #pragma unroll
-    for (int it = 0; it < kRItems; ++it) {
+    for (int it = 0; it < kItems; ++it) {
       const uint32_t peers = __match_any_sync(0xffffffffu, d[it]);
       const uint32_t before = wcnt[warp][d[it]];
       rk[it] = before + __popc(peers & lanemask_lt());
@@ -289,7 +295,7 @@ __global__ void __launch_bounds__(kRBlock) radix_onesweep_k(
     tpre[threadIdx.x] = block_exclusive<kRBlock>(tot, scratch, &all);
     __syncthreads();
 #pragma unroll
-    for (int it = 0; it < kRItems; ++it) {
+    for (int it = 0; it < kItems; ++it) {
       if (d[it] < 256u) {
         const uint32_t lp = tpre[d[it]] + wcnt[warp][d[it]] + rk[it];
         skey[lp] = k[it];
@@ -362,7 +368,9 @@ int32_t scan_exclusive_u32(const uint32_t* in, uint32_t* out, const uint32_t* n_
 size_t radix_clear_bytes() { return sizeof(uint32_t) * (64 + 4 * 256); }
 
 size_t radix_ws_bytes(uint32_t n_max) {
-  const size_t tiles = ((size_t)n_max + kRTile - 1) / kRTile;
+  size_t tiles = ((size_t)n_max + kRTile - 1) / kRTile;
+  const size_t small = ((size_t)std::min(n_max, kRSmallMax) + kRTileSmall - 1) / kRTileSmall;
+  if (small > tiles) tiles = small;
   return sizeof(uint32_t) * (64 + 4 * 256 + 4 * 256 * tiles) + 256;
 }
 
@@ -386,7 +394,8 @@ int32_t radix_passes_u32(uint32_t* k0, uint32_t* v0, uint32_t* k1, uint32_t* v1,
   }
   const RadixLayout l = radix_layout(ws, n_max);
   const size_t tiles = l.pass_stride / 256;
-  const int grid = persistent_grid((const void*)radix_onesweep_k, kRBlock, tiles ? (int)tiles : 1);
+  const int grid = persistent_grid((const void*)radix_onesweep_k<kRItems>, kRBlock,
+                                   tiles ? (int)tiles : 1);
   int alt = 0;
   for (int p = 0; p < passes; ++p) {
     const int b = begin_bit + 8 * p;
@@ -394,7 +403,7 @@ int32_t radix_passes_u32(uint32_t* k0, uint32_t* v0, uint32_t* k1, uint32_t* v1,
     const uint32_t mask = (1u << bits) - 1u;
     uint32_t *ki = alt ? k1 : k0, *vi = alt ? v1 : v0;
     uint32_t *ko = alt ? k0 : k1, *vo = alt ? v0 : v1;
-    VMS_CUDA(launch(radix_onesweep_k, grid, kRBlock, 0, s, (const uint32_t*)ki,
+    VMS_CUDA(launch(radix_onesweep_k<kRItems>, grid, kRBlock, 0, s, (const uint32_t*)ki,
                     (const uint32_t*)vi, ko, vo, n_dev, 0u, b, mask,
                     (const uint32_t*)(l.ghist + p * 256), l.status + p * l.pass_stride,
                     l.counters + p));
@@ -414,7 +423,9 @@ int32_t radix_sort_u32(uint32_t* k0, uint32_t* v0, uint32_t* k1, uint32_t* v1,
     set_error("radix_sort_u32: at most 32 key bits");
     return VMS_ERR_INVALID;
   }
-  const size_t tiles = ((size_t)n_max + kRTile - 1) / kRTile;
+  const bool small = n_max <= kRSmallMax;
+  const uint32_t tile_items = small ? kRTileSmall : kRTile;
+  const size_t tiles = ((size_t)n_max + tile_items - 1) / tile_items;
   uint32_t* counters = static_cast<uint32_t*>(ws);  // one per pass
   uint32_t* ghist = counters + 64;                  // [passes][256]
   uint32_t* status = ghist + 4 * 256;               // [passes][tiles][256]
@@ -423,9 +434,10 @@ int32_t radix_sort_u32(uint32_t* k0, uint32_t* v0, uint32_t* k1, uint32_t* v1,
   const int hgrid = persistent_grid((const void*)radix_hist_k, kRBlock,
                                     (int)std::min<size_t>(2 * 148, (n_max + 4095) / 4096 + 1));
   VMS_CUDA(launch(radix_hist_k, hgrid, kRBlock, 0, s, (const uint32_t*)k0, n_dev, n_host,
-                  begin_bit, end_bit, ghist, status, (size_t)(256 * tiles)));
+                  begin_bit, end_bit, ghist, status, (size_t)(256 * tiles), tile_items));
   mark("radix_hist", s);
-  const int grid = persistent_grid((const void*)radix_onesweep_k, kRBlock, tiles ? (int)tiles : 1);
+  auto* kern = small ? radix_onesweep_k<kRItemsSmall> : radix_onesweep_k<kRItems>;
+  const int grid = persistent_grid((const void*)kern, kRBlock, tiles ? (int)tiles : 1);
   int alt = 0;
   for (int p = 0; p < passes; ++p) {
     const int b = begin_bit + 8 * p;
@@ -433,7 +445,7 @@ int32_t radix_sort_u32(uint32_t* k0, uint32_t* v0, uint32_t* k1, uint32_t* v1,
     const uint32_t mask = (1u << bits) - 1u;
     uint32_t *ki = alt ? k1 : k0, *vi = alt ? v1 : v0;
     uint32_t *ko = alt ? k0 : k1, *vo = alt ? v0 : v1;
-    VMS_CUDA(launch(radix_onesweep_k, grid, kRBlock, 0, s, (const uint32_t*)ki,
+    VMS_CUDA(launch(kern, grid, kRBlock, 0, s, (const uint32_t*)ki,
                     (const uint32_t*)vi, ko, vo, n_dev, n_host, b, mask,
                     (const uint32_t*)(ghist + p * 256), status + (size_t)p * 256 * tiles,
                     counters + p));
