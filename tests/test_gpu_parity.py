@@ -695,3 +695,24 @@ def test_certified_fast_blend_c2_within_contract(cuda, c2_scene):
     print(f"certified fast blend: worst max-abs {worst:.2e}; flagged pixels per frame "
           f"min {min(flagged)} median {int(np.median(flagged))} max {max(flagged)}")
     assert max(flagged) > 0
+
+
+def test_certified_blend_banded_output_identical(cuda):
+    """The certified fast blend through every output path - device tensor,
+    page-locked (zero-copy), pageable (banded blend + copy, a repair launch
+    per band) - gives the same image."""
+    from paper_2506_19415_b200.runtime import VmSession
+
+    sc = _city()
+    path = inputs.city_path(inputs.CITY_SMALL)
+    a = VmSession(sc, buffer_pages=16, staging_pages=6.0, vis_scale=0.5, exact=False)
+    b = VmSession(sc, buffer_pages=16, staging_pages=6.0, vis_scale=0.5, exact=False)
+    cam0 = path.frame_camera(0)
+    pageable = np.empty((cam0.height, cam0.width, 3), np.float32)
+    for f in range(path.frame_count):
+        cam = path.frame_camera(f)
+        dev, _ = a.render_frame(cam, f, out="device")
+        a.flush()
+        ref = dev.cpu().numpy()
+        img, _ = b.render_frame(cam, f, out=pageable)
+        assert np.array_equal(img, ref), f
