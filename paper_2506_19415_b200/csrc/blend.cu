@@ -478,8 +478,9 @@ __global__ void __launch_bounds__(kBlendThreads, kSparse ? 3 : 4) blend_k(const 
   uint32_t certN = 0;
   bool certFlag = false;
   const double fx = (double)px + 0.5, fy = (double)py + 0.5;
+  // the batch loop's one end-of-batch barrier also decides the early exit
+  // (every pixel of the sub-tile finished); the first batch always runs
   for (uint32_t base = start; base < end; base += kBlendThreads) {
-    if (__syncthreads_and(T < kStopF)) break;
     const uint32_t i = base + threadIdx.x;
     bool hit = false;
     BlendRec r;
@@ -744,7 +745,7 @@ __global__ void __launch_bounds__(kBlendThreads, kSparse ? 3 : 4) blend_k(const 
         }
       }
     }
-    __syncthreads();
+    if (__syncthreads_and(T < kStopF)) break;
   }
   if (cert_cnt && inside) {
     // colour: the accumulated bound plus one f32 ulp per step of the final
