@@ -69,15 +69,15 @@ def _run_pair(scene, traj, image_frames, last, **kw):
 
 
 def test_c3_frames_match_oracle(cuda, c3_scene):
-    """C3 at 1080p with the bench's 4096-page buffer: frames 0-48 of the
+    """C3 at 1080p with the bench's 4096-page buffer: the whole 120-frame
     path with page sets, plans, residency and stats bit-exact on every frame
-    and full images at frames 12, 30 and 48 (up to 8.4M resident records per
-    frame on both sides)."""
+    and full images at frames 12, 30, 48, 80 and 119 (up to 8.4M resident
+    records per frame on both sides)."""
     from paper_2506_19415_b200 import scenegen
 
     traj = scenegen.street_path(scenegen.C3, frames=120)
-    worst, req, s = _run_pair(c3_scene, traj, {12, 30, 48}, 48, buffer_pages=C3_BUFFER,
-                              staging_pages=40, vis_scale=0.25)
+    worst, req, s = _run_pair(c3_scene, traj, {12, 30, 48, 80, 119}, 119,
+                              buffer_pages=C3_BUFFER, staging_pages=40, vis_scale=0.25)
     assert s.dot_mode_exact
     assert max(req) > 100
     print(f"C3 1080p: worst max-abs {worst:.2e}, required pages {min(req)}-{max(req)}")
