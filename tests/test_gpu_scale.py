@@ -84,13 +84,13 @@ def test_c3_frames_match_oracle(cuda, c3_scene):
 
 
 def test_c3_4k_frames_match_oracle(cuda, c3_scene):
-    """C5's resolution on the C3 scene: 3840x2160 (vis 960x540), frames 0-24
-    with stats bit-exact on every frame and full 4K images at frames 8 and
-    24."""
+    """C5's resolution on the C3 scene: 3840x2160 (vis 960x540), frames 0-60
+    with stats bit-exact on every frame and full 4K images at frames 8, 24
+    and 60."""
     from paper_2506_19415_b200 import scenegen
 
     traj = scenegen.street_path(scenegen.C3, frames=120, width=3840, height=2160)
-    worst, req, _ = _run_pair(c3_scene, traj, {8, 24}, 24, buffer_pages=C3_BUFFER,
+    worst, req, _ = _run_pair(c3_scene, traj, {8, 24, 60}, 60, buffer_pages=C3_BUFFER,
                               staging_pages=40, vis_scale=0.25)
     print(f"C3 4K: worst max-abs {worst:.2e}, required pages {min(req)}-{max(req)}")
 
