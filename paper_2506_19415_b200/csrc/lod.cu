@@ -189,7 +189,7 @@ VMS_DEV double dot4(const double* q, const double* r) {
 struct Shared {
   Philox rng;
   double total, u, prev_inertia;
-  int idx, changed, any_empty, n_live, k, stop, leaves, nodes, plan_n;
+  int idx, changed, any_empty, n_live, k, stop, leaves, nodes;
   int leaf_off[kMaxLeaves], leaf_n[kMaxLeaves], node_l[kMaxLeaves], node_r[kMaxLeaves];
   double leaf_sum[kMaxLeaves], node_sum[kMaxLeaves];
   double ctr[kFeat];
@@ -199,14 +199,16 @@ struct Shared {
 // block-wide pairwise sum of a[0..n) in shared memory: the leaves on
 // separate threads, then thread 0 adds the internal nodes in post-order
 // (the recursion's order); result in sh.total.  The shape is built once
-// per n (sh.plan_n, reset to -1 at kernel start).
-__device__ void block_pw(Shared& sh, const double* a, int n) {
-  if (threadIdx.x == 0 && sh.plan_n != n) {
-    int nl = 0, nn = 0;
-    pw_build(0, n, sh.leaf_off, sh.leaf_n, nl, sh.node_l, sh.node_r, nn);
-    sh.leaves = nl;
-    sh.nodes = nn;
-    sh.plan_n = n;
+// per n (plan_n: thread 0's record of the n it was built for, -1 at first).
+__device__ void block_pw(Shared& sh, const double* a, int n, int& plan_n) {
+  if (threadIdx.x == 0) {
+    if (plan_n != n) {
+      int nl = 0, nn = 0;
+      pw_build(0, n, sh.leaf_off, sh.leaf_n, nl, sh.node_l, sh.node_r, nn);
+      sh.leaves = nl;
+      sh.nodes = nn;
+      plan_n = n;
+    }
   }
   __syncthreads();
   auto at = [a](int i) { return a[i]; };
@@ -277,7 +279,7 @@ __device__ int g_lod_prof = 0;  // VMSPLAT_LOD_PROF=1: per-section clocks of pag
 template <int phase>
 __device__ __forceinline__ void lod_page(const LodArgs& a, Shared& sh) {
   extern __shared__ __align__(16) unsigned char smem[];
-  if (threadIdx.x == 0) sh.plan_n = -1;
+  int plan_n = -1;  // block_pw's shape cache (thread 0)
   const uint32_t page = blockIdx.x;
   const int R = (int)a.rows_in, K = (int)a.k_cap;
   double* d2 = reinterpret_cast<double*>(smem);
@@ -379,7 +381,7 @@ __device__ __forceinline__ void lod_page(const LodArgs& a, Shared& sh) {
     };
     for (int c = 0; c < k; ++c) {
       if (c > 0) {
-        block_pw(sh, d2, m);
+        block_pw(sh, d2, m, plan_n);
         tick(0);
         const double total = sh.total;
         if (!(total > 0.0)) {
@@ -491,7 +493,7 @@ __device__ __forceinline__ void lod_page(const LodArgs& a, Shared& sh) {
         }
       }
       __syncthreads();
-      block_pw(sh, d2, m);
+      block_pw(sh, d2, m, plan_n);
       if (tid == 0) {
         const double inertia = sh.total, prev = sh.prev_inertia;
         if (inertia > dadd(prev, dmul(1e-9, fmax(1.0, prev)))) {
