@@ -26,11 +26,16 @@ def main():
     from paper_2506_19415_b200.scene_io import read_scene
 
     class A:
-        scene_dir = os.environ.get("VMSPLAT_SCENE_DIR", "/tmp/vmsplat_bench")
+        scene_dir = os.environ.get("VMSPLAT_SCENE_DIR")
+        config = "c2"
+        frames = 120
+        width = 1920
+        height = 1080
+        upload_mode = None
 
     lay, path = bench.ensure_scene(A, 0)
     scene = read_scene(path, mmap_gaussians=True)
-    traj = scenegen.street_path(lay, frames=120)
+    traj = bench.trajectory(A, lay)
     s = VmSession(scene, exact=not a.fast, timing=False)
     for f in range(a.warm):
         s.render_frame(traj.frame_camera(f), f, out="device")
