@@ -585,8 +585,10 @@ def run_ours(args, rank, world, local_rank):
                      "bytes_per_launch": round((blend_bytes if dominant == "blend" else pre_bytes)
                                                / len(stats_t)),
                      "limiter": ("not HBM: the exact blend's inputs are L2-resident (traffic "
-                                 "<< algorithmic bytes); it is bound by FP64 + XU issue and "
-                                 "per-warp FP64 latency (limits: ncu of the same kernel)")
+                                 "<< algorithmic bytes); it is issue-bound (limits: ncu of the "
+                                 "same kernel) and, on the vanishing-point frames, waits at "
+                                 "the end-of-batch barrier for the 8x4 blocks that reach the sky "
+                                 "(DESIGN section 4)")
                      if dominant == "blend" else "HBM read of the resident records",
                      "limits": limits},
         "frame_roofline": {"hbm_bytes": int(hbm_b), "pcie_bytes": int(pcie_b),
