@@ -6,8 +6,9 @@ reference module: ``build_pyramid`` returns the reference's level arrays bit
 for bit, ``cluster_page`` the reference's assignment (and advances the
 caller's Philox ``Generator`` exactly as the reference's draws do),
 ``merge_cluster`` the reference's merged record.  All three run the
-``lod_page_k`` kernel (csrc/lod.cu) through the C ABI ``vms_lod_level``; one
-CTA clusters and merges one page, every page of a level in one launch.
+kernels of csrc/lod.cu through the C ABI ``vms_lod_level``: per page one
+CTA seeds k-means++ (``lod_seed_k``) and one runs the Lloyd iterations and
+the merge (``lod_lloyd_k``), every page of a level in the same launches.
 There is no CPU path: without a GPU these raise ``CudaError``.
 
 Limits of this implementation: at most 4096 records per page (the k-means
