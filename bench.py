@@ -271,10 +271,12 @@ def launches_per_frame(stats, n_faces, upload_mode, n_pages=1000, device_table=F
                          chunk-table sums / scan / emit kernels)         +4
       render graph      preprocess, scan, compact, radix hist + 4 passes,
                         dup_count, scan, dup_emit, tile_prep, 2 radix
-                        passes, blend                                    16
+                        passes, blend                                    15
                         (exact blend: hot_list_k + blend_hot_k on the
                          forked stream; fast blend: blend_repair_k)      +2 / +1
-    (host output without zero-copy runs the blend as 4 band launches)."""
+    (host output without zero-copy runs the blend as 4 band launches).
+    Checked against the ncu launch list of the bench command
+    (profiles/r2/launches_bench.csv: 26.9 launches per frame)."""
     vis = 5 if n_pages <= 32767 else 8
     if n_faces >= 65536 and os.environ.get("VMSPLAT_VIS_BIN", "") != "0":
         vis += 10
@@ -283,7 +285,7 @@ def launches_per_frame(stats, n_faces, upload_mode, n_pages=1000, device_table=F
         up = 2 if upload_mode == 1 else 1
     if device_table:
         vis += 4
-    render = 16 + (2 if exact else 1)
+    render = 15 + (2 if exact else 1)
     return vis + up + render
 
 
