@@ -593,6 +593,14 @@ def run_ours(args, rank, world, local_rank):
                                  "(DESIGN section 4)")
                      if dominant == "blend" else "HBM read of the resident records",
                      "limits": limits},
+        # the roofline that binds the blend: SM issue (4 warp-instructions per
+        # cycle per SM), from the same ncu capture of the kernel
+        "roofline_issue": ({"bound": "issue", "kernel": dominant, "achieved": limits["ipc"],
+                            "peak": 4.0, "unit": "warp-instr/cycle/SM",
+                            "frac": round(limits["ipc"] / 4.0, 3),
+                            "fp64_pipe_frac": round(limits.get("fp64_pct", 0.0) / 100.0, 3),
+                            "source": limits.get("source"), "frame": limits.get("frame")}
+                           if limits and "ipc" in limits else None),
         "frame_roofline": {"hbm_bytes": int(hbm_b), "pcie_bytes": int(pcie_b),
                            "fps": round(1.0 / t_roof, 1),
                            "frac": round((args.steps / sum(s["time_device_frame"]
