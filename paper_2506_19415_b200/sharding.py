@@ -1,9 +1,10 @@
 """View sharding across GPUs.
 
 Independent camera views of a trajectory are split into contiguous blocks,
-one per rank; every rank owns a full session (page table, device page pool,
-pinned host copy of the scene) and renders only its block, so there is no
-data-path collective.  The only collective is the final gather of per-frame
+one per rank; every rank owns a full session (page table, device page pool)
+over the one shared host-resident scene (a tmpfs `.vms` page-locked in
+place by every rank, runtime.HostScene) and renders only its block, so there
+is no data-path collective.  The only collective is the final gather of per-frame
 stats rows (and optionally images) to rank 0 — NCCL over NVLink on GPUs, gloo
 in the CPU tests.  Frame indices stay global, so each shard's page-table LRU
 stamps match a single-process session started at the block's first frame.
