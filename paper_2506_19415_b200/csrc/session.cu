@@ -159,6 +159,13 @@ struct vms_session {
   bool pending_out[2] = {false, false};
   cudaEvent_t ev_vis = nullptr, ev_copy = nullptr, ev_staging = nullptr;
   cudaEvent_t ev_done[2] = {nullptr, nullptr};
+  // cross-frame overlap: frame i's front (scatter, preprocess, sorts, tile
+  // lists) runs on front_stream[i & 1] while frame i - 1 blends on the
+  // caller's stream; ev_pre = that parity's preprocess has read the pool,
+  // ev_front = its tile lists are ready for the blend
+  bool overlap = true;
+  cudaStream_t front_stream[2] = {nullptr, nullptr};
+  cudaEvent_t ev_pre[2] = {nullptr, nullptr}, ev_front[2] = {nullptr, nullptr};
   cudaEvent_t tev[10] = {};
   // pinned host memory
   uint32_t* req_pid = nullptr;
@@ -177,8 +184,8 @@ struct vms_session {
   // device memory owned by the session
   vms_copy* scatter_d = nullptr;
   vms_chunk* chunks_d = nullptr;
-  void* ws = nullptr;  // render workspace
-  size_t ws_bytes = 0;
+  void* ws = nullptr;  // render workspaces, one per frame parity
+  size_t ws_bytes = 0, ws_stride = 0;
   uint32_t m_cap = 0, m_want = 0;
   uint32_t m_limit = 1u << 26;  // largest tile-instance buffer the session grows to
   bool trace = false;
@@ -200,7 +207,8 @@ struct vms_session {
   int64_t max_chunks = 0;
   int parity = 0;
   bool use_graphs = true;
-  Graph vis_graph[2], render_graph[2][2];  // vis: [parity] (device table); render: [timing][banded]
+  // vis: [parity] (device table); front: [parity][timing][banded]; blend: [parity][timing]
+  Graph vis_graph[2], front_graph[2][2][2], blend_graph[2][2];
   // device page table (desc.device_table): its outputs land in mapped memory
   // (plan, stats) and per-parity device chunk tables; the next frame of the
   // same parity waits for ev_chunks before its update overwrites them
@@ -224,6 +232,14 @@ struct vms_session {
 namespace vms {
 namespace {
 
+void reset_render_graphs(vms_session* s) {
+  for (auto& gp : s->front_graph)
+    for (auto& gt : gp)
+      for (auto& g : gt) g.reset();
+  for (auto& gp : s->blend_graph)
+    for (auto& g : gp) g.reset();
+}
+
 void free_session(vms_session* s) {
   if (!s) return;
   for (auto& g : s->vis_graph) g.reset();
@@ -235,17 +251,18 @@ void free_session(vms_session* s) {
     if (p) cudaFreeHost(p);
   for (vms_chunk* p : s->chunks_dev)
     if (p) cudaFree(p);
-  for (auto& gt : s->render_graph)
-    for (auto& g : gt) g.reset();
+  reset_render_graphs(s);
   if (s->pt) vms_pt_destroy(s->pt);
-  for (cudaStream_t x : {s->vis_stream, s->copy_stream, s->cap_stream, s->d2h_stream})
+  for (cudaStream_t x : {s->vis_stream, s->copy_stream, s->cap_stream, s->d2h_stream,
+                         s->front_stream[0], s->front_stream[1]})
     if (x) cudaStreamDestroy(x);
   for (cudaEvent_t e : s->ev_band)
     if (e) cudaEventDestroy(e);
   for (cudaEvent_t e : s->ev_out)
     if (e) cudaEventDestroy(e);
   if (s->ev_d2h) cudaEventDestroy(s->ev_d2h);
-  for (cudaEvent_t e : {s->ev_vis, s->ev_copy, s->ev_staging, s->ev_done[0], s->ev_done[1]})
+  for (cudaEvent_t e : {s->ev_vis, s->ev_copy, s->ev_staging, s->ev_done[0], s->ev_done[1],
+                        s->ev_pre[0], s->ev_pre[1], s->ev_front[0], s->ev_front[1]})
     if (e) cudaEventDestroy(e);
   for (cudaEvent_t e : s->tev)
     if (e) cudaEventDestroy(e);
@@ -276,16 +293,17 @@ int32_t ensure_ws(vms_session* s, int w, int h, uint32_t m_cap) {
   if (s->ws && s->ws_w == w && s->ws_h == h && s->m_cap >= m_cap) return VMS_OK;
   const auto t0 = std::chrono::steady_clock::now();
   const uint32_t n_cap = s->d.capacity * s->d.page_size;
-  const size_t bytes = render_ws_bytes(n_cap, m_cap, tile_count(w, h));
+  const size_t one = (render_ws_bytes(n_cap, m_cap, tile_count(w, h)) + 4095) & ~(size_t)4095;
+  const size_t bytes = 2 * one;  // frames of the two parities are in flight together
   if (s->ws) {
     VMS_CUDA(cudaDeviceSynchronize());
     VMS_CUDA(cudaFree(s->ws));
     s->ws = nullptr;
   }
-  for (auto& gt : s->render_graph)
-    for (auto& g : gt) g.reset();
+  reset_render_graphs(s);
   VMS_CUDA(cudaMalloc(&s->ws, bytes));
   s->ws_bytes = bytes;
+  s->ws_stride = one;
   s->m_cap = m_cap;
   s->ws_w = w;
   s->ws_h = h;
@@ -294,6 +312,11 @@ int32_t ensure_ws(vms_session* s, int w, int h, uint32_t m_cap) {
             m_cap, bytes / 1e6,
             std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
   return VMS_OK;
+}
+
+RenderWs ws_of(const vms_session* s, int par) {
+  return render_carve(static_cast<char*>(s->ws) + (size_t)par * s->ws_stride,
+                      s->d.capacity * s->d.page_size, s->m_cap, tile_count(s->ws_w, s->ws_h));
 }
 
 int32_t ensure_staging(vms_session* s, size_t bytes) {
@@ -364,33 +387,53 @@ int32_t run_captured(vms_session* s, Graph& g, int w, int h, uint32_t m_cap, F&&
   return VMS_OK;
 }
 
-int32_t launch_render(vms_session* s, int w, int h, bool timing, bool banded, cudaStream_t st) {
-  RenderWs ws = render_carve(s->ws, s->d.capacity * s->d.page_size, s->m_cap, tile_count(w, h));
+// The frame's front - memsets, preprocess, depth sort, tile lists - on
+// stream fs (one graph per parity/timing/banded), recording ev_pre[par] once
+// the preprocess has read the pool and ev_front[par] at its end.
+int32_t launch_front(vms_session* s, int par, int w, int h, bool timing, bool banded,
+                     cudaStream_t fs) {
+  const RenderWs ws = ws_of(s, par);
   const uint32_t max_chunks = (uint32_t)s->max_chunks;
   auto enqueue = [&](cudaStream_t q, bool captured) -> int32_t {
     void* ev[4] = {nullptr, nullptr, nullptr, nullptr};
     if (timing)
       for (int i = 0; i < 4; ++i) ev[i] = s->tev[4 + i];
+    const unsigned rf = captured ? cudaEventRecordExternal : cudaEventRecordDefault;
     mark("begin", q);
     int32_t rc = render_clear(w, h, ws, q);
     if (rc) return rc;
     rc = render_preprocess(s->d.pool, s->chunks_d, max_chunks, ws, q);
     if (rc) return rc;
-    if (timing)
-      VMS_CUDA(cudaEventRecordWithFlags(s->tev[4], q,
-                                        captured ? cudaEventRecordExternal : cudaEventRecordDefault));
-    return render_finish(w, h, ws, 0, s->d.exact, ev, captured, banded ? -kBands : 1, q);
+    VMS_CUDA(cudaEventRecordWithFlags(s->ev_pre[par], q, rf));
+    if (timing) VMS_CUDA(cudaEventRecordWithFlags(s->tev[4], q, rf));
+    return render_finish(w, h, ws, 0, s->d.exact, ev, captured, banded ? -kBands : -1, q);
   };
-  int32_t rc = run_captured(s, s->render_graph[timing ? 1 : 0][banded ? 1 : 0], w, h, s->m_cap,
-                            enqueue, st);
-  if (rc || !banded) return rc;
-  // banded: the blend bands are launched after the graph, each followed by
-  // an event the image copy of that band waits for
-  for (int b = 0; b < kBands; ++b) {
-    rc = render_band(w, h, ws, s->d.exact, b, kBands, st);
-    if (rc) return rc;
-    VMS_CUDA(cudaEventRecord(s->ev_band[b], st));
+  int32_t rc = run_captured(s, s->front_graph[par][timing ? 1 : 0][banded ? 1 : 0], w, h,
+                            s->m_cap, enqueue, fs);
+  if (rc) return rc;
+  VMS_CUDA(cudaEventRecord(s->ev_front[par], fs));
+  return VMS_OK;
+}
+
+// The frame's blend on the caller's stream st, after its front: one graph
+// per parity, or (host output, banded) one launch per band, each followed
+// by the event the band's image copy waits for.
+int32_t launch_blend(vms_session* s, int par, int w, int h, bool timing, bool banded,
+                     cudaStream_t st) {
+  const RenderWs ws = ws_of(s, par);
+  VMS_CUDA(cudaStreamWaitEvent(st, s->ev_front[par], 0));
+  int32_t rc = VMS_OK;
+  if (!banded) {
+    rc = run_captured(s, s->blend_graph[par][timing ? 1 : 0], w, h, s->m_cap,
+                      [&](cudaStream_t q, bool) { return render_band(w, h, ws, s->d.exact, 0, 1, q); },
+                      st);
+  } else {
+    for (int b = 0; b < kBands && !rc; ++b) {
+      rc = render_band(w, h, ws, s->d.exact, b, kBands, st);
+      if (!rc) VMS_CUDA(cudaEventRecord(s->ev_band[b], st));
+    }
   }
+  if (rc) return rc;
   if (timing) VMS_CUDA(cudaEventRecord(s->tev[7], st));
   return VMS_OK;
 }
@@ -477,6 +520,18 @@ vms_session* vms_session_create(const vms_session_desc* desc) {
   ok = ok && cudaStreamCreateWithFlags(&s->copy_stream, cudaStreamNonBlocking) == cudaSuccess;
   ok = ok && cudaStreamCreateWithFlags(&s->cap_stream, cudaStreamNonBlocking) == cudaSuccess;
   ok = ok && cudaStreamCreateWithFlags(&s->d2h_stream, cudaStreamNonBlocking) == cudaSuccess;
+  {
+    // VMSPLAT_OVERLAP=0: fronts on the caller's stream (no cross-frame
+    // overlap); VMSPLAT_FRONT_PRIO=0: front streams at default priority
+    const char* ov = std::getenv("VMSPLAT_OVERLAP");
+    s->overlap = !(ov && ov[0] == '0');
+    const char* fp = std::getenv("VMSPLAT_FRONT_PRIO");
+    const int prio = (fp && fp[0] == '0') ? lo : hi;
+    for (cudaStream_t& x : s->front_stream)
+      ok = ok && cudaStreamCreateWithPriority(&x, cudaStreamNonBlocking, prio) == cudaSuccess;
+    for (cudaEvent_t* e : {&s->ev_pre[0], &s->ev_pre[1], &s->ev_front[0], &s->ev_front[1]})
+      ok = ok && cudaEventCreateWithFlags(e, cudaEventDisableTiming) == cudaSuccess;
+  }
   for (cudaEvent_t& e : s->ev_band)
     ok = ok && cudaEventCreateWithFlags(&e, cudaEventDisableTiming) == cudaSuccess;
   ok = ok && cudaEventCreateWithFlags(&s->ev_d2h, cudaEventDisableTiming) == cudaSuccess;
@@ -563,9 +618,7 @@ int32_t vms_session_cert_count(vms_session* s, uint32_t* out) {
     set_error("session_cert_count: invalid arguments");
     return VMS_ERR_INVALID;
   }
-  RenderWs ws = render_carve(s->ws, s->d.capacity * s->d.page_size, s->m_cap,
-                             tile_count(s->ws_w, s->ws_h));
-  return debug_cert_count(ws, out);
+  return debug_cert_count(ws_of(s, s->last_par < 0 ? 0 : s->last_par), out);
 }
 
 int32_t vms_session_set_render_ws(vms_session* s, void* ws, uint64_t bytes, uint32_t m_cap,
@@ -773,43 +826,48 @@ int32_t vms_session_frame(vms_session* s, const vms_frame_args* a, vms_frame_sta
                              cudaMemcpyHostToDevice, s->copy_stream));
     VMS_CUDA(cudaEventRecord(s->ev_copy, s->copy_stream));
   }
-  // [4]-[6] on the main stream: pool slots are rewritten only after the
-  // previous render (stream order), then the frame block, chunk table, graph
+  // [4]-[6] the frame's front on this parity's front stream (the caller's
+  // stream in timing mode): pool slots are rewritten only after the previous
+  // frame's preprocess has read them (ev_pre), then the frame block, chunk
+  // table and the front graph.  Its workspace was last used by the frame two
+  // back, whose blend recycle() has waited for.
   const int W = a->cam.width, H = a->cam.height;
   rc = ensure_ws(s, W, H, s->m_cap > s->m_want ? s->m_cap : s->m_want);
   if (rc) return rc;
-  if (timing) VMS_CUDA(cudaEventRecord(s->tev[8], st));
+  cudaStream_t fs = (timing || !s->overlap) ? st : s->front_stream[par];
+  if (fs != st) VMS_CUDA(cudaStreamWaitEvent(fs, s->ev_pre[par ^ 1], 0));
+  if (timing) VMS_CUDA(cudaEventRecord(s->tev[8], fs));
   if (tl >= 0) {
     s->tl_host[tl][2] = now_us();
-    VMS_CUDA(cudaEventRecord(s->tl_ev[tl][2], st));
+    VMS_CUDA(cudaEventRecord(s->tl_ev[tl][2], fs));
   }
   if (n_plan) {
-    VMS_CUDA(cudaStreamWaitEvent(st, s->ev_copy, 0));
+    VMS_CUDA(cudaStreamWaitEvent(fs, s->ev_copy, 0));
     dim3 grid(64, (unsigned)(n_plan < 65535 ? n_plan : 65535));
-    scatter_k<<<grid, 256, 0, st>>>(s->scatter_d, n_plan, s->staging,
+    scatter_k<<<grid, 256, 0, fs>>>(s->scatter_d, n_plan, s->staging,
                                     reinterpret_cast<char*>(s->d.pool));
-    mark("scatter", st);
-    VMS_CUDA(cudaEventRecord(s->ev_staging, st));
+    mark("scatter", fs);
+    VMS_CUDA(cudaEventRecord(s->ev_staging, fs));
   }
-  RenderWs ws = render_carve(s->ws, s->d.capacity * s->d.page_size, s->m_cap, tile_count(W, H));
+  RenderWs ws = ws_of(s, par);
   FrameDev* f = s->fd_h[par];
   f->cam = a->cam;
   f->image = a->image;
   f->n_chunks = (uint32_t)n_chunks;
   f->n_splats = (uint32_t)n_res;
   f->counters_host = s->counters_h[par];  // mapped: written by tile_prep_k
-  VMS_CUDA(cudaMemcpyAsync(ws.fd, f, sizeof(FrameDev), cudaMemcpyHostToDevice, st));
+  VMS_CUDA(cudaMemcpyAsync(ws.fd, f, sizeof(FrameDev), cudaMemcpyHostToDevice, fs));
   if (n_chunks) {
     if (s->dpt) {
       VMS_CUDA(cudaMemcpyAsync(s->chunks_d, s->chunks_dev[par], sizeof(vms_chunk) * n_chunks,
-                               cudaMemcpyDeviceToDevice, st));
+                               cudaMemcpyDeviceToDevice, fs));
     } else {
       VMS_CUDA(cudaMemcpyAsync(s->chunks_d, s->chunks_h[par], sizeof(vms_chunk) * n_chunks,
-                               cudaMemcpyHostToDevice, st));
+                               cudaMemcpyHostToDevice, fs));
     }
   }
   if (s->dpt) {
-    VMS_CUDA(cudaEventRecord(s->ev_chunks[par], st));
+    VMS_CUDA(cudaEventRecord(s->ev_chunks[par], fs));
     s->chunks_pending[par] = true;
   }
   // host output: the blend runs as kBands launches over bands of tile rows
@@ -820,7 +878,9 @@ int32_t vms_session_frame(vms_session* s, const vms_frame_args* a, vms_frame_sta
   // NEXT frame's render (the image buffer is recycled only after the copy).
   const bool async_out = a->host_image != nullptr && !a->sync && !timing;
   const bool banded = a->host_image != nullptr && !async_out;
-  rc = launch_render(s, W, H, timing, banded, st);
+  rc = launch_front(s, par, W, H, timing, banded, fs);
+  if (rc) return rc;
+  rc = launch_blend(s, par, W, H, timing, banded, st);
   if (rc) return rc;
   if (async_out) {
     VMS_CUDA(cudaEventRecord(s->ev_band[0], st));

@@ -1,20 +1,38 @@
-"""Does a concurrent 25 MB device->host copy per frame slow the render?"""
-import os, sys, time
+"""Does a concurrent 25 MB copy per frame slow the render, and through what?
+
+Modes (C2, frames 5-64, frame left in HBM, fps from CUDA events):
+  none       no copy
+  d2h        the frame's image -> page-locked host (what the e2e path does)
+  d2h_unrel  an unrelated 25 MB device buffer -> page-locked host
+  h2d_unrel  page-locked host -> an unrelated device buffer (PCIe, other direction)
+  d2d_unrel  25 MB device -> device over the copy engine (HBM/L2 only, no PCIe)
+"""
+import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import bench
 from paper_2506_19415_b200 import scenegen
 from paper_2506_19415_b200.runtime import VmSession
 from paper_2506_19415_b200.scene_io import read_scene
+
+
 class A:
-    scene_dir = os.environ.get("VMSPLAT_SCENE_DIR", "/tmp/vmsplat_bench")
+    config = "c2"
+    scene_dir = None
+    frames = 120
+    width = 1920
+    height = 1080
+
+
 lay, path = bench.ensure_scene(A, 0)
 scene = read_scene(path, mmap_gaussians=True)
-traj = scenegen.street_path(lay, frames=120)
+traj = bench.trajectory(A, lay)
 x = torch.empty((1080, 1920, 3), device="cuda")
+y = torch.empty((1080, 1920, 3), device="cuda")
 hs = [torch.empty((1080, 1920, 3)).pin_memory() for _ in range(2)]
 side = torch.cuda.Stream()
-for mode in ("none", "d2h", "d2h_l2"):
+modes = sys.argv[1:] or ["none", "d2h", "d2h_unrel", "h2d_unrel", "d2d_unrel", "none"]
+for mode in modes:
     s = VmSession(scene, buffer_pages=500, staging_pages=40, vis_scale=0.25, timing=False)
     for f in range(5):
         s.render_frame(traj.frame_camera(f), f, out="device")
@@ -28,8 +46,15 @@ for mode in ("none", "d2h", "d2h_l2"):
             ev.record()
             side.wait_event(ev)
             with torch.cuda.stream(side):
-                hs[f % 2].copy_(img if mode == "d2h" else x, non_blocking=True)
+                if mode == "d2h":
+                    hs[f % 2].copy_(img, non_blocking=True)
+                elif mode == "d2h_unrel":
+                    hs[f % 2].copy_(x, non_blocking=True)
+                elif mode == "h2d_unrel":
+                    x.copy_(hs[f % 2], non_blocking=True)
+                else:
+                    y.copy_(x, non_blocking=True)
     e1.record()
     torch.cuda.synchronize()
-    print(mode, "fps", 60 / (e0.elapsed_time(e1) * 1e-3))
+    print(mode, "fps", round(60 / (e0.elapsed_time(e1) * 1e-3), 1), flush=True)
     del s

@@ -8,10 +8,14 @@ from paper_2506_19415_b200 import scenegen, harness
 from paper_2506_19415_b200.runtime import VmSession
 from paper_2506_19415_b200.scene_io import read_scene
 class A:
-    scene_dir = os.environ.get("VMSPLAT_SCENE_DIR", "/tmp/vmsplat_bench")
+    config = "c2"
+    scene_dir = None
+    frames = 120
+    width = 1920
+    height = 1080
 lay, path = bench.ensure_scene(A, 0)
 scene = read_scene(path, mmap_gaussians=True)
-traj = scenegen.street_path(lay, frames=120)
+traj = bench.trajectory(A, lay)
 s = VmSession(scene, buffer_pages=500, staging_pages=40, vis_scale=0.25, timing=False)
 got = []
 harness.run_benchmark(scene, traj, frames=range(0, 64), session=s, pipelined=True,

@@ -392,6 +392,38 @@ def test_c2_whole_trajectory_matches_oracle(cuda, c2_scene):
     print(f"C2: 120 frames, {len(C2_IMAGE_FRAMES)} images, worst max-abs {worst:.2e}")
 
 
+@pytest.mark.parametrize("upload_mode", [None, 2])
+def test_c2_overlapped_frames_identical_to_serial(cuda, c2_scene, upload_mode):
+    """Cross-frame overlap: without timing, frame i's front (page scatter,
+    preprocess, depth sort, tile lists) runs on its parity's front stream
+    while frame i - 1 blends on the caller's stream.  Frames 0-63 enqueued
+    back to back into a device frame stack (no host sync between frames,
+    pages streaming in on most of them) equal the serial timing-mode
+    session's frames bit for bit, with the same stats - including the
+    vanishing-point frames and a frame pair whose pool slots the second
+    frame's scatter rewrites right after the first frame's preprocess."""
+    import torch
+    from paper_2506_19415_b200 import scenegen
+    from paper_2506_19415_b200.runtime import VmSession
+
+    traj = scenegen.street_path(scenegen.C2, frames=120)
+    F = 64
+    ser = VmSession(c2_scene, timing=True, upload_mode=upload_mode)
+    ovl = VmSession(c2_scene, timing=False, upload_mode=upload_mode)
+    cam0 = traj.frame_camera(0)
+    stack = torch.empty((F, cam0.height, cam0.width, 3), dtype=torch.float32, device="cuda")
+    got = [ovl.render_frame(traj.frame_camera(f), f, out=stack[f])[1] for f in range(F)]
+    torch.cuda.synchronize()
+    copies = 0
+    for f in range(F):
+        img, st = ser.render_frame(traj.frame_camera(f), f)
+        for k in STAT_KEYS:
+            assert got[f][k] == st[k], (f, k)
+        copies += st["planned_copies"] > 0
+        assert np.array_equal(stack[f].cpu().numpy(), img), f
+    assert copies > 8
+
+
 def test_c2_render_is_deterministic(cuda, c2_scene):
     from paper_2506_19415_b200 import scenegen
     from paper_2506_19415_b200.runtime import VmSession
