@@ -383,11 +383,14 @@ int32_t vms_session_set_render_ws(vms_session* s, void* ws, uint64_t bytes, uint
  * frames after it. */
 int32_t vms_session_frame(vms_session* s, const vms_frame_args* args, vms_frame_stats* stats,
                           void* stream);
-/* Wait for the last frame (back = 0) or the one before it (back = 1): with
- * a device-accessible host image and sync = 0, vms_session_frame returns as
- * soon as the frame is enqueued and this is how the caller learns that the
- * image is complete. */
+/* Wait for the last frame (back = 0) or one of the frames before it (back <
+ * vms_session_slots): with a device-accessible host image and sync = 0,
+ * vms_session_frame returns as soon as the frame is enqueued and this is how
+ * the caller learns that the image is complete. */
 int32_t vms_session_wait(vms_session* s, int32_t back);
+/* Frames a session keeps in flight (2..4, VMSPLAT_SLOTS, default 3):
+ * vms_session_frame for frame i waits for frame i - slots. */
+int32_t vms_session_slots(const vms_session* s);
 /* Wait for the last frame; out4 = its n_kept, n_inst, overflow, n_need. */
 int32_t vms_session_counters(vms_session* s, uint32_t* out4, void* stream);
 

@@ -148,24 +148,31 @@ struct Graph {
 };
 }  // namespace
 
+// Frames in flight: frame i uses slot i % slots (its pinned host buffers,
+// render workspace, graphs, events); render_frame(i) recycles frame
+// i - slots.  Three slots let the host enqueue a frame while the two before
+// it still render / copy to the host (VMSPLAT_SLOTS=2..4).
+constexpr int kMaxSlots = 4;
+
 struct vms_session {
   vms_session_desc d;
+  int slots = 3;
   vms_pagetable* pt = nullptr;
   cudaStream_t vis_stream = nullptr, copy_stream = nullptr, cap_stream = nullptr;
   cudaStream_t d2h_stream = nullptr;  // banded image copies to the host
   cudaEvent_t ev_band[kBands] = {};
   cudaEvent_t ev_d2h = nullptr;
-  cudaEvent_t ev_out[2] = {nullptr, nullptr};  // asynchronous host copy of a frame done
-  bool pending_out[2] = {false, false};
+  cudaEvent_t ev_out[kMaxSlots] = {};  // asynchronous host copy of a frame done
+  bool pending_out[kMaxSlots] = {};
   cudaEvent_t ev_vis = nullptr, ev_copy = nullptr, ev_staging = nullptr;
-  cudaEvent_t ev_done[2] = {nullptr, nullptr};
+  cudaEvent_t ev_done[kMaxSlots] = {};
   // cross-frame overlap: frame i's front (scatter, preprocess, sorts, tile
   // lists) runs on front_stream[i & 1] while frame i - 1 blends on the
   // caller's stream; ev_pre = that parity's preprocess has read the pool,
   // ev_front = its tile lists are ready for the blend
   bool overlap = true;
-  cudaStream_t front_stream[2] = {nullptr, nullptr};
-  cudaEvent_t ev_pre[2] = {nullptr, nullptr}, ev_front[2] = {nullptr, nullptr};
+  cudaStream_t front_stream[kMaxSlots] = {};
+  cudaEvent_t ev_pre[kMaxSlots] = {}, ev_front[kMaxSlots] = {};
   cudaEvent_t tev[10] = {};
   // pinned host memory
   uint32_t* req_pid = nullptr;
@@ -174,12 +181,12 @@ struct vms_session {
   uint8_t* req_level = nullptr;
   uint32_t* req_meta = nullptr;
   vms::VisFrameDev* vis_fd_h = nullptr;
-  vms_copy* copies[2] = {nullptr, nullptr};    // host -> staging (per frame parity)
-  vms_copy* scatter_h[2] = {nullptr, nullptr};  // staging -> pool offsets
-  vms_chunk* chunks_h[2] = {nullptr, nullptr};
-  vms::FrameDev* fd_h[2] = {nullptr, nullptr};
-  uint32_t* counters_h[2] = {nullptr, nullptr};  // n_kept, n_inst, overflow, n_need
-  bool pending[2] = {false, false};
+  vms_copy* copies[kMaxSlots] = {};    // host -> staging (per frame parity)
+  vms_copy* scatter_h[kMaxSlots] = {};  // staging -> pool offsets
+  vms_chunk* chunks_h[kMaxSlots] = {};
+  vms::FrameDev* fd_h[kMaxSlots] = {};
+  uint32_t* counters_h[kMaxSlots] = {};  // n_kept, n_inst, overflow, n_need
+  bool pending[kMaxSlots] = {};
   int last_par = -1;
   // device memory owned by the session
   vms_copy* scatter_d = nullptr;
@@ -200,15 +207,15 @@ struct vms_session {
   char* staging = nullptr;
   size_t staging_bytes = 0;
   // upload_mode 2 (streaming source): page-locked bounce buffers per parity
-  char* bounce[2] = {nullptr, nullptr};
-  size_t bounce_bytes[2] = {0, 0};
+  char* bounce[kMaxSlots] = {};
+  size_t bounce_bytes[kMaxSlots] = {};
   CopyPool* pool = nullptr;
   std::vector<std::tuple<char*, const char*, size_t>> pieces;
   int64_t max_chunks = 0;
   int parity = 0;
   bool use_graphs = true;
-  // vis: [parity] (device table); front: [parity][timing][banded]; blend: [parity][timing]
-  Graph vis_graph[2], front_graph[2][2][2], blend_graph[2][2];
+  // vis: [slot] (device table); front: [slot][timing][banded]; blend: [slot][timing]
+  Graph vis_graph[kMaxSlots], front_graph[kMaxSlots][2][2], blend_graph[kMaxSlots][2];
   // device page table (desc.device_table): its outputs land in mapped memory
   // (plan, stats) and per-parity device chunk tables; the next frame of the
   // same parity waits for ev_chunks before its update overwrites them
@@ -218,10 +225,15 @@ struct vms_session {
   int32_t* dplan_entry = nullptr;
   int32_t* dplan_slot = nullptr;
   vms_dpt_stats* dstats = nullptr;
-  vms_dpt_frame* dframe = nullptr;
-  vms_chunk* chunks_dev[2] = {nullptr, nullptr};
-  cudaEvent_t ev_chunks[2] = {nullptr, nullptr};
-  bool chunks_pending[2] = {false, false};
+  vms_chunk* chunks_dev[kMaxSlots] = {};
+  cudaEvent_t ev_chunks[kMaxSlots] = {};
+  // the required list in device memory (the update reads it there: reads of
+  // mapped host memory stall behind a concurrent image copy on the bus)
+  uint32_t* dreq_pid = nullptr;
+  uint32_t* dreq_enc = nullptr;
+  uint8_t* dreq_direct = nullptr;
+  uint8_t* dreq_level = nullptr;
+  bool chunks_pending[kMaxSlots] = {};
   std::vector<uint64_t> level_start;  // first row of each level block
   std::vector<uint32_t> plan_pid;
   std::vector<int32_t> plan_order;
@@ -247,32 +259,37 @@ void free_session(vms_session* s) {
   for (cudaEvent_t e : s->ev_chunks)
     if (e) cudaEventDestroy(e);
   for (void* p : {(void*)s->dplan_pid, (void*)s->dplan_level, (void*)s->dplan_entry,
-                  (void*)s->dplan_slot, (void*)s->dstats, (void*)s->dframe})
+                  (void*)s->dplan_slot, (void*)s->dstats})
     if (p) cudaFreeHost(p);
   for (vms_chunk* p : s->chunks_dev)
     if (p) cudaFree(p);
+  for (void* p : {(void*)s->dreq_pid, (void*)s->dreq_enc, (void*)s->dreq_direct,
+                  (void*)s->dreq_level})
+    if (p) cudaFree(p);
   reset_render_graphs(s);
   if (s->pt) vms_pt_destroy(s->pt);
-  for (cudaStream_t x : {s->vis_stream, s->copy_stream, s->cap_stream, s->d2h_stream,
-                         s->front_stream[0], s->front_stream[1]})
+  for (cudaStream_t x : {s->vis_stream, s->copy_stream, s->cap_stream, s->d2h_stream})
     if (x) cudaStreamDestroy(x);
   for (cudaEvent_t e : s->ev_band)
     if (e) cudaEventDestroy(e);
   for (cudaEvent_t e : s->ev_out)
     if (e) cudaEventDestroy(e);
   if (s->ev_d2h) cudaEventDestroy(s->ev_d2h);
-  for (cudaEvent_t e : {s->ev_vis, s->ev_copy, s->ev_staging, s->ev_done[0], s->ev_done[1],
-                        s->ev_pre[0], s->ev_pre[1], s->ev_front[0], s->ev_front[1]})
+  for (cudaEvent_t e : {s->ev_vis, s->ev_copy, s->ev_staging})
     if (e) cudaEventDestroy(e);
   for (cudaEvent_t e : s->tev)
     if (e) cudaEventDestroy(e);
   for (void* p : {(void*)s->req_pid, (void*)s->req_enc, (void*)s->req_direct,
-                  (void*)s->req_level, (void*)s->req_meta, (void*)s->vis_fd_h,
-                  (void*)s->copies[0], (void*)s->copies[1], (void*)s->scatter_h[0],
-                  (void*)s->scatter_h[1], (void*)s->chunks_h[0], (void*)s->chunks_h[1],
-                  (void*)s->fd_h[0], (void*)s->fd_h[1], (void*)s->counters_h[0],
-                  (void*)s->counters_h[1]})
+                  (void*)s->req_level, (void*)s->req_meta, (void*)s->vis_fd_h})
     if (p) cudaFreeHost(p);
+  for (int k = 0; k < kMaxSlots; ++k) {
+    for (void* p : {(void*)s->copies[k], (void*)s->scatter_h[k], (void*)s->chunks_h[k],
+                    (void*)s->fd_h[k], (void*)s->counters_h[k]})
+      if (p) cudaFreeHost(p);
+    if (s->front_stream[k]) cudaStreamDestroy(s->front_stream[k]);
+    for (cudaEvent_t e : {s->ev_done[k], s->ev_pre[k], s->ev_front[k]})
+      if (e) cudaEventDestroy(e);
+  }
   for (void* p : {(void*)s->scatter_d, (void*)s->chunks_d, s->ws, (void*)s->staging})
     if (p) cudaFree(p);
   for (char* p : s->bounce)
@@ -294,7 +311,7 @@ int32_t ensure_ws(vms_session* s, int w, int h, uint32_t m_cap) {
   const auto t0 = std::chrono::steady_clock::now();
   const uint32_t n_cap = s->d.capacity * s->d.page_size;
   const size_t one = (render_ws_bytes(n_cap, m_cap, tile_count(w, h)) + 4095) & ~(size_t)4095;
-  const size_t bytes = 2 * one;  // frames of the two parities are in flight together
+  const size_t bytes = (size_t)s->slots * one;  // one workspace per frame in flight
   if (s->ws) {
     VMS_CUDA(cudaDeviceSynchronize());
     VMS_CUDA(cudaFree(s->ws));
@@ -527,17 +544,21 @@ vms_session* vms_session_create(const vms_session_desc* desc) {
     s->overlap = !(ov && ov[0] == '0');
     const char* fp = std::getenv("VMSPLAT_FRONT_PRIO");
     const int prio = (fp && fp[0] == '0') ? lo : hi;
-    for (cudaStream_t& x : s->front_stream)
-      ok = ok && cudaStreamCreateWithPriority(&x, cudaStreamNonBlocking, prio) == cudaSuccess;
-    for (cudaEvent_t* e : {&s->ev_pre[0], &s->ev_pre[1], &s->ev_front[0], &s->ev_front[1]})
-      ok = ok && cudaEventCreateWithFlags(e, cudaEventDisableTiming) == cudaSuccess;
+    if (const char* sl = std::getenv("VMSPLAT_SLOTS")) {
+      const int v = std::atoi(sl);
+      if (v >= 2 && v <= kMaxSlots) s->slots = v;
+    }
+    for (int k = 0; k < s->slots; ++k) {
+      ok = ok && cudaStreamCreateWithPriority(&s->front_stream[k], cudaStreamNonBlocking, prio) ==
+                     cudaSuccess;
+      for (cudaEvent_t* e : {&s->ev_pre[k], &s->ev_front[k], &s->ev_done[k], &s->ev_out[k]})
+        ok = ok && cudaEventCreateWithFlags(e, cudaEventDisableTiming) == cudaSuccess;
+    }
   }
   for (cudaEvent_t& e : s->ev_band)
     ok = ok && cudaEventCreateWithFlags(&e, cudaEventDisableTiming) == cudaSuccess;
   ok = ok && cudaEventCreateWithFlags(&s->ev_d2h, cudaEventDisableTiming) == cudaSuccess;
-  for (cudaEvent_t& e : s->ev_out)
-    ok = ok && cudaEventCreateWithFlags(&e, cudaEventDisableTiming) == cudaSuccess;
-  for (cudaEvent_t* e : {&s->ev_vis, &s->ev_copy, &s->ev_staging, &s->ev_done[0], &s->ev_done[1]})
+  for (cudaEvent_t* e : {&s->ev_vis, &s->ev_copy, &s->ev_staging})
     ok = ok && cudaEventCreateWithFlags(e, cudaEventDisableTiming) == cudaSuccess;
   for (cudaEvent_t& e : s->tev) ok = ok && cudaEventCreate(&e) == cudaSuccess;
   ok = ok && host_alloc(&s->req_pid, P + 1) == cudaSuccess;
@@ -546,7 +567,7 @@ vms_session* vms_session_create(const vms_session_desc* desc) {
   ok = ok && host_alloc(&s->req_level, P + 1) == cudaSuccess;
   ok = ok && host_alloc(&s->req_meta, 4) == cudaSuccess;
   ok = ok && host_alloc(&s->vis_fd_h, 1) == cudaSuccess;
-  for (int k = 0; k < 2; ++k) {
+  for (int k = 0; k < s->slots; ++k) {
     ok = ok && host_alloc(&s->copies[k], P + 1) == cudaSuccess;
     ok = ok && host_alloc(&s->scatter_h[k], P + 1) == cudaSuccess;
     ok = ok && host_alloc(&s->chunks_h[k], (size_t)s->max_chunks) == cudaSuccess;
@@ -566,8 +587,11 @@ vms_session* vms_session_create(const vms_session_desc* desc) {
     ok = ok && host_alloc(&s->dplan_entry, P + 1) == cudaSuccess;
     ok = ok && host_alloc(&s->dplan_slot, P + 1) == cudaSuccess;
     ok = ok && host_alloc(&s->dstats, 1) == cudaSuccess;
-    ok = ok && host_alloc(&s->dframe, 1) == cudaSuccess;
-    for (int k = 0; k < 2; ++k) {
+    ok = ok && cudaMalloc(&s->dreq_pid, sizeof(uint32_t) * (P + 1)) == cudaSuccess;
+    ok = ok && cudaMalloc(&s->dreq_enc, sizeof(uint32_t) * (P + 1)) == cudaSuccess;
+    ok = ok && cudaMalloc(&s->dreq_direct, P + 1) == cudaSuccess;
+    ok = ok && cudaMalloc(&s->dreq_level, P + 1) == cudaSuccess;
+    for (int k = 0; k < s->slots; ++k) {
       ok = ok && cudaMalloc(&s->chunks_dev[k], sizeof(vms_chunk) * s->max_chunks) == cudaSuccess;
       ok = ok && cudaEventCreateWithFlags(&s->ev_chunks[k], cudaEventDisableTiming) == cudaSuccess;
     }
@@ -577,7 +601,7 @@ vms_session* vms_session_create(const vms_session_desc* desc) {
     free_session(s);
     return nullptr;
   }
-  for (int k = 0; k < 2; ++k) std::memset(s->counters_h[k], 0, sizeof(uint32_t) * 4);
+  for (int k = 0; k < s->slots; ++k) std::memset(s->counters_h[k], 0, sizeof(uint32_t) * 4);
   s->level_start.assign(desc->lod_levels + 1, 0);
   for (uint32_t k = 0; k < desc->lod_levels; ++k)
     s->level_start[k + 1] =
@@ -652,7 +676,7 @@ int32_t vms_session_frame(vms_session* s, const vms_frame_args* a, vms_frame_sta
   const uint32_t P = s->d.page_count;
   const int par = s->parity;
   int32_t rc = VMS_OK;
-  s->parity ^= 1;
+  s->parity = (par + 1) % s->slots;
   // [1]+[2] visibility on its own high-priority stream (overlaps the renders
   // in flight); the compacted required list lands in mapped pinned memory.
   // It touches no per-parity buffer, so it starts before the frame two back
@@ -662,13 +686,13 @@ int32_t vms_session_frame(vms_session* s, const vms_frame_args* a, vms_frame_sta
   if (s->dpt) {
     // this parity's device chunk table is free once the frame two back copied it
     if (s->chunks_pending[par]) VMS_CUDA(cudaStreamWaitEvent(s->vis_stream, s->ev_chunks[par], 0));
-    s->dframe->frame = a->frame;
-    s->dframe->budget = a->budget;
   }
   if (timing) VMS_CUDA(cudaEventRecord(s->tev[0], s->vis_stream));
   if (tl >= 0) VMS_CUDA(cudaEventRecord(s->tl_ev[tl][0], s->vis_stream));
   s->vis_fd_h->cam = a->vis_cam;
   s->vis_fd_h->lod = a->lod;
+  s->vis_fd_h->dpt.frame = a->frame;
+  s->vis_fd_h->dpt.budget = a->budget;
   VMS_CUDA(cudaMemcpyAsync(vis_frame_dev(s->d.vis_ws, s->d.n_faces, P), s->vis_fd_h,
                            sizeof(VisFrameDev), cudaMemcpyHostToDevice, s->vis_stream));
   vms_vis_args v{};
@@ -681,10 +705,12 @@ int32_t vms_session_frame(vms_session* s, const vms_frame_args* a, vms_frame_sta
   v.link_off = s->d.link_off;
   v.link_tgt = s->d.link_tgt;
   v.lod = a->lod;
-  v.out.pid = s->req_pid;
-  v.out.enc = s->req_enc;
-  v.out.direct = s->req_direct;
-  v.out.level = s->req_level;
+  // the host table reads the required list from mapped memory; the device
+  // table from device memory (its counts and frame inputs too)
+  v.out.pid = s->dpt ? s->dreq_pid : s->req_pid;
+  v.out.enc = s->dpt ? s->dreq_enc : s->req_enc;
+  v.out.direct = s->dpt ? s->dreq_direct : s->req_direct;
+  v.out.level = s->dpt ? s->dreq_level : s->req_level;
   v.out.meta = s->req_meta;
   v.workspace = s->d.vis_ws;
   rc = run_captured(s, s->vis_graph[s->dpt ? par : 0], v.cam.width, v.cam.height, 0,
@@ -692,8 +718,10 @@ int32_t vms_session_frame(vms_session* s, const vms_frame_args* a, vms_frame_sta
                       int32_t r = vis_launch(v, q);
                       if (r || !s->dpt) return r;
                       // [3] on the device: update_page_table, then the chunk table
-                      r = vms_dpt_update(s->dpt, s->req_pid, s->req_enc, s->req_direct,
-                                         s->req_level, s->req_meta + 1, s->dframe, s->dplan_pid,
+                      r = vms_dpt_update(s->dpt, s->dreq_pid, s->dreq_enc, s->dreq_direct,
+                                         s->dreq_level, vis_meta_dev(s->d.vis_ws, s->d.n_faces, P) + 1,
+                                         &vis_frame_dev(s->d.vis_ws, s->d.n_faces, P)->dpt,
+                                         s->dplan_pid,
                                          s->dplan_level, s->dplan_entry, s->dplan_slot,
                                          (int64_t)P + 1, s->dstats, q);
                       if (r) return r;
@@ -835,7 +863,8 @@ int32_t vms_session_frame(vms_session* s, const vms_frame_args* a, vms_frame_sta
   rc = ensure_ws(s, W, H, s->m_cap > s->m_want ? s->m_cap : s->m_want);
   if (rc) return rc;
   cudaStream_t fs = (timing || !s->overlap) ? st : s->front_stream[par];
-  if (fs != st) VMS_CUDA(cudaStreamWaitEvent(fs, s->ev_pre[par ^ 1], 0));
+  if (fs != st)
+    VMS_CUDA(cudaStreamWaitEvent(fs, s->ev_pre[(par + s->slots - 1) % s->slots], 0));
   if (timing) VMS_CUDA(cudaEventRecord(s->tev[8], fs));
   if (tl >= 0) {
     s->tl_host[tl][2] = now_us();
@@ -925,6 +954,7 @@ int32_t vms_session_frame(vms_session* s, const vms_frame_args* a, vms_frame_sta
                 k, s->tl_host[k][0] - h0, s->tl_host[k][1] - h0, s->tl_host[k][2] - h0,
                 s->tl_host[k][3] - h0, 1e3 * d[0], 1e3 * d[1], 1e3 * d[2], 1e3 * d[3], 1e3 * d[4]);
       }
+      (void)cudaGetLastError();  // frames without a host copy never recorded their d2h event
     }
   }
   s->pending[par] = true;
@@ -970,13 +1000,15 @@ int32_t vms_session_frame(vms_session* s, const vms_frame_args* a, vms_frame_sta
 }
 
 int32_t vms_session_wait(vms_session* s, int32_t back) {
-  if (!s || back < 0 || back > 1) {
+  if (!s || back < 0 || back >= s->slots) {
     set_error("session_wait: invalid arguments");
     return VMS_ERR_INVALID;
   }
   if (s->last_par < 0) return VMS_OK;
-  return recycle(s, back == 0 ? s->last_par : s->last_par ^ 1);
+  return recycle(s, (s->last_par + s->slots - back) % s->slots);
 }
+
+int32_t vms_session_slots(const vms_session* s) { return s ? s->slots : 0; }
 
 int32_t vms_session_counters(vms_session* s, uint32_t* out4, void* stream) {
   if (!s || !out4) return VMS_ERR_INVALID;

@@ -245,7 +245,17 @@ __global__ void __launch_bounds__(kFrontThreads) vis_back_k(
     }
     run += tot;
   }
-  if (threadIdx.x == 0) meta[1] = run;  // required pages
+  if (threadIdx.x == 0) {
+    meta[1] = run;  // required pages
+    // the host's copy of the counts: plain stores into the mapped words (no
+    // copy-engine transfer that could queue behind a frame's image copy)
+    if (out.meta) {
+      out.meta[0] = meta[0];
+      out.meta[1] = run;
+      out.meta[2] = meta[2];
+      out.meta[3] = meta[3];
+    }
+  }
 }
 
 __global__ void vis_setup_raw_k(const double* __restrict__ raw, const uint32_t* __restrict__ ids,
@@ -787,12 +797,16 @@ int32_t vis_init() {
   return VMS_OK;
 }
 
+uint32_t* vis_meta_dev(void* ws, uint32_t n_faces, uint32_t page_count) {
+  return carve_ws(ws, n_faces, page_count).n_tris;
+}
+
 VisFrameDev* vis_frame_dev(void* ws, uint32_t n_faces, uint32_t page_count) {
   return carve_ws(ws, n_faces, page_count).fd;
 }
 
 int32_t vis_frame(const VisArgs& a, cudaStream_t s) {
-  VisFrameDev f;
+  VisFrameDev f{};
   f.cam = a.cam;
   f.lod = a.lod;
   VMS_CUDA(cudaMemcpyAsync(vis_frame_dev(a.workspace, a.n_faces, a.page_count), &f,
@@ -924,7 +938,7 @@ int32_t vis_launch(const VisArgs& a, cudaStream_t s) {
       w.depth, w.direct, w.pos, a.page_count, w.fd, a.out);
   mark("vis_required", s);
   }
-  if (a.out.meta) {
+  if (a.out.meta && !back) {  // (vis_back_k stores them itself)
     VMS_CUDA(cudaMemcpyAsync(a.out.meta, w.n_tris, sizeof(uint32_t) * 4,
                              cudaMemcpyDeviceToHost, s));
   }

@@ -28,12 +28,15 @@ using VisArgs = vms_vis_args;
 struct VisFrameDev {
   VisCamera cam;
   VisLod lod;
+  vms_dpt_frame dpt;  // the device page table's frame inputs (same H2D copy)
 };
 
 size_t vis_ws_bytes(uint32_t n_faces, uint32_t page_count);
 // One-time setup (shared-memory limits); outside graph capture.
 int32_t vis_init();
 VisFrameDev* vis_frame_dev(void* ws, uint32_t n_faces, uint32_t page_count);
+// [dev] n_tris, n_req, err, 0 of the last vis_launch
+uint32_t* vis_meta_dev(void* ws, uint32_t n_faces, uint32_t page_count);
 // Upload a.cam / a.lod into the workspace, then vis_launch.
 int32_t vis_frame(const VisArgs& a, cudaStream_t s);
 // The kernel sequence only (camera and LOD from the workspace block; a.cam's

@@ -122,9 +122,9 @@ def run_benchmark(scene, path, config: BenchConfig | None = None, frame_sink=Non
     (float32 (h, w, 3) host array); frames are not kept otherwise.
     B200 extensions: ``frames`` restricts the run to those frame indices, in
     order (a shard of the path); ``session`` reuses an existing one;
-    ``pipelined`` submits frames i + 1 and i + 2 before handing frame i to
-    the sink, so each frame's transfer to the host overlaps the next frame's
-    visibility pass and render (the durations are then not measured: zeros)."""
+    ``pipelined`` keeps the session's slots full (frames i + 1 .. i + slots
+    submitted before frame i goes to the sink), so each frame's transfer to
+    the host overlaps the next frames' visibility pass and render (the durations are then not measured: zeros)."""
     cfg = config or BenchConfig()
     if scene.page_count == 0:
         raise DataError("benchmark needs a paged scene")
@@ -140,15 +140,16 @@ def run_benchmark(scene, path, config: BenchConfig | None = None, frame_sink=Non
             if frame_sink is not None:
                 frame_sink(i, image)
         return out
-    # frames i - 1 and i in flight after submitting i: the session recycles
-    # frame i - 2 (its image copy complete) inside render_frame(i), so that
-    # frame goes to the sink without a wait, and each frame's copy to the host
-    # overlaps both the next render and the next visibility pass
+    # frames i - slots + 1 .. i in flight after submitting i: the session
+    # recycles frame i - slots (its image copy complete) inside
+    # render_frame(i), so that frame goes to the sink without a wait, and each
+    # frame's copy to the host overlaps the next frames' visibility and render
     held = []  # (index, image) submitted, not yet handed over, oldest first
+    depth = getattr(s, "slots", 2)
     for i in indices:
         image, st = s.render_frame(path.frame_camera(i), i, wait=False)
         out.append(FrameStats.from_session(i, {**st, **{f"time_{k}": 0.0 for k in STAGES}}))
-        if len(held) == 2:
+        if len(held) == depth:
             done = held.pop(0)
             if frame_sink is not None:
                 frame_sink(*done)

@@ -691,9 +691,9 @@ class VmSession:
         session alternates two such buffers), returned as soon as the frame
         is enqueued; a float32 (h, w, 3) CUDA tensor -> written in place, the
         same way.  ``wait=False`` with page-locked host output also
-        returns as soon as the frame is enqueued (frames pipeline two deep);
-        the array is complete after ``wait(0)`` (or ``wait(1)`` once the next
-        frame has been submitted)."""
+        returns as soon as the frame is enqueued (``slots`` frames in
+        flight); the array is complete after ``wait(0)`` (or ``wait(k)`` once
+        k more frames have been submitted, k < slots)."""
         t = _device.torch()
         lib = self._lib
         h0 = time.perf_counter()
@@ -837,9 +837,15 @@ class VmSession:
                                 .pin_memory())
         return self._pinned_out[1]
 
+    @property
+    def slots(self) -> int:
+        """Frames the session keeps in flight: render_frame(i) waits for
+        frame i - slots (VMSPLAT_SLOTS, default 3)."""
+        return int(self._lib.vms_session_slots(self._h))
+
     def wait(self, back: int = 0):
-        """Block until the last submitted frame (back=0) or the one before
-        it (back=1) is complete - for ``render_frame(..., wait=False)``."""
+        """Block until the last submitted frame (back=0) or one before it
+        (back < slots) is complete - for ``render_frame(..., wait=False)``."""
         _lib.check(self._lib.vms_session_wait(self._h, int(back)), "wait")
 
     def flush(self):
