@@ -498,14 +498,19 @@ def run_ours(args, rank, world, local_rank):
         sess = new_session()
         torch.cuda.synchronize()
         e0.record(stream)
+        call_ms = []
         for f in range(F):
+            t1 = time.perf_counter()
             sess.render_frame(traj.frame_camera(f), f, out="device")
+            call_ms.append((time.perf_counter() - t1) * 1e3)
         e1.record(stream)
         torch.cuda.synchronize()
         sess.flush()
         ms_traj = e0.elapsed_time(e1)
+        slow = max(range(F), key=lambda k: call_ms[k])
         traj_fps = {"value": round(F / (ms_traj / 1e3), 3), "unit": UNIT, "frames": F,
                     "ms_per_frame": round(ms_traj / F, 4),
+                    "slowest_call": {"frame": slow, "host_ms": round(call_ms[slow], 3)},
                     "what": "every frame 0..F-1 of the trajectory from a fresh session "
                             "(cold page cache at frame 0), frame left in HBM"}
     # last pass over the timed frames with per-stage CUDA events (one sync

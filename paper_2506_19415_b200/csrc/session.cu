@@ -201,7 +201,8 @@ struct vms_session {
   static constexpr int kTl = 32;
   bool timeline = false;
   int tl_n = 0;
-  cudaEvent_t tl_ev[kTl][5] = {};  // vis start, vis end, render start, render end, d2h end
+  // vis start, vis end, render (front) start, render end, d2h end, front end, blend start
+  cudaEvent_t tl_ev[kTl][7] = {};
   double tl_host[kTl][4] = {};     // enter, vis waited, host work done, exit
   int ws_w = 0, ws_h = 0;
   char* staging = nullptr;
@@ -909,6 +910,11 @@ int32_t vms_session_frame(vms_session* s, const vms_frame_args* a, vms_frame_sta
   const bool banded = a->host_image != nullptr && !async_out;
   rc = launch_front(s, par, W, H, timing, banded, fs);
   if (rc) return rc;
+  if (tl >= 0) {
+    VMS_CUDA(cudaEventRecord(s->tl_ev[tl][5], fs));
+    VMS_CUDA(cudaStreamWaitEvent(st, s->ev_front[par], 0));
+    VMS_CUDA(cudaEventRecord(s->tl_ev[tl][6], st));
+  }
   rc = launch_blend(s, par, W, H, timing, banded, st);
   if (rc) return rc;
   if (async_out) {
@@ -946,13 +952,14 @@ int32_t vms_session_frame(vms_session* s, const vms_frame_args* a, vms_frame_sta
       VMS_CUDA(cudaEventSynchronize(s->tl_ev[tl][3]));
       const double h0 = 0.0;
       for (int k = 0; k < vms_session::kTl; ++k) {
-        float d[5] = {0, 0, 0, 0, 0};
-        for (int j = 0; j < 5; ++j) cudaEventElapsedTime(&d[j], s->tl_ev[0][0], s->tl_ev[k][j]);
+        float d[7] = {0, 0, 0, 0, 0, 0, 0};
+        for (int j = 0; j < 7; ++j) cudaEventElapsedTime(&d[j], s->tl_ev[0][0], s->tl_ev[k][j]);
         fprintf(stderr,
                 "[tl] %2d host %12.1f %12.1f %12.1f %12.1f  dev vis %8.1f %8.1f render %8.1f %8.1f"
-                " d2h end %8.1f\n",
+                " d2h end %8.1f front end %8.1f blend start %8.1f\n",
                 k, s->tl_host[k][0] - h0, s->tl_host[k][1] - h0, s->tl_host[k][2] - h0,
-                s->tl_host[k][3] - h0, 1e3 * d[0], 1e3 * d[1], 1e3 * d[2], 1e3 * d[3], 1e3 * d[4]);
+                s->tl_host[k][3] - h0, 1e3 * d[0], 1e3 * d[1], 1e3 * d[2], 1e3 * d[3], 1e3 * d[4],
+                1e3 * d[5], 1e3 * d[6]);
       }
       (void)cudaGetLastError();  // frames without a host copy never recorded their d2h event
     }

@@ -816,12 +816,17 @@ class VmSession:
             # references: the pool's tuple and getrefcount's argument
             if sys.getrefcount(pool[i][1]) <= 2:
                 return pool[i][1]
-        ten = t.empty((camera.height, camera.width, 3), dtype=t.float32, pin_memory=True)
-        arr = ten.numpy()
-        pool.append((ten, arr))
-        if len(pool) > 64:  # the caller keeps frames: stop tracking the oldest
+        # page-locking synchronises the device and takes milliseconds: grow
+        # the pool to what a pipelined caller needs in one go (the frames in
+        # flight, the one being handed over and the one being submitted)
+        first = None
+        for _ in range(max(1, self.slots + 2 - len(pool))):
+            ten = t.empty((camera.height, camera.width, 3), dtype=t.float32, pin_memory=True)
+            pool.append((ten, ten.numpy()))
+            first = pool[-1][1] if first is None else first
+        while len(pool) > 64:  # the caller keeps frames: stop tracking the oldest
             del pool[0]
-        return arr
+        return first
 
     def _zero_copy(self, arr) -> bool:
         # asked every call (cudaPointerGetAttributes is cheap): a cached answer
