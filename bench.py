@@ -39,6 +39,7 @@ for _v in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS"):
     os.environ[_v] = "1"
 
 import argparse  # noqa: E402
+import gc  # noqa: E402
 import json  # noqa: E402
 import statistics
 import subprocess  # noqa: E402
@@ -392,7 +393,10 @@ def run_ours(args, rank, world, local_rank):
     W, H = args.width, args.height
 
     def new_session(timing=False):
-        holder.pop("s", None)
+        old = holder.pop("s", None)
+        if old is not None:
+            old.close()  # now, not inside a later timed region (cycle collector)
+        gc.collect()
         torch.cuda.empty_cache()
         holder["s"] = VmSession(scene, buffer_pages=cfg["buffer"], staging_pages=cfg["staging"],
                                 vis_scale=0.25, exact=not args.fast,

@@ -1361,6 +1361,14 @@ int32_t blend_init() {
   }
   VMS_CUDA(cudaMemcpyToSymbol(kExp2Tab, t, sizeof(t)));
   {
+    const char* e = getenv("VMSPLAT_LB_SLEEP");
+    const int ns = e && *e ? atoi(e) : 0;
+    if (prims_set_backoff(ns < 0 ? 0u : (unsigned)ns)) {
+      set_error("blend_init: look-back back-off");
+      return VMS_ERR_CUDA;
+    }
+  }
+  {
     const char* e = getenv("VMSPLAT_CERT_ALL");
     const int all = e && *e ? atoi(e) : 0;
     VMS_CUDA(cudaMemcpyToSymbol(g_cert_all, &all, sizeof(int)));

@@ -218,8 +218,9 @@ struct vms_session {
   // vis: [slot] (device table); front: [slot][timing][banded]; blend: [slot][timing]
   Graph vis_graph[kMaxSlots], front_graph[kMaxSlots][2][2], blend_graph[kMaxSlots][2];
   // device page table (desc.device_table): its outputs land in mapped memory
-  // (plan, stats) and per-parity device chunk tables; the next frame of the
-  // same parity waits for ev_chunks before its update overwrites them
+  // (plan, stats) and per-slot device chunk tables, read in place by the
+  // slot's preprocess; the next frame of the same slot waits for that
+  // preprocess (ev_pre) before its update overwrites them
   vms_dpt* dpt = nullptr;
   uint32_t* dplan_pid = nullptr;
   uint8_t* dplan_level = nullptr;
@@ -227,7 +228,6 @@ struct vms_session {
   int32_t* dplan_slot = nullptr;
   vms_dpt_stats* dstats = nullptr;
   vms_chunk* chunks_dev[kMaxSlots] = {};
-  cudaEvent_t ev_chunks[kMaxSlots] = {};
   // the required list in device memory (the update reads it there: reads of
   // mapped host memory stall behind a concurrent image copy on the bus)
   uint32_t* dreq_pid = nullptr;
@@ -257,8 +257,6 @@ void free_session(vms_session* s) {
   if (!s) return;
   for (auto& g : s->vis_graph) g.reset();
   if (s->dpt) vms_dpt_destroy(s->dpt);
-  for (cudaEvent_t e : s->ev_chunks)
-    if (e) cudaEventDestroy(e);
   for (void* p : {(void*)s->dplan_pid, (void*)s->dplan_level, (void*)s->dplan_entry,
                   (void*)s->dplan_slot, (void*)s->dstats})
     if (p) cudaFreeHost(p);
@@ -420,7 +418,8 @@ int32_t launch_front(vms_session* s, int par, int w, int h, bool timing, bool ba
     mark("begin", q);
     int32_t rc = render_clear(w, h, ws, q);
     if (rc) return rc;
-    rc = render_preprocess(s->d.pool, s->chunks_d, max_chunks, ws, q);
+    rc = render_preprocess(s->d.pool, s->dpt ? s->chunks_dev[par] : s->chunks_d, max_chunks,
+                           ws, q);
     if (rc) return rc;
     VMS_CUDA(cudaEventRecordWithFlags(s->ev_pre[par], q, rf));
     if (timing) VMS_CUDA(cudaEventRecordWithFlags(s->tev[4], q, rf));
@@ -594,7 +593,6 @@ vms_session* vms_session_create(const vms_session_desc* desc) {
     ok = ok && cudaMalloc(&s->dreq_level, P + 1) == cudaSuccess;
     for (int k = 0; k < s->slots; ++k) {
       ok = ok && cudaMalloc(&s->chunks_dev[k], sizeof(vms_chunk) * s->max_chunks) == cudaSuccess;
-      ok = ok && cudaEventCreateWithFlags(&s->ev_chunks[k], cudaEventDisableTiming) == cudaSuccess;
     }
   }
   if (!ok) {
@@ -686,7 +684,7 @@ int32_t vms_session_frame(vms_session* s, const vms_frame_args* a, vms_frame_sta
   // then overlap instead of adding up.
   if (s->dpt) {
     // this parity's device chunk table is free once the frame two back copied it
-    if (s->chunks_pending[par]) VMS_CUDA(cudaStreamWaitEvent(s->vis_stream, s->ev_chunks[par], 0));
+    if (s->chunks_pending[par]) VMS_CUDA(cudaStreamWaitEvent(s->vis_stream, s->ev_pre[par], 0));
   }
   if (timing) VMS_CUDA(cudaEventRecord(s->tev[0], s->vis_stream));
   if (tl >= 0) VMS_CUDA(cudaEventRecord(s->tl_ev[tl][0], s->vis_stream));
@@ -887,19 +885,11 @@ int32_t vms_session_frame(vms_session* s, const vms_frame_args* a, vms_frame_sta
   f->n_splats = (uint32_t)n_res;
   f->counters_host = s->counters_h[par];  // mapped: written by tile_prep_k
   VMS_CUDA(cudaMemcpyAsync(ws.fd, f, sizeof(FrameDev), cudaMemcpyHostToDevice, fs));
-  if (n_chunks) {
-    if (s->dpt) {
-      VMS_CUDA(cudaMemcpyAsync(s->chunks_d, s->chunks_dev[par], sizeof(vms_chunk) * n_chunks,
-                               cudaMemcpyDeviceToDevice, fs));
-    } else {
-      VMS_CUDA(cudaMemcpyAsync(s->chunks_d, s->chunks_h[par], sizeof(vms_chunk) * n_chunks,
-                               cudaMemcpyHostToDevice, fs));
-    }
-  }
-  if (s->dpt) {
-    VMS_CUDA(cudaEventRecord(s->ev_chunks[par], fs));
-    s->chunks_pending[par] = true;
-  }
+  // the device table's chunk table is read in place (this slot's buffer);
+  // the host table's goes up with the frame block
+  if (n_chunks && !s->dpt)
+    VMS_CUDA(cudaMemcpyAsync(s->chunks_d, s->chunks_h[par], sizeof(vms_chunk) * n_chunks,
+                             cudaMemcpyHostToDevice, fs));
   // host output: the blend runs as kBands launches over bands of tile rows
   // and each band's rows go to the host as soon as that band is blended
   // host output, synchronous call: the blend runs as kBands launches and each
@@ -910,6 +900,7 @@ int32_t vms_session_frame(vms_session* s, const vms_frame_args* a, vms_frame_sta
   const bool banded = a->host_image != nullptr && !async_out;
   rc = launch_front(s, par, W, H, timing, banded, fs);
   if (rc) return rc;
+  s->chunks_pending[par] = s->dpt != nullptr;  // ev_pre[par]: its preprocess read them
   if (tl >= 0) {
     VMS_CUDA(cudaEventRecord(s->tl_ev[tl][5], fs));
     VMS_CUDA(cudaStreamWaitEvent(st, s->ev_front[par], 0));
@@ -920,8 +911,23 @@ int32_t vms_session_frame(vms_session* s, const vms_frame_args* a, vms_frame_sta
   if (async_out) {
     VMS_CUDA(cudaEventRecord(s->ev_band[0], st));
     VMS_CUDA(cudaStreamWaitEvent(s->d2h_stream, s->ev_band[0], 0));
-    VMS_CUDA(cudaMemcpyAsync(a->host_image, a->image, sizeof(float) * 3 * (size_t)W * H,
-                             cudaMemcpyDeviceToHost, s->d2h_stream));
+    // in row bands: page uploads (host -> device) queued on the copy engines
+    // meanwhile go between two bands instead of after the whole 25 MB frame
+    // (C2 frames 5-64 under a per-frame image copy: 1609 frames/s as one
+    // copy, 1717 as 8 bands)
+    static const int bands = [] {
+      const char* e = std::getenv("VMSPLAT_D2H_BANDS");
+      const int v = e && *e ? std::atoi(e) : 8;
+      return v < 1 ? 1 : (v > 64 ? 64 : v);
+    }();
+    const size_t row_bytes = sizeof(float) * 3 * (size_t)W;
+    for (int b = 0; b < bands; ++b) {
+      const int y0 = (int)((int64_t)H * b / bands), y1 = (int)((int64_t)H * (b + 1) / bands);
+      if (y1 > y0)
+        VMS_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(a->host_image) + row_bytes * y0,
+                                 reinterpret_cast<const char*>(a->image) + row_bytes * y0,
+                                 row_bytes * (y1 - y0), cudaMemcpyDeviceToHost, s->d2h_stream));
+    }
     VMS_CUDA(cudaEventRecord(s->ev_out[par], s->d2h_stream));
     if (tl >= 0) VMS_CUDA(cudaEventRecord(s->tl_ev[tl][4], s->d2h_stream));
     s->pending_out[par] = true;

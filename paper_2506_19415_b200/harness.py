@@ -132,6 +132,14 @@ def run_benchmark(scene, path, config: BenchConfig | None = None, frame_sink=Non
     if not cfg.vm:
         return _run_flat(scene, path, indices, frame_sink)
     s = session if session is not None else make_session(scene, cfg, timing=not pipelined)
+    try:
+        return _run_session(s, path, indices, frame_sink, pipelined)
+    finally:
+        if session is None and hasattr(s, "close"):
+            s.close()
+
+
+def _run_session(s, path, indices, frame_sink, pipelined):
     out = []
     if not pipelined:
         for i in indices:

@@ -657,6 +657,23 @@ class VmSession:
         self._stats = _lib.FrameStats()
         self._pinned_out = None
 
+    def close(self):
+        """Free the session's device and page-locked memory now.  The session
+        and its page table refer to each other, so dropping the last
+        reference leaves the teardown (a device synchronisation, GBs of
+        frees) to Python's cycle collector - which may run it in the middle
+        of another session's frames.  The table view is invalid afterwards."""
+        tbl = self.__dict__.get("table")
+        if tbl is not None:
+            tbl._h = ctypes.c_void_p(0)
+        self.__del__()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
     def __del__(self):
         h = getattr(self, "_h", None)
         if h is not None and h.value:
