@@ -176,6 +176,10 @@ int32_t vms_debug_exp(const double* x, int64_t n, double* out, void* stream);
  * image is re-blended by the FP64 repair kernel (tests: must equal exact
  * mode). */
 int32_t vms_debug_cert_all(int32_t on);
+/* Exact blend: per-pixel splat walks for groups of small splats (on = 1,
+ * the default; VMSPLAT_LANE_LISTS) when they save more than margin steps -
+ * for same-process A/B and identity tests (synchronises the device). */
+int32_t vms_debug_lane_lists(int32_t on, int32_t margin);
 
 /* ---- kernel-level drop-ins (pkg/src/vmsplat/kernels/__init__.py) ------ */
 

@@ -158,6 +158,7 @@ SIGNATURES = {
     "vms_session_dpt": (P, [P]),
     "vms_session_cert_count": (I32, [P, P]),
     "vms_debug_cert_all": (I32, [I32]),
+    "vms_debug_lane_lists": (I32, [I32, I32]),
     "vms_session_set_render_ws": (I32, [P, P, ctypes.c_uint64, U32, I32, I32]),
     "vms_session_frame": (I32, [P, ctypes.POINTER(FrameArgs), ctypes.POINTER(FrameStats), P]),
     "vms_session_counters": (I32, [P, P, P]),

@@ -176,6 +176,7 @@ int32_t vms_tile_size(void) { return tile_size(); }
 int32_t vms_debug_blend_trace(void* dev_ptr) { return debug_blend_trace(dev_ptr); }
 
 int32_t vms_debug_cert_all(int32_t on) { return debug_cert_all(on); }
+int32_t vms_debug_lane_lists(int32_t on, int32_t margin) { return debug_lane_lists(on, margin); }
 
 int32_t vms_debug_exp(const double* x, int64_t n, double* out, void* stream) {
   if (n < 0 || (n > 0 && (!x || !out))) {

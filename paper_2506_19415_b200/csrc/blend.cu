@@ -359,6 +359,11 @@ constexpr float kCertTol = 9e-4f;
 __device__ int g_cert_all = 0;
 __device__ uint32_t g_cert_why[4];
 constexpr int kPairStep = 2;  // splats whose box tests and sigmas are evaluated together
+// exact blend: per-pixel splat walks (VMSPLAT_LANE_LISTS: 0 off - the dense
+// warp walk; 1 for groups of small splats saving more than g_lane_margin
+// steps; 2, the default, every group)
+__device__ int g_lane_lists = 2;
+__device__ int g_lane_margin = 2;
 
 __constant__ double kBlendC[10] = {
     0x1.71547652b82fep+6,   // 0: 64 / ln2
@@ -639,6 +644,72 @@ __global__ void __launch_bounds__(kBlendThreads, kSparse ? 3 : 4) blend_k(const 
           cb = __double2float_rn(__dadd_rn((double)cb, __dmul_rn(wt, q.b)));
           T = __double2float_rn(__dmul_rn(t, __dsub_rn(1.0, wgt)));
         };
+        // Lane lists for groups of small splats (the far splats of the long,
+        // vanishing-point lists cover a few lanes of the 8x4 block each): the
+        // group's boxes become per-pixel bit sets (8 column and 4 row
+        // ballots), and every lane walks only the splats covering its pixel,
+        // in list order - max over lanes of popc(own) steps instead of
+        // popc(m), same arithmetic per pixel-splat, so the same image.
+        if (g_lane_lists) {
+          const bool in_m = (m >> lane) & 1u;
+          int cl = 0, ch = 0, rl = 0, rh = 0;
+          if (in_m) {
+            const Staged& q = grp[lane];
+            cl = max(q.x0 - wx0, 0);
+            ch = min(q.x0 + q.xw - wx0, 8);
+            rl = max(q.y0 - wy0, 0);
+            rh = min(q.y0 + q.yh - wy0, 4);
+          }
+          const uint32_t area = __reduce_add_sync(0xffffffffu, (uint32_t)((ch - cl) * (rh - rl)));
+          const uint32_t nm = __popc(m);
+          const bool force = g_lane_lists >= 2;  // every group
+          if (force || area * 4u < nm * 3u * 32u) {  // mean coverage below 3/4 of the block
+            const int cx = lane & 7, ry = lane >> 3;
+            uint32_t colw = 0, roww = 0;
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+              const uint32_t b = __ballot_sync(0xffffffffu, cl <= c && c < ch);
+              colw = cx == c ? b : colw;
+            }
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+              const uint32_t b = __ballot_sync(0xffffffffu, rl <= r && r < rh);
+              roww = ry == r ? b : roww;
+            }
+            uint32_t own = colw & roww;  // group splats whose box holds this pixel
+            const uint32_t steps =
+                __reduce_max_sync(0xffffffffu, T >= kStopF ? (uint32_t)__popc(own) : 0u);
+            if (force || steps + (uint32_t)g_lane_margin < nm) {
+              auto sig = [&](const Staged& q) -> double {
+                const double dx = __dsub_rn(fx, q.cx);
+                const double dy = __dsub_rn(fy, q.cy);
+                return __dadd_rn(__dadd_rn(__dmul_rn(__dmul_rn(q.ca, dx), dx),
+                                           __dmul_rn(__dmul_rn(q.cb2, dy), dx)),
+                                 __dmul_rn(__dmul_rn(q.cc, dy), dy));
+              };
+              while (own && T >= kStopF) {
+                const int j0 = __ffs(own) - 1;
+                own &= own - 1;
+                const bool two = own != 0u;
+                const int j1 = two ? __ffs(own) - 1 : j0;
+                own &= two ? own - 1 : own;
+                const Staged& q0 = grp[j0];
+                const Staged& q1 = grp[j1];
+                const double s0 = sig(q0), s1 = sig(q1);
+                const bool l0 = s0 >= q0.skip, l1 = two && s1 >= q1.skip;
+                if (g_lane_lists == 3 && !__any_sync(__activemask(), l0 || l1)) continue;
+                double w0 = __dmul_rn(q0.al, exp_tab(l0 ? s0 : 0.0, tab));
+                double w1 = __dmul_rn(q1.al, exp_tab(l1 ? s1 : 0.0, tab));
+                if (w0 > kBlendC[8]) w0 = kBlendC[8];
+                if (w1 > kBlendC[8]) w1 = kBlendC[8];
+                if (l0) apply(q0, w0);
+                if (l1 && T >= kStopF) apply(q1, w1);
+              }
+              __syncwarp();
+              m = 0u;
+            }
+          }
+        }
         while (m) {
           int j[kPairStep];
           int got = 0;
@@ -1361,12 +1432,12 @@ int32_t blend_init() {
   }
   VMS_CUDA(cudaMemcpyToSymbol(kExp2Tab, t, sizeof(t)));
   {
-    const char* e = getenv("VMSPLAT_LB_SLEEP");
-    const int ns = e && *e ? atoi(e) : 0;
-    if (prims_set_backoff(ns < 0 ? 0u : (unsigned)ns)) {
-      set_error("blend_init: look-back back-off");
-      return VMS_ERR_CUDA;
-    }
+    const char* e = getenv("VMSPLAT_LANE_LISTS");
+    const int on = e && *e ? atoi(e) : 2;
+    const char* mg = getenv("VMSPLAT_LANE_MARGIN");
+    const int margin = mg && *mg ? atoi(mg) : 2;
+    VMS_CUDA(cudaMemcpyToSymbol(g_lane_lists, &on, sizeof(int)));
+    VMS_CUDA(cudaMemcpyToSymbol(g_lane_margin, &margin, sizeof(int)));
   }
   {
     const char* e = getenv("VMSPLAT_CERT_ALL");
@@ -1390,6 +1461,14 @@ int32_t debug_exp(const double* x, uint64_t n, double* out, cudaStream_t s) {
   if (const int32_t rc = blend_init()) return rc;
   if (n) exp_eval_k<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(x, n, out);
   VMS_LAUNCH_CHECK("debug_exp");
+  return VMS_OK;
+}
+
+int32_t debug_lane_lists(int on, int margin) {
+  if (const int32_t rc = blend_init()) return rc;
+  VMS_CUDA(cudaDeviceSynchronize());
+  VMS_CUDA(cudaMemcpyToSymbol(g_lane_lists, &on, sizeof(int)));
+  VMS_CUDA(cudaMemcpyToSymbol(g_lane_margin, &margin, sizeof(int)));
   return VMS_OK;
 }
 

@@ -91,10 +91,6 @@ __device__ __forceinline__ void st_status(uint32_t* p, uint32_t v) {
 // inclusive prefix, or up to the first predecessor that has not published
 // yet, which is then re-read.
 constexpr int kWindow = 8;
-// back-off (ns) of a look-back round that found no new predecessor status:
-// spinning warps otherwise take issue slots from the kernels they share SMs
-// with (the previous frame's blend, under the cross-frame overlap)
-__device__ unsigned g_lb_sleep = 0;
 
 __device__ __forceinline__ uint32_t look_back(const uint32_t* status, uint32_t t, uint32_t stride) {
   uint32_t excl = 0;
@@ -116,10 +112,6 @@ __device__ __forceinline__ uint32_t look_back(const uint32_t* status, uint32_t t
     }
     if (found) break;
     j -= used;
-    if (used == 0) {
-      const unsigned ns = g_lb_sleep;
-      if (ns) __nanosleep(ns);
-    }
   }
   return excl;
 }
@@ -353,10 +345,6 @@ int persistent_grid(const void* kern, int threads, int cap) {
 }
 
 }  // namespace
-
-int32_t prims_set_backoff(unsigned ns) {
-  return cudaMemcpyToSymbol(g_lb_sleep, &ns, sizeof(ns)) == cudaSuccess ? 0 : -1;
-}
 
 size_t scan_ws_bytes(uint32_t n_max) {
   return sizeof(uint32_t) * (((size_t)n_max + kLbTile - 1) / kLbTile + 64);

@@ -13,8 +13,6 @@ namespace vms {
 // scan_ws_bytes() bytes.
 // n_max: upper bound on n (sizes the look-back status array in ws).
 size_t scan_ws_bytes(uint32_t n_max);
-// Look-back back-off in ns when a round sees no new predecessor (0 = spin).
-int32_t prims_set_backoff(unsigned ns);
 // clear = false: the caller zeroed the first scan_ws_bytes(n_max) of ws
 // (e.g. hoisted to the start of a captured frame, so the kernels chain).
 int32_t scan_exclusive_u32(const uint32_t* in, uint32_t* out, const uint32_t* n_dev,

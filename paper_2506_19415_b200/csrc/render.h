@@ -121,6 +121,8 @@ int32_t debug_exp(const double* x, uint64_t n, double* out, cudaStream_t s);
 // Certified fast blend: flag every pixel (tests); pixels flagged by the
 // last blend (synchronises the device).
 int32_t debug_cert_all(int on);
+// exact blend: lane lists on/off and their step margin (tests, A/B)
+int32_t debug_lane_lists(int on, int margin);
 int32_t debug_cert_count(const RenderWs& w, uint32_t* out);
 
 // Zero the frame's counters and primitive workspaces (all memsets of a

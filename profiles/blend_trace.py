@@ -17,12 +17,16 @@ def main():
     from paper_2506_19415_b200.scene_io import read_scene
 
     class A:
-        scene_dir = os.environ.get("VMSPLAT_SCENE_DIR", "/tmp/vmsplat_bench")
+        config = "c2"
+        scene_dir = None
+        frames = 120
+        width = 1920
+        height = 1080
 
     frame = int(sys.argv[1]) if len(sys.argv) > 1 else 25
     lay, path = bench.ensure_scene(A, 0)
     scene = read_scene(path, mmap_gaussians=True)
-    traj = scenegen.street_path(lay, frames=120)
+    traj = bench.trajectory(A, lay)
     s = VmSession(scene, timing=False)
     lib = _lib.load()
     for f in range(frame):
@@ -58,6 +62,12 @@ def main():
     for i in range(len(t)):
         last[sms[i]] = max(last[sms[i]], en[i])
     print(f"  SM finish time: min {last.min():.1f} median {np.median(last):.1f} max {last.max():.1f} us")
+    slots = 148 * 4
+    print(f"  bound: CTA-time / {slots} slots {dur.sum() / slots:.1f} us, longest CTA {dur.max():.1f} us")
+    for cut in (2048, 4096, 8192):
+        m = ln >= cut
+        print(f"  lists >= {cut}: {m.sum()} CTAs, {dur[m].sum() / dur.sum():.1%} of CTA time, "
+              f"longest {dur[m].max() if m.any() else 0:.1f} us")
     big = np.flatnonzero(ln >= 4096)
     print(f"  CTAs with lists >= 4096: {len(big)}; launch index, start, dur, length:")
     for i in big[:64]:

@@ -424,6 +424,31 @@ def test_c2_overlapped_frames_identical_to_serial(cuda, c2_scene, upload_mode):
     assert copies > 8
 
 
+def test_c2_lane_lists_identical_to_dense_walk(cuda, c2_scene):
+    """The exact blend's per-pixel splat walks (lane lists, taken for groups
+    of small splats) apply each pixel's splats in list order with the dense
+    walk's arithmetic: C2 frames 5-34 (the benchmarked frames, vanishing
+    point included) are bit-identical with lane lists off, adaptive (the
+    default) and forced on every group."""
+    from paper_2506_19415_b200 import _lib, scenegen
+    from paper_2506_19415_b200.runtime import VmSession
+
+    lib = _lib.load()
+    traj = scenegen.street_path(scenegen.C2, frames=120)
+    frames = {}
+    try:
+        for mode in (0, 1, 2):
+            _lib.check(lib.vms_debug_lane_lists(mode, 2), "lane lists")
+            s = VmSession(c2_scene, timing=False)
+            frames[mode] = [s.render_frame(traj.frame_camera(f), f)[0] for f in range(35)]
+            s.close()
+    finally:
+        lib.vms_debug_lane_lists(1, 2)
+    for f in range(5, 35):
+        assert np.array_equal(frames[1][f], frames[0][f]), f
+        assert np.array_equal(frames[2][f], frames[0][f]), f
+
+
 def test_c2_render_is_deterministic(cuda, c2_scene):
     from paper_2506_19415_b200 import scenegen
     from paper_2506_19415_b200.runtime import VmSession
