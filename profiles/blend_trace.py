@@ -32,7 +32,7 @@ def main():
     for f in range(frame):
         s.render_frame(traj.frame_camera(f), f, out="device")
     s.flush()
-    buf = torch.zeros(8 * 12000, dtype=torch.int64, device="cuda")
+    buf = torch.zeros(8 * 40000, dtype=torch.int64, device="cuda")
     lib.vms_debug_blend_trace(buf.data_ptr())
     s.render_frame(traj.frame_camera(frame), frame, out="device")
     s.flush()
@@ -62,7 +62,7 @@ def main():
     for i in range(len(t)):
         last[sms[i]] = max(last[sms[i]], en[i])
     print(f"  SM finish time: min {last.min():.1f} median {np.median(last):.1f} max {last.max():.1f} us")
-    slots = 148 * 4
+    slots = 148 * (8 if len(t) > 9000 else 4)
     print(f"  bound: CTA-time / {slots} slots {dur.sum() / slots:.1f} us, longest CTA {dur.max():.1f} us")
     for cut in (2048, 4096, 8192):
         m = ln >= cut
