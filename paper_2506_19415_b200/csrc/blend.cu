@@ -342,6 +342,9 @@ struct SplatF64 {
   double cx, cy, ca, cb2, cc, al, r, g, b;
   double skip;  // sigma below which alpha * exp(sigma) < 2^-36 (no effect on f32 T)
   int x0, xw, y0, yh;  // clamped box: [x0, x0 + xw) x [y0, y0 + yh)
+  // 104-byte stride (26 banks): lanes loading the same field of different
+  // staged splats (lane lists) collide only 16 splats apart, not 4 (96 B)
+  int pad_[2];
 };
 
 // 2^(j/64) as double-double, j = 0..63
