@@ -381,6 +381,11 @@ __constant__ double kBlendC[10] = {
     0.5,                    // 9
 };
 
+// tab[j * S] = 2^(j/64): S = 1 (one table), or S = 8 (eight interleaved
+// copies, the caller passing copy lane % 8: a 128-bit shared load is served
+// 8 lanes at a time, and entry j of copy c sits in banks 4c..4c+3 for every
+// j, so per-lane table lookups never conflict)
+template <int S = 1>
 __device__ __forceinline__ double exp_tab(double x, const double2* __restrict__ tab) {
   // exp(x), x in [-700, 0]: x = (64 m + j) ln2/64 + r, |r| <= ln2/128
   const double t = __fma_rn(x, kBlendC[0], kBlendC[1]);
@@ -393,7 +398,7 @@ __device__ __forceinline__ double exp_tab(double x, const double2* __restrict__ 
   q = __fma_rn(q, r, kBlendC[9]);
   q = __fma_rn(q, r, 1.0);
   const double sr = __dmul_rn(q, r);  // exp(r) - 1
-  const double2 tj = tab[k & 63];
+  const double2 tj = tab[(k & 63) * S];
   const double v = __dadd_rn(tj.x, __fma_rn(tj.x, sr, tj.y));
   return __hiloint2double(__double2hiint(v) + ((k >> 6) << 20), __double2loint(v));
 }
@@ -447,7 +452,7 @@ __global__ void __launch_bounds__(kBlendThreads, kSparse ? 3 : 4) blend_k(const 
   using Staged = typename std::conditional<kExact, SplatF64, BlendRec>::type;
   __shared__ Staged sp[kBlendThreads];
   __shared__ uint32_t wsum[kBlendThreads / 32];
-  __shared__ double2 tab[kExact ? 64 : 1];
+  __shared__ double2 tab[kExact ? 64 * 8 : 1];
   extern __shared__ double wbuf[];  // kSparse: (warps) x kSparseGroup x kSparseRow
   unsigned long long t_start = 0;
   unsigned long long* trace = g_blend_trace;
@@ -461,7 +466,9 @@ __global__ void __launch_bounds__(kBlendThreads, kSparse ? 3 : 4) blend_k(const 
   const int wx0 = sx0 + (warp & 1) * 8, wy0 = sy0 + (warp >> 1) * 4;
   const int px = wx0 + (lane & 7), py = wy0 + (lane >> 3);
   const bool inside = px < w && py < h;
-  if (kExact && threadIdx.x < 64) tab[threadIdx.x] = kExp2Tab[threadIdx.x];
+  if (kExact)
+    for (int t = threadIdx.x; t < 64 * 8; t += kBlendThreads) tab[t] = kExp2Tab[t >> 3];
+  const double2* __restrict__ tabl = tab + (lane & 7);  // this lane's table copy
   const bool spill = ctr->overflow != 0u;
   const uint32_t start = spill ? 0u : ranges[2 * tile];
   const uint32_t end = spill ? ctr->n_kept : ranges[2 * tile + 1];
@@ -578,7 +585,7 @@ __global__ void __launch_bounds__(kBlendThreads, kSparse ? 3 : 4) blend_k(const 
                                                       __dmul_rn(sxy, dx)),
                                             syy);
                 if (sg < q.skip) continue;
-                double wk = __dmul_rn(q.al, exp_tab(sg, tab));
+                double wk = __dmul_rn(q.al, exp_tab<8>(sg, tabl));
                 if (wk > kBlendC[8]) wk = kBlendC[8];
                 row[pbit] = wk;
                 pm |= 1u << pbit;
@@ -639,7 +646,7 @@ __global__ void __launch_bounds__(kBlendThreads, kSparse ? 3 : 4) blend_k(const 
         auto blend = [&](const Staged& q, double sg) {
           // _core.pyx:56-78: FP64 arithmetic, f32 storage of T and colour
           const double t = (double)T;
-          double wgt = __dmul_rn(q.al, exp_tab(sg, tab));
+          double wgt = __dmul_rn(q.al, exp_tab<8>(sg, tabl));
           if (wgt > kBlendC[8]) wgt = kBlendC[8];
           const double wt = __dmul_rn(wgt, t);
           cr = __double2float_rn(__dadd_rn((double)cr, __dmul_rn(wt, q.r)));
@@ -701,8 +708,8 @@ __global__ void __launch_bounds__(kBlendThreads, kSparse ? 3 : 4) blend_k(const 
                 const double s0 = sig(q0), s1 = sig(q1);
                 const bool l0 = s0 >= q0.skip, l1 = two && s1 >= q1.skip;
                 if (g_lane_lists == 3 && !__any_sync(__activemask(), l0 || l1)) continue;
-                double w0 = __dmul_rn(q0.al, exp_tab(l0 ? s0 : 0.0, tab));
-                double w1 = __dmul_rn(q1.al, exp_tab(l1 ? s1 : 0.0, tab));
+                double w0 = __dmul_rn(q0.al, exp_tab<8>(l0 ? s0 : 0.0, tabl));
+                double w1 = __dmul_rn(q1.al, exp_tab<8>(l1 ? s1 : 0.0, tabl));
                 if (w0 > kBlendC[8]) w0 = kBlendC[8];
                 if (w1 > kBlendC[8]) w1 = kBlendC[8];
                 if (l0) apply(q0, w0);
@@ -736,7 +743,7 @@ __global__ void __launch_bounds__(kBlendThreads, kSparse ? 3 : 4) blend_k(const 
 #pragma unroll
           for (int k = 0; k < kPairStep; ++k) {
             const Staged& q = grp[j[k]];
-            double wk = __dmul_rn(q.al, exp_tab(l[k] ? sg[k] : 0.0, tab));
+            double wk = __dmul_rn(q.al, exp_tab<8>(l[k] ? sg[k] : 0.0, tabl));
             if (wk > kBlendC[8]) wk = kBlendC[8];
             wv[k] = wk;
           }
@@ -763,7 +770,7 @@ __global__ void __launch_bounds__(kBlendThreads, kSparse ? 3 : 4) blend_k(const 
           // weight < 2^-36: T is unchanged bit for bit and the colour moves by
           // < 2^-36 (far tails of elongated splats) - skip the exp
           if (sig < s.skip) continue;
-          double wgt = __dmul_rn(s.al, exp_tab(sig, tab));
+          double wgt = __dmul_rn(s.al, exp_tab<8>(sig, tabl));
           if (wgt > kBlendC[8]) wgt = kBlendC[8];
           const double wt = __dmul_rn(wgt, t);
           cr = __double2float_rn(__dadd_rn((double)cr, __dmul_rn(wt, s.r)));
@@ -1285,15 +1292,28 @@ uint32_t hot_len() {
   return n;
 }
 
+int blend_sparse() {
+  static const int sparse = [] {
+    const char* e = getenv("VMSPLAT_BLEND_SPARSE");
+    return e && *e ? atoi(e) : 0;
+  }();
+  return sparse;
+}
+
+// Hot tiles (single-band frames, exact blend): their own kernel on a forked
+// stream, concurrent with the regular blend of the other tiles.
+bool hot_path(int exact, int bands) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return exact && !blend_sparse() && bands == 1 && hot_enabled() && g_hot[dev & 15].side;
+}
+
 int32_t launch_band(int width, int height, const uint32_t* vals, const RenderWs& w, float* image,
                     int accumulate, int exact, int band, int bands, cudaStream_t s) {
   const int ts = tile_size();
   const int tiles_x = ceil_div(width, ts), tiles_y = ceil_div(height, ts);
   const uint32_t n_tiles = (uint32_t)tiles_x * tiles_y;
-  static const int sparse = [] {
-    const char* e = getenv("VMSPLAT_BLEND_SPARSE");
-    return e && *e ? atoi(e) : 0;
-  }();
+  const int sparse = blend_sparse();
   auto* kern = exact ? (sparse ? (ts == 16 ? blend_k<true, 16, true> : blend_k<true, 32, true>)
                                : (ts == 16 ? blend_k<true, 16> : blend_k<true, 32>))
                      : (ts == 16 ? blend_k<false, 16> : blend_k<false, 32>);
@@ -1301,16 +1321,13 @@ int32_t launch_band(int width, int height, const uint32_t* vals, const RenderWs&
   const int r0 = blend_band_row(band, bands, tiles_y), r1 = blend_band_row(band + 1, bands, tiles_y);
   const uint32_t first = (uint32_t)r0 * tiles_x, count = (uint32_t)(r1 - r0) * tiles_x;
   const size_t dsmem = (exact && sparse) ? kSparseSmem : 0;
-  // hot tiles (single-band frames, exact blend): their own kernel on a
-  // forked stream, concurrent with the regular blend of the other tiles
+  // hot tiles: the list (hot_list_k) was built with the tile lists, so the
+  // blend starts as soon as they are ready
   int dev = 0;
   cudaGetDevice(&dev);
   const HotStreams& hs = g_hot[dev & 15];
-  const bool hot = exact && !sparse && bands == 1 && hot_enabled() && hs.side;
+  const bool hot = hot_path(exact, bands);
   if (hot) {
-    VMS_CUDA(launch(hot_list_k, 1, 1024, 0, s, (const uint32_t*)w.ranges, n_tiles, hot_len(),
-                    (const RenderCounters*)w.ctr, w.hot, w.tile_hot));
-    mark("hot_list", s);
     VMS_CUDA(cudaEventRecord(hs.fork, s));
     VMS_CUDA(cudaStreamWaitEvent(hs.side, hs.fork, 0));
     auto* hk = ts == 16 ? blend_hot_k<16> : blend_hot_k<32>;
@@ -1386,6 +1403,11 @@ int32_t tiles_and_blend(int width, int height, const uint32_t* vals, const Rende
                         w.radix_ws, s);
   if (st) return st;
   const uint32_t* tv = alt ? w.tv1 : w.tv0;
+  if (hot_path(exact, nb)) {
+    VMS_CUDA(launch(hot_list_k, 1, 1024, 0, s, (const uint32_t*)w.ranges, n_tiles, hot_len(),
+                    (const RenderCounters*)w.ctr, w.hot, w.tile_hot));
+    mark("hot_list", s);
+  }
   record(events, 2, external, s);
   if (bands < 0) return VMS_OK;  // the caller launches the bands
   if (tv != sorted_tiles(w, n_tiles)) {
