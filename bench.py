@@ -11,8 +11,9 @@ page uploads (pinned host -> HBM) -> preprocess -> sorts -> blend.
          part of every step (the scene lives in host memory by design).
   e2e    frames/s with every frame delivered to host memory through the
          public API: the benchmark harness (harness.run_benchmark, pipelined:
-         frame i + 1 is submitted before frame i is handed to the sink, so each
-         frame's PCIe transfer overlaps the next frame's render; host wall
+         the session's three frame slots stay full - frame i goes to the sink
+         once frame i + 3 is submitted - so each frame's PCIe transfer
+         overlaps the next frames' renders; host wall
          clock, device synchronised on both sides).  e2e_sync: one synchronous
          render_frame(out=<page-locked numpy>) per step (also the N > 1 e2e).
 
@@ -473,7 +474,7 @@ def run_ours(args, rank, world, local_rank):
     fresh_session()
     ms_e2e, stats_e2e = timed(pinned.numpy())
     # e2e through the benchmark harness (harness.run_benchmark, pipelined:
-    # frame i + 1 is submitted before frame i is handed to the sink, each a
+    # frames i + 1 .. i + 3 are submitted before frame i goes to the sink, each a
     # fresh page-locked array written by the blend) - single-GPU line only
     e2e_pipe = None
     traj_fps = None
@@ -481,7 +482,7 @@ def run_ours(args, rank, world, local_rank):
         from paper_2506_19415_b200 import harness
 
         # warm-up frames through the same pipelined path (this also sizes the
-        # session's pool of page-locked output arrays: two in flight)
+        # session's pool of page-locked output arrays: slots + 2 of them)
         sess = new_session()
         harness.run_benchmark(scene, traj, frames=range(args.warmup), session=sess,
                               pipelined=True)
