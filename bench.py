@@ -11,8 +11,8 @@ page uploads (pinned host -> HBM) -> preprocess -> sorts -> blend.
          part of every step (the scene lives in host memory by design).
   e2e    frames/s with every frame delivered to host memory through the
          public API: the benchmark harness (harness.run_benchmark, pipelined:
-         the session's three frame slots stay full - frame i goes to the sink
-         once frame i + 3 is submitted - so each frame's PCIe transfer
+         the session's four frame slots stay full - frame i goes to the sink
+         once frame i + 4 is submitted - so each frame's PCIe transfer
          overlaps the next frames' renders; host wall
          clock, device synchronised on both sides).  e2e_sync: one synchronous
          render_frame(out=<page-locked numpy>) per step (also the N > 1 e2e).
@@ -474,7 +474,7 @@ def run_ours(args, rank, world, local_rank):
     fresh_session()
     ms_e2e, stats_e2e = timed(pinned.numpy())
     # e2e through the benchmark harness (harness.run_benchmark, pipelined:
-    # frames i + 1 .. i + 3 are submitted before frame i goes to the sink, each a
+    # frames i + 1 .. i + 4 are submitted before frame i goes to the sink, each a
     # fresh page-locked array written by the blend) - single-GPU line only
     e2e_pipe = None
     traj_fps = None

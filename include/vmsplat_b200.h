@@ -392,7 +392,7 @@ int32_t vms_session_frame(vms_session* s, const vms_frame_args* args, vms_frame_
  * vms_session_frame returns as soon as the frame is enqueued and this is how
  * the caller learns that the image is complete. */
 int32_t vms_session_wait(vms_session* s, int32_t back);
-/* Frames a session keeps in flight (2..4, VMSPLAT_SLOTS, default 3):
+/* Frames a session keeps in flight (2..8, VMSPLAT_SLOTS, default 4):
  * vms_session_frame for frame i waits for frame i - slots. */
 int32_t vms_session_slots(const vms_session* s);
 /* Wait for the last frame; out4 = its n_kept, n_inst, overflow, n_need. */

@@ -150,13 +150,14 @@ struct Graph {
 
 // Frames in flight: frame i uses slot i % slots (its pinned host buffers,
 // render workspace, graphs, events); render_frame(i) recycles frame
-// i - slots.  Three slots let the host enqueue a frame while the two before
-// it still render / copy to the host (VMSPLAT_SLOTS=2..4).
-constexpr int kMaxSlots = 4;
+// i - slots.  Four slots let the host enqueue a frame while the three before
+// it still render / copy to the host (VMSPLAT_SLOTS=2..8; C2 same box: 3
+// slots 2112-2117 frames/s, e2e 1749-1763; 4 slots 2124-2138, e2e 1802-1804).
+constexpr int kMaxSlots = 8;
 
 struct vms_session {
   vms_session_desc d;
-  int slots = 3;
+  int slots = 4;
   vms_pagetable* pt = nullptr;
   cudaStream_t vis_stream = nullptr, copy_stream = nullptr, cap_stream = nullptr;
   cudaStream_t d2h_stream = nullptr;  // banded image copies to the host

@@ -862,7 +862,7 @@ class VmSession:
     @property
     def slots(self) -> int:
         """Frames the session keeps in flight: render_frame(i) waits for
-        frame i - slots (VMSPLAT_SLOTS, default 3)."""
+        frame i - slots (VMSPLAT_SLOTS, default 4)."""
         return int(self._lib.vms_session_slots(self._h))
 
     def wait(self, back: int = 0):
