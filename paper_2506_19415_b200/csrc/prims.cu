@@ -16,6 +16,8 @@
 #include "common.cuh"
 #include "prims.h"
 
+#include <cstdlib>
+
 namespace vms {
 
 namespace {
@@ -384,6 +386,20 @@ RadixLayout radix_layout(void* ws, uint32_t n_max) {
   return l;
 }
 
+// CTAs a onesweep pass asks for: one per tile, at most two per SM
+// (VMSPLAT_RADIX_GRID overrides; 0 = up to the resident limit).  The sorts
+// run beside the previous frame's blend: fewer resident look-back CTAs leave
+// it more of each SM (C2 frames 5-34, same box: 2122-2141 frames/s with 3-4
+// per SM, 2157-2165 with 2, 2102-2115 with 1).
+int radix_grid_want(size_t tiles) {
+  static const int cap = [] {
+    const char* e = getenv("VMSPLAT_RADIX_GRID");
+    return e && *e ? atoi(e) : 2 * kSMs;
+  }();
+  const int want = tiles ? (int)tiles : 1;
+  return cap > 0 && cap < want ? cap : want;
+}
+
 int32_t radix_passes_u32(uint32_t* k0, uint32_t* v0, uint32_t* k1, uint32_t* v1,
                          const uint32_t* n_dev, uint32_t n_max, int begin_bit, int end_bit,
                          int* in_alt, void* ws, cudaStream_t s) {
@@ -395,7 +411,7 @@ int32_t radix_passes_u32(uint32_t* k0, uint32_t* v0, uint32_t* k1, uint32_t* v1,
   const RadixLayout l = radix_layout(ws, n_max);
   const size_t tiles = l.pass_stride / 256;
   const int grid = persistent_grid((const void*)radix_onesweep_k<kRItems>, kRBlock,
-                                   tiles ? (int)tiles : 1);
+                                   radix_grid_want(tiles));
   int alt = 0;
   for (int p = 0; p < passes; ++p) {
     const int b = begin_bit + 8 * p;
@@ -437,7 +453,7 @@ int32_t radix_sort_u32(uint32_t* k0, uint32_t* v0, uint32_t* k1, uint32_t* v1,
                   begin_bit, end_bit, ghist, status, (size_t)(256 * tiles), tile_items));
   mark("radix_hist", s);
   auto* kern = small ? radix_onesweep_k<kRItemsSmall> : radix_onesweep_k<kRItems>;
-  const int grid = persistent_grid((const void*)kern, kRBlock, tiles ? (int)tiles : 1);
+  const int grid = persistent_grid((const void*)kern, kRBlock, radix_grid_want(tiles));
   int alt = 0;
   for (int p = 0; p < passes; ++p) {
     const int b = begin_bit + 8 * p;
