@@ -1,7 +1,4 @@
 # Final capture, last code of round 2 (4 slots, radix grid cap): suite, smoke, both arms, launch list, C3/4K/C4 (WITH_SAN / WITH_FULL add sanitizers / ncu full captures)
-# lists): sanitizers on the new code, the GPU suite, smoke(), both bench
-# arms, the ncu launch list of the bench command, ncu --set full of frame 12
-# (all kernels) and of the frame-25 blend, stage times, C3 / 4K / C4 lines.
 O=gpurun_out/r2/final3; mkdir -p $O/sanitize
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv,noheader
 CS="compute-sanitizer --print-limit 50 --error-exitcode 9"

@@ -150,11 +150,15 @@ def test_run_benchmark_c1_matches_reference_stats(cuda, tmp_path):
 
 
 @pytest.mark.gpu
-def test_pipelined_harness_frames_identical(cuda):
-    """run_benchmark(pipelined=True) (frame i + 1 submitted before frame i is
-    handed to the sink, host images written asynchronously) delivers the
-    same frames, in order, and the same counters as the synchronous run."""
+@pytest.mark.parametrize("slots", ["2", "4", "8"])
+def test_pipelined_harness_frames_identical(cuda, monkeypatch, slots):
+    """run_benchmark(pipelined=True) (the session's frame slots kept full,
+    host images written asynchronously) delivers the same frames, in order,
+    and the same counters as the synchronous run - with 2, 4 (the default)
+    and 8 frames in flight (VMSPLAT_SLOTS)."""
     from paper_2506_19415_b200 import scenegen
+
+    monkeypatch.setenv("VMSPLAT_SLOTS", slots)
 
     lay = scenegen.CityLayout(n_pages=40, page_size=256, levels=3, seed=5, scale=0.12)
     sc = scenegen.city_scene(lay)
@@ -171,11 +175,12 @@ def test_pipelined_harness_frames_identical(cuda):
            [(f.required, f.missing, f.bytes_copied, f.resident_per_level) for f in sb]
 
 
-def test_pipelined_delivery_order_without_gpu():
+@pytest.mark.parametrize("slots", [2, 3, 4])
+def test_pipelined_delivery_order_without_gpu(slots):
     """harness.run_benchmark(pipelined=True) against a stand-in session that
-    models the real one's two-deep recycling: frame i - 2 is complete once
-    frame i has been submitted.  Every frame reaches the sink exactly once, in
-    order, and only when complete."""
+    models the real one's recycling with `slots` frames in flight: frame
+    i - slots is complete once frame i has been submitted.  Every frame
+    reaches the sink exactly once, in order, and only when complete."""
 
     class Paged:
         page_count = 1
@@ -188,21 +193,23 @@ def test_pipelined_delivery_order_without_gpu():
         def __init__(self):
             self.submitted = []
             self.done = set()
+            self.slots = slots
 
         def render_frame(self, cam, i, wait=True):
             assert not wait
             self.submitted.append(i)
-            if len(self.submitted) >= 3:
-                self.done.add(self.submitted[-3])  # recycled inside the call
+            if len(self.submitted) > slots:
+                self.done.add(self.submitted[-slots - 1])  # recycled inside the call
             st = {"required_pages": 1, "missing_pages": 0, "bytes_copied": 0, "usage": 0.5,
                   "resident_per_level": (1,), "thresholds": (1.0,)}
             st.update({f"time_{s}": 0.1 for s in harness.STAGES})
             return np.full((2, 2, 3), float(i), np.float32), st
 
         def wait(self, back):
+            assert 0 <= back < slots
             self.done.update(self.submitted[len(self.submitted) - 1 - back:])
 
-    for n in (1, 2, 3, 7):
+    for n in (1, 2, 3, 7, 12):
         sess, got = Session(), []
 
         def sink(i, im, sess=sess, got=got):
