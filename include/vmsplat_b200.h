@@ -395,6 +395,10 @@ int32_t vms_session_wait(vms_session* s, int32_t back);
 /* Frames a session keeps in flight (2..8, VMSPLAT_SLOTS, default 4):
  * vms_session_frame for frame i waits for frame i - slots. */
 int32_t vms_session_slots(const vms_session* s);
+/* Allocate the render workspaces of every frame slot for width x height now
+ * (a session otherwise allocates them at its first frame; nothing else
+ * changes - the page cache stays cold). */
+int32_t vms_session_prepare(vms_session* s, int32_t width, int32_t height);
 /* Wait for the last frame; out4 = its n_kept, n_inst, overflow, n_need. */
 int32_t vms_session_counters(vms_session* s, uint32_t* out4, void* stream);
 

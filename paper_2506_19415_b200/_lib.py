@@ -164,6 +164,7 @@ SIGNATURES = {
     "vms_session_counters": (I32, [P, P, P]),
     "vms_session_wait": (I32, [P, I32]),
     "vms_session_slots": (I32, [P]),
+    "vms_session_prepare": (I32, [P, I32, I32]),
     "vms_host_accessible": (I32, [P]),
     "vms_host_register": (I32, [P, ctypes.c_uint64, I32, ctypes.POINTER(P)]),
     "vms_host_unregister": (I32, [P]),

@@ -645,6 +645,14 @@ int32_t vms_session_cert_count(vms_session* s, uint32_t* out) {
   return debug_cert_count(ws_of(s, s->last_par < 0 ? 0 : s->last_par), out);
 }
 
+int32_t vms_session_prepare(vms_session* s, int32_t width, int32_t height) {
+  if (!s || width < 1 || height < 1) {
+    set_error("session_prepare: invalid arguments");
+    return VMS_ERR_INVALID;
+  }
+  return ensure_ws(s, width, height, s->m_cap > s->m_want ? s->m_cap : s->m_want);
+}
+
 int32_t vms_session_set_render_ws(vms_session* s, void* ws, uint64_t bytes, uint32_t m_cap,
                                   int32_t width, int32_t height) {
   // the session owns its scratch; this only raises the instance capacity
@@ -805,8 +813,12 @@ int32_t vms_session_frame(vms_session* s, const vms_frame_args* a, vms_frame_sta
   out->host_update_s =
       std::chrono::duration<double>(std::chrono::steady_clock::now() - h0).count();
   // uploads into staging on the copy stream (overlap the renders in flight)
+  // the most a plan can move: the budget in level-0 pages, plus the page that
+  // crosses it (update_page_table's break-on-budget)
+  const size_t budget_bytes =
+      (size_t)(std::ceil(std::max(0.0, (double)a->budget)) + 1.0) * s->d.page_size * rb;
   if (n_plan) {
-    rc = ensure_staging(s, bytes);
+    rc = ensure_staging(s, std::max<size_t>(bytes, budget_bytes));
     if (rc) return rc;
     VMS_CUDA(cudaStreamWaitEvent(s->copy_stream, s->ev_staging, 0));  // staging reuse
     if (timing) VMS_CUDA(cudaEventRecord(s->tev[2], s->copy_stream));
@@ -817,7 +829,9 @@ int32_t vms_session_frame(vms_session* s, const vms_frame_args* a, vms_frame_sta
       if (s->bounce_bytes[par] < bytes) {
         if (s->bounce[par]) VMS_CUDA(cudaFreeHost(s->bounce[par]));
         s->bounce[par] = nullptr;
-        const size_t want = bytes + bytes / 4;
+        // page-locking is slow and synchronising: size each slot's buffer
+        // once for the largest plan the staging budget allows
+        const size_t want = std::max<size_t>(bytes + bytes / 4, budget_bytes);
         VMS_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&s->bounce[par]), want,
                                cudaHostAllocPortable));
         s->bounce_bytes[par] = want;

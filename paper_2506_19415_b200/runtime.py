@@ -865,6 +865,12 @@ class VmSession:
         frame i - slots (VMSPLAT_SLOTS, default 4)."""
         return int(self._lib.vms_session_slots(self._h))
 
+    def prepare(self, camera) -> None:
+        """Allocate the render workspaces for the camera's resolution now
+        (otherwise the first frame does it); the page cache stays cold."""
+        _lib.check(self._lib.vms_session_prepare(self._h, int(camera.width), int(camera.height)),
+                   "prepare")
+
     def wait(self, back: int = 0):
         """Block until the last submitted frame (back=0) or one before it
         (back < slots) is complete - for ``render_frame(..., wait=False)``."""
