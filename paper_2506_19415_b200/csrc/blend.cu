@@ -707,7 +707,6 @@ __global__ void __launch_bounds__(kBlendThreads, kSparse ? 3 : 4) blend_k(const 
                 const Staged& q1 = grp[j1];
                 const double s0 = sig(q0), s1 = sig(q1);
                 const bool l0 = s0 >= q0.skip, l1 = two && s1 >= q1.skip;
-                if (g_lane_lists == 3 && !__any_sync(__activemask(), l0 || l1)) continue;
                 double w0 = __dmul_rn(q0.al, exp_tab<8>(l0 ? s0 : 0.0, tabl));
                 double w1 = __dmul_rn(q1.al, exp_tab<8>(l1 ? s1 : 0.0, tabl));
                 if (w0 > kBlendC[8]) w0 = kBlendC[8];
