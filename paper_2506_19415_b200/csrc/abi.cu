@@ -404,7 +404,10 @@ int32_t vms_upload_pages(const vms_copy* copies, int64_t n, const void* host_bas
     return VMS_OK;
   }
   mark("begin", s);
-  int vec16 = 1;
+  // 16-byte vector copies only when the bases are aligned too: a scene
+  // registered in place is the file mapping plus the header, not 16-aligned
+  int vec16 = ((reinterpret_cast<uintptr_t>(host_base) | reinterpret_cast<uintptr_t>(dev_base)) &
+               15u) == 0;
   for (int64_t i = 0; i < n; ++i)
     vec16 &= ((copies[i].src_offset | copies[i].dst_offset | copies[i].nbytes) & 15u) == 0;
   dim3 grid(64, (unsigned)(n < 65535 ? n : 65535));

@@ -25,7 +25,8 @@ fps = []
 reps = int(os.environ.get("AB_REPS", "5"))
 for rep in range(reps):
     t_a = time.perf_counter()
-    s = VmSession(scene, buffer_pages=500, staging_pages=40, vis_scale=0.25, timing=False)
+    s = VmSession(scene, buffer_pages=500, staging_pages=40, vis_scale=0.25, timing=False,
+                  upload_mode=int(os.environ["AB_UPLOAD"]) if os.environ.get("AB_UPLOAD") else None)
     t_b = time.perf_counter()
     harness.run_benchmark(scene, traj, frames=range(5), session=s, pipelined=True)
     torch.cuda.synchronize()

@@ -23,7 +23,8 @@ traj = bench.trajectory(A, lay)
 lo, hi = int(os.environ.get("AB_FROM", "5")), int(os.environ.get("AB_TO", "65"))
 fps = []
 for rep in range(int(os.environ.get("AB_REPS", "5"))):
-    s = VmSession(scene, buffer_pages=500, staging_pages=40, vis_scale=0.25, timing=False)
+    s = VmSession(scene, buffer_pages=500, staging_pages=40, vis_scale=0.25, timing=False,
+                  upload_mode=int(os.environ["AB_UPLOAD"]) if os.environ.get("AB_UPLOAD") else None)
     for f in range(lo):
         s.render_frame(traj.frame_camera(f), f, out="device")
     torch.cuda.synchronize()
